@@ -1,0 +1,375 @@
+"""bench.py — time-to-R / join rows per second of the Figaro two-table path on B200.
+
+Workload (BASELINE.json configs[3], the north-star config): uniform Cartesian
+join of A (1e8 x 64) and B (1e8 x 64) fp64, i.e. 1e16 join rows, 128 columns;
+synthetic SplitMix64 data generated on the device (no datasets).  A "step" is
+one figaro_r (grouping-free for a Cartesian product): head/tail prefix pass over
+B, fused Claim-1 assembly + TSQR leaves, TSQR tree, canonical R.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
+
+N > 1 is launched by torchrun, one rank per GPU (NCCL): each rank generates its
+row shard of A and B in place, exchanges the B column sums (carry all-gather),
+computes its local R and all-gathers the R factors, then every rank runs the
+same TSQR tree (`jq_tsqr_stack`).  Strong scaling: the join is fixed.
+
+Timing: W >= 3 untimed steps, then K steps on the device stream with CUDA
+events, barrier + synchronize on both sides, max over ranks.  Inputs (102.4 GB)
+exceed the 126 MB L2, so no explicit flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.13   # measured DMMA (mma.sync f64) peak on this pool, profiles/r01_fp64_peak.txt
+CONFIGS = {
+    1: dict(m=1000, n=4, keys=None, name="C1 cartesian 1000x4 |x| 1000x4"),
+    2: dict(m=1_000_000, n=16, keys="groups", key_groups=10_000, name="C2 natural join 10k keys x 100 rows/side, 16+16"),
+    3: dict(m=10_000_000, n=32, keys="zipf", name="C3 Zipf(1.1) keys, 1e7 rows/side, 32+32"),
+    4: dict(m=100_000_000, n=64, keys=None, name="C4 uniform cartesian 1e8 x 64 |x| 1e8 x 64"),
+    5: dict(m=1_000_000, n=128, keys=None, want_v=True, name="C5 full SVD cartesian 1e6 x 128 |x| 1e6 x 128"),
+}
+METRIC = "join rows/sec (m1*m2/t), time-to-R"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, cfg_id: int):
+    """The reference's CPU path: the oracle port of SPEC.md (numpy / LAPACK, all host
+    threads) on a bounded sample of the same workload, extrapolated linearly in
+    m1 + m2 (the Figaro CPU cost is O((m1+m2) N^2))."""
+    import oracle as O
+    cfg = CONFIGS[cfg_id]
+    m_full = cfg["m"]
+    m_s = min(m_full, args.ref_rows)
+    a, b = O.config_tables(cfg_id, rows=m_s)
+    join_full = float(m_full) * float(m_full) if cfg["keys"] is None else None
+    if join_full is None:
+        ag, bg = O.config_tables(cfg_id)
+        _, _, ac, _, bc, _ = O.group_keys(ag.keys, bg.keys)
+        join_full = float(np.sum(ac.astype(np.float64) * bc))
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if cfg.get("want_v"):
+            O.figaro_svd(a, b, want_vectors=True, lapack=True)
+        else:
+            O.figaro_r(a, b, lapack=True)
+        t = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(t)
+    t_sample = float(np.mean(times))
+    t_full = t_sample * (2.0 * m_full) / (2.0 * m_s)
+    value = join_full / t_full
+    cores = len(os.sched_getaffinity(0))
+    return {"value": value, "unit": "join rows/s", "cores": cores, "kind": "port",
+            "sample": f"{cfg['name']} with m1=m2={m_s} rows (same SplitMix64 recipe), full SPEC "
+                      f"pipeline reduce->LAPACK Householder QR->canonicalize, mean of {args.steps} after "
+                      f"{args.warmup} warm-up = {t_sample:.3f} s, extrapolated x{m_full / m_s:.0f} linearly "
+                      f"in m1+m2 to {t_full:.1f} s for the full config",
+            "ms_per_step_sample": t_sample * 1e3, "ms_per_step_full_extrapolated": t_full * 1e3}
+
+
+# ---------------------------------------------------------------- our arm
+def make_inputs(cfg_id, rank, world, device):
+    import torch
+    from paper_2503_23385_b200 import datagen
+    cfg = CONFIGS[cfg_id]
+    m, n = cfg["m"], cfg["n"]
+    a0, a1 = m * rank // world, m * (rank + 1) // world
+    A = torch.empty((a1 - a0, n), dtype=torch.float64, device=device)
+    B = torch.empty((a1 - a0, n), dtype=torch.float64, device=device)
+    datagen.uniform(1000 * cfg_id + 1, a1 - a0, n, row0=a0, out=A)
+    datagen.uniform(1000 * cfg_id + 2, a1 - a0, n, row0=a0, out=B)
+    ka = kb = None
+    if cfg["keys"] == "groups":
+        ka = torch.from_numpy(datagen.near_equal_keys(m, cfg["key_groups"])).to(device)
+        kb = ka.clone()
+    elif cfg["keys"] == "zipf":
+        ka = torch.from_numpy(datagen.zipf_sorted_keys(1000 * cfg_id + 3, m)).to(device)
+        kb = torch.from_numpy(datagen.zipf_sorted_keys(1000 * cfg_id + 4, m)).to(device)
+    torch.cuda.synchronize()
+    return A, B, ka, kb, a0
+
+
+def join_rows(cfg_id, ka, kb):
+    cfg = CONFIGS[cfg_id]
+    if ka is None:
+        return float(cfg["m"]) ** 2
+    from paper_2503_23385_b200 import group_keys
+    g = group_keys(ka, kb)
+    return float(np.sum(g[2].astype(np.float64) * g[4]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-rows", type=int, default=1_000_000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+        cb = run_reference(args, args.config)
+        line = {"metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": cb["ms_per_step_full_extrapolated"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "impl": "reference",
+                "config": {"workload": cfg["name"], "sample_rows_per_side": min(cfg["m"], args.ref_rows)},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2503_23385_b200 import _native as N
+    import paper_2503_23385_b200 as P
+
+    torch.cuda.set_device(local)
+    N.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    A, B, ka, kb, a0 = make_inputs(args.config, rank, world, device)
+    m, n = cfg["m"], cfg["n"]
+    nn = 2 * n
+    jrows = join_rows(args.config, ka, kb) if world == 1 else float(m) ** 2
+    lib, ctx = N.lib(), N.ctx()
+    stream = torch.cuda.current_stream()
+
+    r_out = torch.empty((nn, nn), dtype=torch.float64, device=device)
+    if world > 1:
+        if cfg["keys"] is not None:
+            raise SystemExit("multi-GPU bench covers the Cartesian configs (1, 4, 5)")
+        sums = torch.empty(n, dtype=torch.float64, device=device)
+        all_sums = torch.empty((world, n), dtype=torch.float64, device=device)
+        r_loc = torch.empty((nn, nn), dtype=torch.float64, device=device)
+        r_all = torch.empty((world, nn, nn), dtype=torch.float64, device=device)
+
+    def step():
+        N.use_torch_stream(A)
+        if world == 1:
+            if cfg.get("want_v"):
+                res = P.figaro_svd(P.Table(A, ka), P.Table(B, kb), want_vectors=True)
+                return res.values
+            return P.figaro_r(P.Table(A, ka), P.Table(B, kb))
+        rows = A.shape[0]
+        N.check(lib.jq_colsums(ctx, N.ptr(B), rows, n, N.ptr(sums)))
+        dist.all_gather_into_tensor(all_sums, sums)                 # carry exchange (NCCL)
+        prefix = all_sums[:rank].sum(0) if rank else torch.zeros(n, dtype=torch.float64, device=device)
+        total = all_sums.sum(0)
+        N.check(lib.jq_figaro_r_shard(ctx, N.ptr(A), rows, n, m, N.ptr(B), rows, n, m, a0,
+                                      N.ptr(prefix.contiguous()), N.ptr(total.contiguous()), N.ptr(r_loc)))
+        dist.all_gather_into_tensor(r_all, r_loc)                   # R all-gather (NCCL)
+        N.check(lib.jq_tsqr_stack(ctx, N.ptr(r_all), world, nn, N.ptr(r_out)))
+        return r_out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    launches0 = N.kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stage = []
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+        if world == 1:
+            stage.append(N.last_timing())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = N.kernel_launches() - launches0
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = jrows / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (TSQR leaves, FP64 tensor pipe)
+    roof, roof_hbm, stage_avg = None, None, None
+    if stage:
+        stage_avg = {k: float(np.mean([s[k] for s in stage])) for k in ("group_ms", "scan_ms", "tsqr_ms", "tree_ms", "svd_ms", "total_ms")}
+        M = float(stage[0]["reduced_rows"])
+        m_red = (m + m - 1) if cfg["keys"] is None else M
+        flops = 2.0 * m_red * nn * nn - 2.0 / 3.0 * nn ** 3
+        achieved = flops / (stage_avg["tsqr_ms"] / 1e3) / 1e12
+        roof = {"kernel": "tsqr_kernel (fused Claim-1 assembly + Householder TSQR leaves)",
+                "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 figure",
+                "algorithmic": f"2*M*N^2 - 2/3*N^3 with M={int(m_red)}, N={nn}",
+                "share_of_step": stage_avg["tsqr_ms"] / ms}
+        pk = peaks()
+        gbs = (8.0 * m * n) / (stage_avg["scan_ms"] / 1e3) / 1e9 if stage_avg["scan_ms"] > 0 else None
+        if gbs:
+            roof_hbm = {"kernel": "segscan (head/tail prefix pass over B)", "bound": "hbm", "achieved": gbs,
+                        "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                        "algorithmic": f"8*m2*n2 = {8 * m * n} bytes read"}
+
+    # ---- end-to-end through the public API with host buffers (rank 0 view, N=1)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        e2e = run_e2e(args, cfg, A, B, ka, kb, jrows)
+        A = B = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        del A, B
+        torch.cuda.empty_cache()
+        try:
+            ra = argparse.Namespace(**vars(args))
+            ra.steps, ra.warmup = 2, 1
+            cb = run_reference(ra, args.config)
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # reported, never fatal for the GPU line
+            cpu = {"value": None, "unit": "join rows/s", "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "join rows/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "time_to_r_ms": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (SplitMix64 uniform(0,1), generated on device)",
+                "config": {"workload": cfg["name"], "m1": m, "m2": m, "n1": n, "n2": n,
+                           "join_rows": jrows, "parallelism": f"rows{world}",
+                           "l2": "inputs 16*m*n bytes >> 126 MB L2 (no flush needed)" if m * n * 16 > 2**28 else "small config: L2-resident"},
+                "gpu_launches": launches, "clocks": clk, "roofline": roof, "roofline_hbm": roof_hbm,
+                "stages_ms": stage_avg, "step_ms_all": step_ms, "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, cfg, A, B, ka, kb, jrows):
+    """figaro_r(Table(host), Table(host)): H2D of both tables from pinned host memory
+    and the D2H of R inside the timed region, every step."""
+    import torch
+    import paper_2503_23385_b200 as P
+    host = {}
+    cudart = torch.cuda.cudart()
+    try:
+        for name, t in (("A", A), ("B", B)):
+            h = np.empty(tuple(t.shape), dtype=np.float64)
+            rc = cudart.cudaHostRegister(h.ctypes.data, h.nbytes, 0)
+            pinned = int(rc) == 0 if not hasattr(rc, "value") else rc.value == 0
+            torch.cuda.synchronize()
+            torch.from_numpy(h).copy_(t)      # D2H once (outside timing)
+            host[name] = (h, pinned)
+        hka = ka.cpu().numpy() if ka is not None else None
+        hkb = kb.cpu().numpy() if kb is not None else None
+        del A, B
+        torch.cuda.empty_cache()
+        ta, tb = P.Table(host["A"][0], hka), P.Table(host["B"][0], hkb)
+        nsteps = max(1, min(args.steps, 3))
+        P.figaro_r(ta, tb)                     # warm-up (workspace sizing)
+        times = []
+        for _ in range(nsteps):
+            t0 = time.perf_counter()
+            r = P.figaro_r(ta, tb)              # returns after the D2H of R
+            times.append(time.perf_counter() - t0)
+        t = float(np.mean(times))
+        h2d = sum(h.nbytes for h, _ in host.values()) + (hka.nbytes + hkb.nbytes if hka is not None else 0)
+        return {"value": jrows / t, "unit": "join rows/s", "ms_per_step": t * 1e3, "steps": nsteps,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(r.nbytes),
+                "pinned": all(p for _, p in host.values()),
+                "api": "paper_2503_23385_b200.figaro_r(Table(numpy), Table(numpy)) -> jq_figaro_r"}
+    finally:
+        for h, pinned in host.values():
+            if pinned:
+                cudart.cudaHostUnregister(h.ctypes.data)
+
+
+if __name__ == "__main__":
+    main()

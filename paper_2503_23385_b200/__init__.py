@@ -1,0 +1,82 @@
+"""paper_2503_23385_b200 — B200-native Figaro two-table QR / SVD (arXiv 2503.23385).
+
+Drop-in mirror of the reference package `joinqr` for its hot path: the same
+public names, argument layout, return types and error behaviour
+(pkg/src/joinqr/__init__.py:20-77, SPEC.md), resolved lazily like the
+reference (`__getattr__`, :65-73).  Every compute call goes through the C ABI
+of libjoinqr.so (include/joinqr.h) to hand-written sm_100a kernels; there is
+no CPU fallback.  Names of the reference that are not on the hot path
+(CSV IO, CLI/bench harness, brute-force oracle, Givens cross-check) raise an
+AttributeError that says so ("Out of scope").
+"""
+
+import importlib
+
+__version__ = "0.1.0"
+
+_EXPORTS = {
+    "as_matrix": ".matrix",
+    "matmul": ".matrix",
+    "gram": ".matrix",
+    "max_abs_diff": ".matrix",
+    "transpose": ".matrix",
+    "frobenius_norm": ".matrix",
+    "hconcat": ".matrix",
+    "vconcat": ".matrix",
+    "scale": ".matrix",
+    "row_slice": ".matrix",
+    "is_upper_triangular": ".matrix",
+    "head": ".headtail",
+    "tail": ".headtail",
+    "head_tail": ".headtail",
+    "Table": ".joins",
+    "ReducedMatrix": ".joins",
+    "reduce_cartesian": ".joins",
+    "reduce_natural_join": ".joins",
+    "reduce_join": ".joins",
+    "group_keys": ".joins",
+    "householder_r": ".qr",
+    "canonicalize": ".qr",
+    "figaro_r": ".qr",
+    "SvdResult": ".svd",
+    "svd_of_r": ".svd",
+    "figaro_svd": ".svd",
+    "GenSpec": ".datagen",
+    "gen_uniform": ".datagen",
+    "set_device": "._native",
+    "last_timing": "._native",
+}
+
+_OUT_OF_SCOPE = {
+    "givens_r": "cross-validation reference only (SPEC.md:299)",
+    "materialize_cartesian": "brute-force oracle (CPU checker lives in oracle/)",
+    "materialize_natural_join": "brute-force oracle (CPU checker lives in oracle/)",
+    "baseline_r": "brute-force oracle (CPU checker lives in oracle/)",
+    "baseline_svd": "brute-force oracle (CPU checker lives in oracle/)",
+    "det_lu": "oracle plumbing (CPU checker lives in oracle/)",
+    "read_table": "CSV IO is excluded from the timed path (SPEC.md:532)",
+    "read_matrix": "CSV IO is excluded from the timed path (SPEC.md:532)",
+    "write_matrix": "CSV IO is excluded from the timed path (SPEC.md:532)",
+    "write_table": "CSV IO is excluded from the timed path (SPEC.md:532)",
+    "write_svd": "CSV IO is excluded from the timed path (SPEC.md:532)",
+    "BenchCell": "bench harness: use bench.py",
+    "BenchReport": "bench harness: use bench.py",
+    "run_bench": "bench harness: use bench.py",
+    "track_peak_memory": "bench harness: use bench.py",
+}
+
+
+def __getattr__(name):
+    if name in _OUT_OF_SCOPE:
+        raise AttributeError(f"{name} is not part of the B200 hot path: {_OUT_OF_SCOPE[name]}")
+    try:
+        module_name = _EXPORTS[name]
+    except KeyError:
+        raise AttributeError(f"module {__name__!r} has no attribute {name!r}") from None
+    value = getattr(importlib.import_module(module_name, __name__), name)
+    globals()[name] = value
+    return value
+
+
+def __dir__():
+    return sorted(set(globals()) | set(_EXPORTS))

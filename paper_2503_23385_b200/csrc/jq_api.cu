@@ -1,0 +1,354 @@
+// jq_api.cu — context, error plumbing, workspace and the figaro_r / figaro_svd
+// orchestration of libjoinqr.so (include/joinqr.h).
+//
+// figaro_r on the device, no host round trip between stages:
+//   [keys]  group_keys_dev        bit-exact grouping (jq_group.cu)
+//           segscan_dev(B)        head/tail prefix carries + group heads (jq_headtail.cu)
+//           figaro_tsqr_dev       fused Claim-1 assembly + TSQR leaves + tree (jq_tsqr.cu)
+//           -> canonical R, exact zeros below the diagonal.
+// Validation flags (unsorted keys, Jacobi non-convergence) are raised on the
+// device and read once at the end of the call.
+#include <cstring>
+#include <string>
+
+#include "jq_internal.cuh"
+
+namespace jq {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+int ws_reserve(jq_ctx* ctx, size_t bytes) {
+  bytes += 4096;
+  if (bytes <= ctx->ws.cap) return JQ_OK;
+  if (ctx->ws.base) {
+    JQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    JQ_CUDA(cudaFree(ctx->ws.base));
+    ctx->ws.base = nullptr;
+    ctx->ws.cap = 0;
+  }
+  size_t cap = bytes + bytes / 8;
+  cudaError_t e = cudaMalloc(&ctx->ws.base, cap);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->ws.base = nullptr;
+    return fail(JQ_E_OOM, "cannot allocate " + std::to_string(cap >> 20) + " MiB of device workspace");
+  }
+  ctx->ws.cap = cap;
+  return JQ_OK;
+}
+
+int begin_call(jq_ctx* ctx) {
+  JQ_CUDA(cudaSetDevice(ctx->device));
+  ws_reset(ctx);
+  JQ_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), ctx->stream));
+  return JQ_OK;
+}
+
+int sync_and_check_flags(jq_ctx* ctx) {
+  JQ_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  JQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int f = *ctx->h_flags;
+  if (f & FLAG_UNSORTED_A) return fail(JQ_E_UNSORTED, "left table keys are not sorted non-decreasing");
+  if (f & FLAG_UNSORTED_B) return fail(JQ_E_UNSORTED, "right table keys are not sorted non-decreasing");
+  if (f & FLAG_NOCONV) return fail(JQ_E_NOCONV, "Jacobi SVD did not converge in 64 sweeps");
+  return JQ_OK;
+}
+
+static float ev_ms(jq_ctx* ctx, int a, int b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.f;
+  }
+  return ms;
+}
+
+// Workspace needed by figaro_r_dev for these sizes (inputs already on device).
+static size_t figaro_ws(int64_t m1, int64_t n1, int64_t m2, int64_t n2, bool keyed, int sms) {
+  const int64_t cap = keyed ? std::max<int64_t>(1, std::min(m1, m2)) : 1;
+  return (keyed ? group_ws_bytes(m1, m2) : 0) + segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) +
+         figaro_tsqr_ws_bytes(m1, m2, n1 + n2, sms) + ws_bytes(size_t(n1 + n2) * (n1 + n2), 8);
+}
+
+// Device-resident figaro_r: R (n x n, canonical) into r_out (device).
+static int figaro_r_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
+                        const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
+  const bool keyed = ka != nullptr;
+  cudaEventRecord(ctx->ev[0], ctx->stream);
+  Groups gr;
+  if (keyed) JQ_TRY(group_keys_dev(ctx, ka, m1, kb, m2, &gr));
+  cudaEventRecord(ctx->ev[1], ctx->stream);
+  SegScan ss;
+  const int64_t cap = keyed ? gr.cap : 1;
+  if (n2 > 0)
+    JQ_TRY(segscan_dev(ctx, b, m2, n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
+                       keyed ? gr.b_count : nullptr, keyed ? gr.d_n : nullptr, cap, &ss));
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  FigaroArgs fa{};
+  fa.a = a; fa.m1 = m1; fa.n1 = n1;
+  fa.b = b; fa.m2 = m2; fa.n2 = n2;
+  fa.gid_a = keyed ? gr.gid_a : nullptr;
+  fa.gid_b = keyed ? gr.gid_b : nullptr;
+  fa.a_count = keyed ? gr.a_count : nullptr;
+  fa.b_count = keyed ? gr.b_count : nullptr;
+  fa.b_start = keyed ? gr.b_start : nullptr;
+  fa.b_totals = n2 > 0 ? ss.totals : nullptr;
+  fa.b_carry = n2 > 0 ? ss.carry : nullptr;
+  fa.b_prefix0 = nullptr;
+  fa.m1_global = m1; fa.m2_global = m2; fa.b_row0 = 0;
+  JQ_TRY(figaro_tsqr_dev(ctx, fa, r_out, true));
+  return JQ_OK;
+}
+
+static void record_timing(jq_ctx* ctx, bool svd) {
+  jq_timing& t = ctx->timing;
+  t.group_ms = ev_ms(ctx, 0, 1);
+  t.scan_ms = ev_ms(ctx, 1, 2);
+  t.tsqr_ms = ev_ms(ctx, 3, 4);
+  t.tree_ms = ev_ms(ctx, 4, 5);
+  t.svd_ms = svd ? ev_ms(ctx, 5, 6) : 0.0;
+  t.total_ms = ev_ms(ctx, 0, svd ? 6 : 5);
+}
+
+static int check_tables(int64_t m1, int64_t n1, const int64_t* ka, int64_t m2, int64_t n2, const int64_t* kb) {
+  if ((ka == nullptr) != (kb == nullptr)) return fail(JQ_E_KEYS, "both tables must carry keys, or neither");
+  if (m1 < 0 || m2 < 0 || n1 < 0 || n2 < 0) return fail(JQ_E_INVALID, "negative size");
+  if (n1 + n2 == 0) return fail(JQ_E_INVALID, "the join has no columns");
+  if (n1 > 256 || n2 > 256 || n1 + n2 > 256) return fail(JQ_E_INVALID, "n1 + n2 above 256 is not supported");
+  if (!ka && (m1 == 0 || m2 == 0)) return fail(JQ_E_INVALID, "reduce_cartesian needs non-empty inputs");
+  return JQ_OK;
+}
+
+}  // namespace jq
+
+using namespace jq;
+
+extern "C" {
+
+int jq_version(void) { return 100; }
+const char* jq_last_error(void) { return g_err.c_str(); }
+
+int jq_ctx_create(int device, jq_ctx** out) {
+  if (!out) return fail(JQ_E_INVALID, "null output pointer");
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(JQ_E_NODEV, "no CUDA device is visible (libjoinqr needs a B200 / sm_100a GPU)");
+  }
+  if (device < 0 || device >= count) return fail(JQ_E_NODEV, "device index out of range");
+  JQ_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  JQ_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(JQ_E_NODEV, std::string("libjoinqr is built for sm_100a; device is ") + prop.name);
+  jq_ctx* ctx = new jq_ctx();
+  ctx->device = device;
+  ctx->sms = prop.multiProcessorCount;
+  JQ_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  JQ_CUDA(cudaMalloc(&ctx->d_flags, sizeof(int)));
+  JQ_CUDA(cudaMallocHost(&ctx->h_flags, sizeof(int)));
+  for (auto& e : ctx->ev) JQ_CUDA(cudaEventCreate(&e));
+  *out = ctx;
+  return JQ_OK;
+}
+
+int jq_ctx_destroy(jq_ctx* ctx) {
+  if (!ctx) return JQ_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->ws.base) cudaFree(ctx->ws.base);
+  if (ctx->d_flags) cudaFree(ctx->d_flags);
+  if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+  for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return JQ_OK;
+}
+
+int jq_ctx_set_stream(jq_ctx* ctx, void* s) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  ctx->stream = s ? reinterpret_cast<cudaStream_t>(s) : ctx->own_stream;
+  return JQ_OK;
+}
+
+int jq_ctx_sync(jq_ctx* ctx) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  return JQ_OK;
+}
+
+int jq_ctx_set_variant(jq_ctx* ctx, int variant) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (variant != 0) return fail(JQ_E_INVALID, "only variant 0 (dense Claim-1 reduction) is built");
+  ctx->variant = variant;
+  return JQ_OK;
+}
+
+int jq_last_timing(jq_ctx* ctx, jq_timing* out) {
+  if (!ctx || !out) return fail(JQ_E_INVALID, "null argument");
+  *out = ctx->timing;
+  return JQ_OK;
+}
+
+int64_t jq_kernel_launches(jq_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int jq_canonicalize(jq_ctx* ctx, const double* r, int64_t n, double* out) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (n <= 0) return JQ_OK;
+  JQ_TRY(begin_call(ctx));
+  JQ_TRY(ws_reserve(ctx, stage_bytes(r, n * n) + stage_bytes((const double*)out, n * n)));
+  const double* dr;
+  double* dout;
+  JQ_TRY(stage_in(ctx, r, n * n, &dr));
+  JQ_TRY(stage_out(ctx, out, n * n, &dout));
+  JQ_TRY(canonicalize_dev(ctx, dr, n, dout));
+  JQ_TRY(copy_out(ctx, out, (const double*)dout, n * n));
+  return sync_and_check_flags(ctx);
+}
+
+int jq_householder_r(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, double* r) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (cols <= 0) return fail(JQ_E_INVALID, "householder_r needs at least one column");
+  if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
+  if (rows < 0) return fail(JQ_E_INVALID, "negative row count");
+  JQ_TRY(begin_call(ctx));
+  JQ_TRY(ws_reserve(ctx, stage_bytes(m, rows * cols) + stage_bytes((const double*)r, cols * cols) +
+                             tsqr_ws_bytes(rows, cols, ctx->sms)));
+  const double* dm;
+  double* dr;
+  JQ_TRY(stage_in(ctx, m, rows * cols, &dm));
+  JQ_TRY(stage_out(ctx, r, cols * cols, &dr));
+  JQ_TRY(tsqr_dense_dev(ctx, dm, rows, cols, dr, false));
+  JQ_TRY(copy_out(ctx, r, (const double*)dr, cols * cols));
+  return sync_and_check_flags(ctx);
+}
+
+int jq_figaro_r(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
+                const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_TRY(check_tables(m1, n1, ka, m2, n2, kb));
+  JQ_TRY(begin_call(ctx));
+  const int64_t n = n1 + n2;
+  JQ_TRY(ws_reserve(ctx, stage_bytes(a, m1 * n1) + stage_bytes(b, m2 * n2) + stage_bytes(ka, m1) +
+                             stage_bytes(kb, m2) + stage_bytes((const double*)r, n * n) +
+                             figaro_ws(m1, n1, m2, n2, ka != nullptr, ctx->sms)));
+  const double *da, *db;
+  const int64_t *dka, *dkb;
+  double* dr;
+  JQ_TRY(stage_in(ctx, a, m1 * n1, &da));
+  JQ_TRY(stage_in(ctx, b, m2 * n2, &db));
+  JQ_TRY(stage_in(ctx, ka, m1, &dka));
+  JQ_TRY(stage_in(ctx, kb, m2, &dkb));
+  JQ_TRY(stage_out(ctx, r, n * n, &dr));
+  JQ_TRY(figaro_r_dev(ctx, da, m1, n1, dka, db, m2, n2, dkb, dr));
+  JQ_TRY(copy_out(ctx, r, (const double*)dr, n * n));
+  int rc = sync_and_check_flags(ctx);
+  record_timing(ctx, false);
+  return rc;
+}
+
+int jq_figaro_svd(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
+                  const double* b, int64_t m2, int64_t n2, const int64_t* kb, int want_v,
+                  double* values, double* v, double* r) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_TRY(check_tables(m1, n1, ka, m2, n2, kb));
+  JQ_TRY(begin_call(ctx));
+  const int64_t n = n1 + n2;
+  JQ_TRY(ws_reserve(ctx, stage_bytes(a, m1 * n1) + stage_bytes(b, m2 * n2) + stage_bytes(ka, m1) +
+                             stage_bytes(kb, m2) + stage_bytes((const double*)values, n) +
+                             stage_bytes((const double*)v, n * n) + ws_bytes(n * n, 8) +
+                             figaro_ws(m1, n1, m2, n2, ka != nullptr, ctx->sms) + svd_ws_bytes(n)));
+  const double *da, *db;
+  const int64_t *dka, *dkb;
+  double *dval, *dv = nullptr;
+  JQ_TRY(stage_in(ctx, a, m1 * n1, &da));
+  JQ_TRY(stage_in(ctx, b, m2 * n2, &db));
+  JQ_TRY(stage_in(ctx, ka, m1, &dka));
+  JQ_TRY(stage_in(ctx, kb, m2, &dkb));
+  JQ_TRY(stage_out(ctx, values, n, &dval));
+  if (want_v) JQ_TRY(stage_out(ctx, v, n * n, &dv));
+  double* dr = ws_alloc<double>(ctx, n * n);
+  JQ_TRY(figaro_r_dev(ctx, da, m1, n1, dka, db, m2, n2, dkb, dr));
+  JQ_TRY(svd_dev(ctx, dr, n, want_v, dval, dv));
+  cudaEventRecord(ctx->ev[6], ctx->stream);
+  JQ_TRY(copy_out(ctx, values, (const double*)dval, n));
+  if (want_v) JQ_TRY(copy_out(ctx, v, (const double*)dv, n * n));
+  if (r) JQ_TRY(copy_out(ctx, r, (const double*)dr, n * n));
+  int rc = sync_and_check_flags(ctx);
+  record_timing(ctx, true);
+  return rc;
+}
+
+int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1,
+                      const double* b, int64_t b_rows, int64_t n2, int64_t m2, int64_t b_row0,
+                      const double* b_prefix, const double* b_total, double* r_local) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (a_rows < 0 || b_rows < 0 || n1 < 0 || n2 < 0 || n1 + n2 == 0 || n1 + n2 > 256)
+    return fail(JQ_E_INVALID, "bad shard geometry");
+  if (m1 <= 0 || m2 <= 0 || b_row0 < 0 || b_row0 + b_rows > m2)
+    return fail(JQ_E_INVALID, "bad global sizes for the shard");
+  JQ_TRY(begin_call(ctx));
+  const int64_t n = n1 + n2;
+  JQ_TRY(ws_reserve(ctx, stage_bytes(a, a_rows * n1) + stage_bytes(b, b_rows * n2) +
+                             stage_bytes(b_prefix, n2) + stage_bytes(b_total, n2) +
+                             stage_bytes((const double*)r_local, n * n) +
+                             figaro_ws(a_rows, n1, b_rows, n2, false, ctx->sms)));
+  const double *da, *db, *dpre, *dtot;
+  double* dr;
+  JQ_TRY(stage_in(ctx, a, a_rows * n1, &da));
+  JQ_TRY(stage_in(ctx, b, b_rows * n2, &db));
+  JQ_TRY(stage_in(ctx, b_prefix, n2, &dpre));
+  JQ_TRY(stage_in(ctx, b_total, n2, &dtot));
+  JQ_TRY(stage_out(ctx, r_local, n * n, &dr));
+  cudaEventRecord(ctx->ev[0], ctx->stream);
+  cudaEventRecord(ctx->ev[1], ctx->stream);
+  SegScan ss{};
+  if (n2 > 0) JQ_TRY(segscan_dev(ctx, db, b_rows, n2, nullptr, nullptr, nullptr, nullptr, 1, &ss));
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  FigaroArgs fa{};
+  fa.a = da; fa.m1 = a_rows; fa.n1 = n1;
+  fa.b = db; fa.m2 = b_rows; fa.n2 = n2;
+  fa.b_totals = dtot;
+  fa.b_carry = n2 > 0 ? ss.carry : nullptr;
+  fa.b_prefix0 = dpre;
+  fa.m1_global = m1; fa.m2_global = m2; fa.b_row0 = b_row0;
+  JQ_TRY(figaro_tsqr_dev(ctx, fa, dr, false));
+  JQ_TRY(copy_out(ctx, r_local, (const double*)dr, n * n));
+  int rc = sync_and_check_flags(ctx);
+  record_timing(ctx, false);
+  return rc;
+}
+
+int jq_tsqr_stack(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, double* r) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (count <= 0 || n <= 0 || n > 256) return fail(JQ_E_INVALID, "bad R stack geometry");
+  JQ_TRY(begin_call(ctx));
+  JQ_TRY(ws_reserve(ctx, stage_bytes(rs, count * n * n) + stage_bytes((const double*)r, n * n) +
+                             2 * ws_bytes(size_t(count + 1) * 256 * 256, 8)));
+  const double* drs;
+  double* dr;
+  JQ_TRY(stage_in(ctx, rs, count * n * n, &drs));
+  JQ_TRY(stage_out(ctx, r, n * n, &dr));
+  JQ_TRY(tsqr_stack_dev(ctx, drs, count, n, dr, true));
+  JQ_TRY(copy_out(ctx, r, (const double*)dr, n * n));
+  return sync_and_check_flags(ctx);
+}
+
+}  // extern "C"

@@ -1,0 +1,364 @@
+// jq_headtail.cu — the Figaro head/tail operators on the GPU (SPEC.md:107-165,
+// PAPER.md:49-51) and the Claim-1 assembly of the reduced matrix.
+//
+// head(M) = (1/sqrt(m)) sum_i M_i;  tail row r (i = r+1) = (sqrt(i) M_i - S_i/sqrt(i)) / sqrt(i+1)
+// with S_i the in-group prefix sum.  The prefix is computed by a deterministic
+// reduce-then-scan with FIXED tile boundaries (TILE_ROWS rows), so results do not
+// depend on the grid size or on timing (SPEC.md:302 asks for run-to-run
+// determinism; decoupled look-back would not give it):
+//   1. segscan_tile_kernel  one warp per tile: in-tile segmented column sums,
+//                           partial group totals (HBM-bound: reads x once);
+//   2. segscan_carry_kernel per column, sequential over tiles: exclusive carry;
+//   3. group_fixup_kernel   adds the carry to groups that span tiles.
+// The figaro_r path consumes the carries inside the fused TSQR loader
+// (jq_tsqr.cu) and never writes the reduced matrix; reduce_* / head_tail (the
+// API that returns the matrix itself) use the emit kernels below.
+#include <algorithm>
+#include <cmath>
+
+#include "jq_internal.cuh"
+
+namespace jq {
+
+constexpr int MAXC = 8;  // columns per lane (cols <= 256)
+
+// One warp per TILE_ROWS tile.  Segment id of row r: gid[r] (or 0 when gid is
+// null = one segment).  Writes agg[t] (sum of the segment open at the tile end,
+// restricted to the tile), flag[t] (tile contains a segment start) and, for each
+// segment that ends inside the tile, its in-tile partial sum into totals[seg].
+__global__ void __launch_bounds__(256) segscan_tile_kernel(
+    const double* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ gid,
+    int64_t ntiles, double* __restrict__ agg, int* __restrict__ flag, double* __restrict__ totals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= ntiles) return;
+  const int64_t r0 = t * TILE_ROWS, r1 = min(rows, r0 + TILE_ROWS);
+  double s[MAXC];
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k) s[k] = 0.0;
+  int seg = gid ? gid[r0] : 0;
+  int any_start = (r0 == 0) || (gid && gid[r0 - 1] != seg);
+  for (int64_t r = r0; r < r1; ++r) {
+    const int sr = gid ? gid[r] : 0;
+    const bool start = (r == 0) || (r > r0 && sr != seg);
+    if (start && r > r0) {
+      // previous segment ended at r-1 inside this tile
+      if (seg >= 0)
+#pragma unroll
+        for (int k = 0; k < MAXC; ++k)
+          if (k * 32 + lane < cols) totals[(int64_t)seg * cols + k * 32 + lane] = s[k];
+      any_start = 1;
+    }
+    seg = sr;
+    const double* row = x + r * cols;
+#pragma unroll
+    for (int k = 0; k < MAXC; ++k) {
+      const int c = k * 32 + lane;
+      if (c < cols) {
+        const double v = __ldg(row + c);
+        s[k] = start ? v : s[k] + v;
+      }
+    }
+  }
+  // open segment at the tile end
+  const bool ends_here = (r1 == rows) || (gid && gid[r1] != seg) ;
+  if (ends_here && seg >= 0)
+#pragma unroll
+    for (int k = 0; k < MAXC; ++k)
+      if (k * 32 + lane < cols) totals[(int64_t)seg * cols + k * 32 + lane] = s[k];
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k)
+    if (k * 32 + lane < cols) agg[t * cols + k * 32 + lane] = s[k];
+  if (lane == 0) flag[t] = any_start;
+}
+
+// carry[0] = 0; carry[t+1] = flag[t] ? agg[t] : carry[t] + agg[t]   (fixed order)
+__global__ void segscan_carry_kernel(const double* __restrict__ agg, const int* __restrict__ flag,
+                                     int64_t ntiles, int cols, double* __restrict__ carry) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double cur = 0.0;
+  int64_t t = 0;
+  for (; t + 8 <= ntiles; t += 8) {
+    double a[8];
+    int f[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { a[u] = agg[(t + u) * cols + c]; f[u] = flag[t + u]; }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      carry[(t + u) * cols + c] = cur;
+      cur = f[u] ? a[u] : cur + a[u];
+    }
+  }
+  for (; t < ntiles; ++t) {
+    carry[t * cols + c] = cur;
+    cur = flag[t] ? agg[t * cols + c] : cur + agg[t * cols + c];
+  }
+}
+
+// totals[g] += carry[last tile of g] for groups that began before that tile.
+__global__ void group_fixup_kernel(const int64_t* __restrict__ gstart, const int64_t* __restrict__ gcount,
+                                   const int64_t* __restrict__ d_ngroups, int64_t single_rows,
+                                   int cols, const double* __restrict__ carry, double* __restrict__ totals) {
+  const int64_t ng = d_ngroups ? d_ngroups[0] : 1;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < ng * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = idx / cols;
+    const int c = (int)(idx - g * cols);
+    const int64_t st = gstart ? gstart[g] : 0;
+    const int64_t cnt = gcount ? gcount[g] : single_rows;
+    if (cnt <= 0) continue;
+    const int64_t tl = (st + cnt - 1) / TILE_ROWS;
+    if (st < tl * TILE_ROWS) totals[g * cols + c] += carry[tl * cols + c];
+  }
+}
+
+size_t segscan_ws_bytes(int64_t rows, int64_t cols, int64_t groups_cap) {
+  int64_t nt = std::max<int64_t>(1, cdiv(rows, TILE_ROWS));
+  return 2 * ws_bytes(size_t(nt) * cols, 8) + ws_bytes(nt, 4) +
+         ws_bytes(size_t(std::max<int64_t>(groups_cap, 1)) * cols, 8);
+}
+
+int segscan_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int32_t* gid,
+                const int64_t* gstart, const int64_t* gcount, const int64_t* d_ngroups,
+                int64_t groups_cap, SegScan* s) {
+  if (cols > 32 * MAXC) return fail(JQ_E_INVALID, "more than 256 columns per table");
+  s->ntiles = std::max<int64_t>(1, cdiv(rows, TILE_ROWS));
+  s->carry = ws_alloc<double>(ctx, size_t(s->ntiles) * cols);
+  s->tile_agg = ws_alloc<double>(ctx, size_t(s->ntiles) * cols);
+  s->tile_flag = ws_alloc<int>(ctx, s->ntiles);
+  s->totals = ws_alloc<double>(ctx, size_t(std::max<int64_t>(groups_cap, 1)) * cols);
+  if (!s->carry || !s->tile_agg || !s->tile_flag || !s->totals)
+    return fail(JQ_E_OOM, "workspace exhausted (head/tail scan)");
+  JQ_CUDA(cudaMemsetAsync(s->totals, 0, size_t(std::max<int64_t>(groups_cap, 1)) * cols * 8, ctx->stream));
+  if (rows == 0) {
+    JQ_CUDA(cudaMemsetAsync(s->carry, 0, size_t(s->ntiles) * cols * 8, ctx->stream));
+    return JQ_OK;
+  }
+  const int wpb = 8;
+  segscan_tile_kernel<<<(unsigned)cdiv(s->ntiles, wpb), 32 * wpb, 0, ctx->stream>>>(
+      x, rows, (int)cols, gid, s->ntiles, s->tile_agg, s->tile_flag, s->totals);
+  JQ_CHECK_LAUNCH(ctx);
+  segscan_carry_kernel<<<(unsigned)cdiv(cols, 64), 64, 0, ctx->stream>>>(s->tile_agg, s->tile_flag,
+                                                                         s->ntiles, (int)cols, s->carry);
+  JQ_CHECK_LAUNCH(ctx);
+  group_fixup_kernel<<<(unsigned)std::min<int64_t>(cdiv(std::max<int64_t>(groups_cap, 1) * cols, 256), 4096),
+                       256, 0, ctx->stream>>>(gstart, gcount, d_ngroups, rows, (int)cols, s->carry,
+                                              s->totals);
+  JQ_CHECK_LAUNCH(ctx);
+  return JQ_OK;
+}
+
+// ------------------------------------------------------------------ emit kernels
+// Tail rows of every segment: row r of x with in-group index rr >= 1 goes to output
+// row base(g) + rr - 1, columns [col0, col0 + cols), scaled by sqrt(count(g)); columns
+// [0, col0) of that output row are zeroed (the exact-zero block).
+__global__ void __launch_bounds__(256) tail_emit_kernel(
+    const double* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ gid,
+    const int64_t* __restrict__ gstart, const int64_t* __restrict__ scale_count, double scale_all,
+    const int64_t* __restrict__ out_base, int64_t out_base_all, int out_ld, int col0,
+    const double* __restrict__ carry, int64_t ntiles, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= ntiles) return;
+  const int64_t r0 = t * TILE_ROWS, r1 = min(rows, r0 + TILE_ROWS);
+  double s[MAXC];
+#pragma unroll
+  for (int k = 0; k < MAXC; ++k) s[k] = (k * 32 + lane < cols) ? carry[t * cols + k * 32 + lane] : 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int g = gid ? gid[r] : 0;
+    const double* row = x + r * cols;
+    if (g < 0) continue;
+    const int64_t rr = r - (gid ? gstart[g] : 0);
+    if (rr == 0) {
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k)
+        if (k * 32 + lane < cols) s[k] = __ldg(row + k * 32 + lane);
+      continue;
+    }
+    const double si = sqrt((double)rr), si1 = sqrt((double)rr + 1.0);
+    const double sc = sqrt(scale_count ? (double)scale_count[g] : scale_all);
+    double* orow = out + ((gid ? out_base[g] : out_base_all) + rr - 1) * out_ld;
+    for (int c = lane; c < col0; c += 32) orow[c] = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXC; ++k) {
+      const int c = k * 32 + lane;
+      if (c < cols) {
+        const double v = __ldg(row + c);
+        orow[col0 + c] = (si * v - s[k] / si) / si1 * sc;
+        s[k] += v;
+      }
+    }
+  }
+}
+
+// Top block rows: A row i of group g -> output row red_off[g] + (i - a_start[g]):
+// [sqrt(m2g) A_i | totals_b[g] / sqrt(m2g)].
+__global__ void top_emit_kernel(const double* __restrict__ a, int64_t m1, int n1,
+                                const int32_t* __restrict__ gid_a, const int64_t* __restrict__ a_start,
+                                const int64_t* __restrict__ b_count, int64_t m2_all,
+                                const int64_t* __restrict__ red_off, const double* __restrict__ b_totals,
+                                int n2, double* __restrict__ out) {
+  const int n = n1 + n2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m1 * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / n;
+    const int c = (int)(idx - i * n);
+    const int g = gid_a ? gid_a[i] : 0;
+    if (g < 0) continue;
+    const double m2g = gid_a ? (double)b_count[g] : (double)m2_all;
+    const int64_t orow = gid_a ? red_off[g] + (i - a_start[g]) : i;
+    out[orow * n + c] = c < n1 ? a[i * n1 + c] * sqrt(m2g) : b_totals[(int64_t)g * n2 + (c - n1)] / sqrt(m2g);
+  }
+}
+
+__global__ void tail_base_kernel(const int64_t* __restrict__ red_off, const int64_t* __restrict__ a_count,
+                                 const int64_t* __restrict__ d_ng, int64_t* __restrict__ base) {
+  const int64_t ng = d_ng[0];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x)
+    base[g] = red_off[g] + a_count[g];
+}
+
+__global__ void head_row_kernel(const double* __restrict__ totals, int cols, double m, double* __restrict__ out) {
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) out[c] = totals[c] / sqrt(m);
+}
+
+__global__ void group_bounds_kernel(const int64_t* __restrict__ red_off, const int64_t* __restrict__ d_ng,
+                                    int64_t* __restrict__ bounds) {
+  const int64_t ng = d_ng[0];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    bounds[2 * g] = red_off[g];
+    bounds[2 * g + 1] = red_off[g + 1];
+  }
+}
+
+static unsigned grid_for(int64_t work, int threads = 256, int64_t cap = 148 * 16) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, threads), cap));
+}
+
+// ------------------------------------------------------------------ public API
+}  // namespace jq
+
+using namespace jq;
+
+extern "C" int jq_head_tail(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, double* out) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (rows <= 0) return fail(JQ_E_INVALID, "head/tail undefined for a matrix with 0 rows");
+  if (cols <= 0) return JQ_OK;
+  if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
+  JQ_TRY(begin_call(ctx));
+  size_t need = stage_bytes(m, rows * cols) + stage_bytes((const double*)out, rows * cols) +
+                segscan_ws_bytes(rows, cols, 1);
+  JQ_TRY(ws_reserve(ctx, need));
+  const double* dm;
+  double* dout;
+  JQ_TRY(stage_in(ctx, m, rows * cols, &dm));
+  JQ_TRY(stage_out(ctx, out, rows * cols, &dout));
+  SegScan ss;
+  JQ_TRY(segscan_dev(ctx, dm, rows, cols, nullptr, nullptr, nullptr, nullptr, 1, &ss));
+  head_row_kernel<<<1, 256, 0, ctx->stream>>>(ss.totals, (int)cols, (double)rows, dout);
+  JQ_CHECK_LAUNCH(ctx);
+  tail_emit_kernel<<<(unsigned)cdiv(ss.ntiles, 8), 256, 0, ctx->stream>>>(
+      dm, rows, (int)cols, nullptr, nullptr, nullptr, 1.0, nullptr, 1, (int)cols, 0, ss.carry,
+      ss.ntiles, dout);
+  JQ_CHECK_LAUNCH(ctx);
+  JQ_TRY(copy_out(ctx, out, (const double*)dout, rows * cols));
+  return sync_and_check_flags(ctx);
+}
+
+extern "C" int jq_colsums(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, double* sums) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (cols <= 0) return JQ_OK;
+  if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
+  JQ_TRY(begin_call(ctx));
+  JQ_TRY(ws_reserve(ctx, stage_bytes(x, rows * cols) + stage_bytes((const double*)sums, cols) +
+                             segscan_ws_bytes(rows, cols, 1)));
+  const double* dx;
+  double* ds;
+  JQ_TRY(stage_in(ctx, x, rows * cols, &dx));
+  JQ_TRY(stage_out(ctx, sums, cols, &ds));
+  SegScan ss;
+  JQ_TRY(segscan_dev(ctx, dx, rows, cols, nullptr, nullptr, nullptr, nullptr, 1, &ss));
+  JQ_CUDA(cudaMemcpyAsync(ds, ss.totals, cols * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  JQ_TRY(copy_out(ctx, sums, (const double*)ds, cols));
+  return sync_and_check_flags(ctx);
+}
+
+extern "C" int jq_reduce(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
+                         const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* out,
+                         int64_t out_capacity, int64_t* out_rows, int64_t* group_bounds) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if ((ka == nullptr) != (kb == nullptr)) return fail(JQ_E_KEYS, "both tables must carry keys, or neither");
+  if (n1 < 0 || n2 < 0 || n1 > 256 || n2 > 256) return fail(JQ_E_INVALID, "column counts must lie in 0..256");
+  const bool keyed = ka != nullptr;
+  if (!keyed && (m1 <= 0 || m2 <= 0)) return fail(JQ_E_INVALID, "reduce_cartesian needs non-empty inputs");
+  JQ_TRY(begin_call(ctx));
+  const int64_t n = n1 + n2;
+  const int64_t cap = keyed ? std::max<int64_t>(1, std::min(m1, m2)) : 1;
+  size_t need = stage_bytes(a, m1 * n1) + stage_bytes(b, m2 * n2) + stage_bytes(ka, m1) +
+                stage_bytes(kb, m2) + (keyed ? group_ws_bytes(m1, m2) : 0) +
+                segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) + ws_bytes(cap, 8) + 4096;
+  if (out) need += stage_bytes((const double*)out, out_capacity * n);
+  if (group_bounds) need += ws_bytes(2 * cap, 8);
+  JQ_TRY(ws_reserve(ctx, need));
+  const int64_t *dka = nullptr, *dkb = nullptr;
+  JQ_TRY(stage_in(ctx, ka, m1, &dka));
+  JQ_TRY(stage_in(ctx, kb, m2, &dkb));
+  Groups gr;
+  int64_t ng = 1, total_rows = m1 + m2 - 1;
+  if (keyed) {
+    JQ_TRY(group_keys_dev(ctx, dka, m1, dkb, m2, &gr));
+    int64_t hn[2];
+    JQ_CUDA(cudaMemcpyAsync(hn, gr.d_n, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    JQ_TRY(sync_and_check_flags(ctx));
+    ng = hn[0];
+    total_rows = hn[1];
+  }
+  if (out_rows) *out_rows = total_rows;
+  if (group_bounds && ng > 0) {
+    if (keyed) {
+      int64_t* db = ws_alloc<int64_t>(ctx, 2 * ng);
+      group_bounds_kernel<<<grid_for(ng), 256, 0, ctx->stream>>>(gr.red_off, gr.d_n, db);
+      JQ_CHECK_LAUNCH(ctx);
+      JQ_CUDA(cudaMemcpyAsync(group_bounds, db, 2 * ng * 8, cudaMemcpyDefault, ctx->stream));
+    } else {
+      group_bounds[0] = 0;
+      group_bounds[1] = total_rows;
+    }
+  }
+  if (!out || total_rows == 0) return sync_and_check_flags(ctx);
+  if (out_capacity < total_rows) return fail(JQ_E_INVALID, "output buffer too small for the reduced matrix");
+  const double *da, *db;
+  double* dout;
+  JQ_TRY(stage_in(ctx, a, m1 * n1, &da));
+  JQ_TRY(stage_in(ctx, b, m2 * n2, &db));
+  JQ_TRY(stage_out(ctx, out, total_rows * n, &dout));
+  if (n2 == 0)  // bottom rows are exact-zero rows of width n1
+    JQ_CUDA(cudaMemsetAsync(dout, 0, total_rows * n * 8, ctx->stream));
+  SegScan ss;
+  const int64_t cols_b = std::max<int64_t>(n2, 1);
+  if (n2 > 0) {
+    JQ_TRY(segscan_dev(ctx, db, m2, n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
+                       keyed ? gr.b_count : nullptr, keyed ? gr.d_n : nullptr, cap, &ss));
+  } else {
+    JQ_TRY(segscan_dev(ctx, db, 0, cols_b, nullptr, nullptr, nullptr, nullptr, cap, &ss));
+  }
+  top_emit_kernel<<<grid_for(m1 * n), 256, 0, ctx->stream>>>(
+      da, m1, (int)n1, keyed ? gr.gid_a : nullptr, keyed ? gr.a_start : nullptr,
+      keyed ? gr.b_count : nullptr, m2, keyed ? gr.red_off : nullptr, ss.totals, (int)n2, dout);
+  JQ_CHECK_LAUNCH(ctx);
+  if (n2 > 0) {
+    int64_t* base = nullptr;
+    if (keyed) {
+      base = ws_alloc<int64_t>(ctx, cap);
+      tail_base_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(gr.red_off, gr.a_count, gr.d_n, base);
+      JQ_CHECK_LAUNCH(ctx);
+    }
+    tail_emit_kernel<<<(unsigned)cdiv(ss.ntiles, 8), 256, 0, ctx->stream>>>(
+        db, m2, (int)n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
+        keyed ? gr.a_count : nullptr, (double)m1, base, m1, (int)n, (int)n1, ss.carry, ss.ntiles, dout);
+    JQ_CHECK_LAUNCH(ctx);
+  }
+  JQ_TRY(copy_out(ctx, out, (const double*)dout, total_rows * n));
+  return sync_and_check_flags(ctx);
+}

@@ -1,0 +1,295 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): grouping bit-exact; |R| (row signs normalised)
+and R^T R within 1e-10 relative Frobenius; singular values within 1e-10
+relative.  Head/tail and the reduced matrix are checked entrywise at 1e-12
+(their only difference from the oracle is the blocked vs sequential prefix sum).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2503_23385_b200 as P
+    return P
+
+
+def rel_fro(x, y):
+    x, y = np.asarray(x), np.asarray(y)
+    return np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)
+
+
+def check_r(r, r_ref, tol=1e-10):
+    r, r_ref = np.asarray(r), np.asarray(r_ref)
+    assert np.all(np.tril(r, -1) == 0.0), "R must have exact zeros below the diagonal"
+    assert np.all(np.diag(r) >= 0), "R must be canonical"
+    assert rel_fro(np.abs(r), np.abs(r_ref)) <= tol, rel_fro(np.abs(r), np.abs(r_ref))
+    assert rel_fro(r.T @ r, r_ref.T @ r_ref) <= tol
+
+
+def rand_tables(rng, m1, n1, m2, n2, groups=None):
+    if groups is None:
+        return O.Table(rng.random((m1, n1))), O.Table(rng.random((m2, n2)))
+    ka = np.sort(rng.integers(0, groups, m1))
+    kb = np.sort(rng.integers(0, groups, m2))
+    return O.Table(rng.random((m1, n1)), ka), O.Table(rng.random((m2, n2)), kb)
+
+
+def to_p(P, t):
+    return P.Table(t.data, t.keys)
+
+
+# ------------------------------------------------------------ SPEC golden examples
+def test_spec_examples_on_gpu(P):
+    for c in GOLD["head"]:
+        assert np.allclose(P.head(c["in"]), c["out"], rtol=0, atol=1e-14)
+    for c in GOLD["tail"]:
+        t = P.tail(c["in"])
+        if "out_shape" in c:
+            assert t.shape == tuple(c["out_shape"])
+        else:
+            assert np.allclose(t, c["out"], rtol=0, atol=1e-14)
+    for c in GOLD["reduce_cartesian"]:
+        assert np.allclose(P.reduce_cartesian(c["a"], c["b"]).matrix, c["out"], rtol=0, atol=1e-14)
+    for c in GOLD["reduce_natural_join"]:
+        red = P.reduce_natural_join(P.Table(c["a"], c["ka"]), P.Table(c["b"], c["kb"]))
+        assert red.matrix.shape == (c["rows"], 2)
+    for c in GOLD["householder_r"]:
+        assert np.allclose(P.canonicalize(P.householder_r(c["in"])), c["canonical"], atol=1e-14)
+    for c in GOLD["canonicalize"]:
+        assert np.array_equal(P.canonicalize(c["in"]), np.array(c["out"], dtype=float))
+    for c in GOLD["figaro_r"]:
+        r = P.figaro_r(P.Table(c["a"]), P.Table(c["b"]))
+        assert np.allclose(r, c["out"], rtol=1e-14, atol=1e-14)
+        assert P.is_upper_triangular(r)
+    for c in GOLD["svd_of_r"]:
+        s = P.svd_of_r(c["in"], True)
+        assert np.allclose(s.values, c["values"], atol=1e-14)
+        assert np.allclose(np.abs(s.right_vectors), np.abs(np.array(c["v"])), atol=1e-14)
+    for c in GOLD["figaro_svd"]:
+        s = P.figaro_svd(P.Table(c["a"]), P.Table(c["b"]))
+        assert np.allclose(s.values, c["values"], rtol=1e-13)
+
+
+# ------------------------------------------------------------ head / tail
+@pytest.mark.parametrize("rows,cols", [(1, 3), (2, 1), (7, 5), (1023, 8), (1024, 8), (1025, 17),
+                                       (5000, 64), (3000, 256)])
+def test_head_tail(P, rows, cols):
+    rng = np.random.default_rng(rows * 7 + cols)
+    m = rng.standard_normal((rows, cols))
+    got = P.head_tail(m)
+    ref = O.head_tail(m)
+    assert np.max(np.abs(got - ref)) <= 1e-12 * max(1, np.abs(ref).max())
+    g = O.gram(m)
+    assert O.max_abs_diff(O.gram(got), g) <= 1e-12 * max(1, np.abs(g).max())
+
+
+def test_head_tail_constant_rows(P):
+    m = np.tile(np.array([0.3, -2.0, 5.5]), (3000, 1))
+    assert np.abs(P.tail(m)).max() <= 1e-12
+
+
+# ------------------------------------------------------------ grouping (bit-exact)
+@pytest.mark.parametrize("m1,m2,universe", [(1, 1, 1), (10, 7, 5), (1000, 1500, 37), (200_000, 150_000, 50_000),
+                                            (100_000, 100_000, 10)])
+def test_group_keys_bit_exact(P, m1, m2, universe):
+    rng = np.random.default_rng(m1 + m2)
+    ka = np.sort(rng.integers(-universe, universe, m1))
+    kb = np.sort(rng.integers(-universe, universe, m2))
+    got = P.group_keys(ka, kb)
+    ref = O.group_keys(ka, kb)
+    for x, y in zip(got, ref):
+        assert x.dtype == np.int64 and np.array_equal(x, y)
+
+
+def test_group_keys_disjoint_and_extremes(P):
+    got = P.group_keys(np.array([1, 1, 3]), np.array([2, 4]))
+    assert len(got[0]) == 0 and got[5].tolist() == [0]
+    big = np.array([np.iinfo(np.int64).min, -1, 0, np.iinfo(np.int64).max])
+    for x, y in zip(P.group_keys(big, big), O.group_keys(big, big)):
+        assert np.array_equal(x, y)
+
+
+def test_unsorted_keys_raise(P):
+    with pytest.raises(ValueError, match="sorted"):
+        P.group_keys(np.array([2, 1]), np.array([1, 2]))
+    with pytest.raises(ValueError, match="sorted"):
+        P.figaro_r(P.Table(np.ones((2, 1)), [1, 1]), P.Table(np.ones((2, 1)), [3, 2]))
+
+
+# ------------------------------------------------------------ reduce (SPEC order)
+@pytest.mark.parametrize("case", ["cart_small", "cart_m1", "cart_m2", "cart_big", "nat", "nat_big"])
+def test_reduce_matches_oracle(P, case):
+    rng = np.random.default_rng(hash(case) % 2**32)
+    shapes = {"cart_small": (5, 3, 7, 2, None), "cart_m1": (1, 2, 9, 3, None),
+              "cart_m2": (6, 2, 1, 4, None), "cart_big": (3000, 8, 5000, 16, None),
+              "nat": (60, 3, 80, 2, 9), "nat_big": (20000, 4, 30000, 5, 700)}
+    m1, n1, m2, n2, groups = shapes[case]
+    a, b = rand_tables(rng, m1, n1, m2, n2, groups)
+    ref = O.reduce_join(a, b)
+    got = P.reduce_join(to_p(P, a), to_p(P, b))
+    assert got.matrix.shape == ref.matrix.shape
+    assert np.max(np.abs(got.matrix - ref.matrix), initial=0) <= 1e-12 * max(1, np.abs(ref.matrix).max(initial=0))
+    assert got.group_boundaries == ref.group_boundaries
+    if groups is None:
+        assert np.all(got.matrix[m1:, :n1] == 0.0)   # exact zeros
+
+
+# ------------------------------------------------------------ householder_r / figaro_r
+@pytest.mark.parametrize("rows,cols", [(1, 1), (3, 5), (7, 3), (64, 16), (1000, 31), (20000, 64),
+                                       (5000, 100), (3000, 128), (2000, 200), (1500, 256)])
+def test_householder_r(P, rows, cols):
+    rng = np.random.default_rng(rows + 1000 * cols)
+    m = rng.standard_normal((rows, cols))
+    r = np.asarray(P.householder_r(m))
+    assert P.is_upper_triangular(r)
+    ref = O.householder_r_lapack(m)
+    g = m.T @ m
+    assert np.abs(r.T @ r - g).max() <= 1e-10 * max(1, np.abs(g).max())
+    if rows >= cols:
+        check_r(P.canonicalize(r), O.canonicalize(ref))
+
+
+@pytest.mark.parametrize("m1,n1,m2,n2,groups", [
+    (2, 1, 2, 1, None), (1, 3, 1, 2, None), (1, 1, 9, 4, None), (7, 4, 1, 3, None),
+    (1000, 4, 1000, 4, None), (3000, 8, 2000, 8, None), (4000, 32, 5000, 32, None),
+    (2500, 64, 2500, 64, None), (3000, 100, 2000, 120, None),
+    (400, 5, 300, 6, 40), (6000, 16, 7000, 16, 600), (20000, 32, 20000, 32, 100)])
+def test_figaro_r_matches_oracle(P, m1, n1, m2, n2, groups):
+    rng = np.random.default_rng(m1 + 3 * m2 + n1 + (groups or 0))
+    a, b = rand_tables(rng, m1, n1, m2, n2, groups)
+    r = np.asarray(P.figaro_r(to_p(P, a), to_p(P, b)))
+    red = O.reduce_join(a, b).matrix
+    if red.shape[0] >= red.shape[1] and np.linalg.matrix_rank(red) == red.shape[1]:
+        check_r(r, O.canonicalize(O.householder_r_lapack(red)))
+    g = O.gram(red)
+    assert np.abs(r.T @ r - g).max() <= 1e-10 * max(1, np.abs(g).max())
+
+
+def test_figaro_r_empty_join_and_materialised(P):
+    a = P.Table(np.ones((2, 2)), [1, 1])
+    b = P.Table(np.ones((3, 1)), [2, 2, 2])
+    assert np.array_equal(P.figaro_r(a, b), np.zeros((3, 3)))
+    rng = np.random.default_rng(5)
+    ta, tb = rand_tables(rng, 30, 2, 25, 3, 4)
+    j = O.materialize_natural_join(ta, tb)
+    check_r(P.figaro_r(to_p(P, ta), to_p(P, tb)), O.baseline_r(j))
+
+
+# ------------------------------------------------------------ svd
+@pytest.mark.parametrize("n", [1, 2, 3, 8, 33, 64, 128, 256])
+def test_svd_of_r(P, n):
+    rng = np.random.default_rng(n)
+    r = np.triu(rng.standard_normal((n, n)))
+    s = P.svd_of_r(r, True)
+    ref = np.linalg.svd(r, compute_uv=False)
+    assert np.max(np.abs(s.values - ref)) <= 1e-10 * ref[0]
+    v = np.asarray(s.right_vectors)
+    assert np.abs(v.T @ v - np.eye(n)).max() <= 1e-10
+    rec = v @ np.diag(s.values ** 2) @ v.T
+    assert np.abs(r.T @ r - rec).max() <= 1e-8 * max(1, s.values[0] ** 2)
+    if n <= 64:
+        so = O.svd_of_r(r)
+        assert np.max(np.abs(s.values - so.values)) <= 1e-10 * so.values[0]
+
+
+def test_svd_rank_deficient_and_zero(P):
+    s = P.svd_of_r(np.zeros((4, 4)), True)
+    assert np.array_equal(s.values, np.zeros(4)) and np.array_equal(s.right_vectors, np.eye(4))
+    rng = np.random.default_rng(9)
+    a, b = O.Table(rng.random((2, 3))), O.Table(rng.random((2, 3)))  # rank <= 3 < 6
+    s = P.figaro_svd(to_p(P, a), to_p(P, b), True)
+    ref = np.linalg.svd(O.materialize_cartesian(a.data, b.data), compute_uv=False)
+    ref = np.concatenate([ref, np.zeros(6 - len(ref))])      # J is 4 x 6: two zero values
+    assert np.max(np.abs(s.values - ref)) <= 1e-10 * ref[0]
+
+
+@pytest.mark.parametrize("m,n,groups", [(1000, 4, None), (3000, 16, None), (5000, 64, None), (4000, 16, 300)])
+def test_figaro_svd_matches_oracle(P, m, n, groups):
+    rng = np.random.default_rng(m + n)
+    a, b = rand_tables(rng, m, n, m + 17, n, groups)
+    s = P.figaro_svd(to_p(P, a), to_p(P, b), True)
+    red = O.reduce_join(a, b).matrix
+    ref = np.linalg.svd(red, compute_uv=False)
+    assert np.max(np.abs(np.asarray(s.values) - ref)) <= 1e-10 * ref[0]
+
+
+# ------------------------------------------------------------ generator (bit-exact)
+def test_gen_uniform_bit_exact(P):
+    t = P.gen_uniform(P.GenSpec(1000, 7, 1234567, key_groups=10))
+    ot = O.gen_uniform(O.GenSpec(1000, 7, 1234567, key_groups=10))
+    assert np.array_equal(np.asarray(t.data), ot.data)
+    assert np.array_equal(np.asarray(t.keys), ot.keys)
+    from paper_2503_23385_b200 import datagen
+    blk = datagen.uniform(42, 33, 5, row0=1001)
+    assert np.array_equal(blk, O.datagen.uniform_matrix(42, 33, 5, row0=1001))
+
+
+def test_zipf_keys_bit_exact(P):
+    from paper_2503_23385_b200 import datagen
+    got = datagen.zipf_sorted_keys(3003, 200_000, 1.1, 50_000)
+    ref = np.sort(O.zipf_keys(3003, 200_000, 1.1, 50_000), kind="stable")
+    assert np.array_equal(got, ref)
+
+
+# ------------------------------------------------------------ shard building blocks
+def test_shard_r_and_stack_equal_single_device(P):
+    """Row-sharded Cartesian figaro_r == unsharded figaro_r."""
+    from paper_2503_23385_b200 import _native as N
+    rng = np.random.default_rng(11)
+    m1, n1, m2, n2 = 5000, 6, 7000, 5
+    A, B = rng.random((m1, n1)), rng.random((m2, n2))
+    n = n1 + n2
+    ref = np.asarray(P.figaro_r(P.Table(A), P.Table(B)))
+    for parts in (1, 2, 3, 5):
+        ab = np.linspace(0, m1, parts + 1).astype(int)
+        bb = np.linspace(0, m2, parts + 1).astype(int)
+        sums = np.stack([B[bb[p]:bb[p + 1]].sum(axis=0) for p in range(parts)])
+        total = sums.sum(axis=0)
+        rs = np.zeros((parts, n, n))
+        for p in range(parts):
+            pre = np.ascontiguousarray(sums[:p].sum(axis=0)) if p else np.zeros(n2)
+            a_sh = np.ascontiguousarray(A[ab[p]:ab[p + 1]])
+            b_sh = np.ascontiguousarray(B[bb[p]:bb[p + 1]])
+            N.check(N.lib().jq_figaro_r_shard(N.ctx(), a_sh.ctypes.data, len(a_sh), n1, m1,
+                                              b_sh.ctypes.data, len(b_sh), n2, m2, int(bb[p]),
+                                              pre.ctypes.data, total.ctypes.data, rs[p].ctypes.data))
+        r = np.zeros((n, n))
+        N.check(N.lib().jq_tsqr_stack(N.ctx(), rs.ctypes.data, parts, n, r.ctypes.data))
+        check_r(r, ref, 1e-12)
+
+
+def test_colsums(P):
+    from paper_2503_23385_b200 import _native as N
+    x = np.random.default_rng(1).random((10_000, 40))
+    s = np.zeros(40)
+    N.check(N.lib().jq_colsums(N.ctx(), x.ctypes.data, 10_000, 40, s.ctypes.data))
+    assert np.allclose(s, x.sum(axis=0), rtol=1e-13)
+
+
+def test_device_tensors_in_place(P):
+    import torch
+    rng = np.random.default_rng(3)
+    A, B = rng.random((3000, 8)), rng.random((2000, 8))
+    ta = P.Table(torch.from_numpy(A).cuda())
+    tb = P.Table(torch.from_numpy(B).cuda())
+    r = P.figaro_r(ta, tb)
+    assert r.is_cuda
+    check_r(r.cpu().numpy(), np.asarray(P.figaro_r(P.Table(A), P.Table(B))), 1e-14)
+
+
+def test_determinism(P):
+    rng = np.random.default_rng(8)
+    a, b = P.Table(rng.random((30000, 16))), P.Table(rng.random((30000, 16)))
+    r1, r2 = P.figaro_r(a, b), P.figaro_r(a, b)
+    assert np.array_equal(r1, r2)
