@@ -221,32 +221,17 @@ def main():
     lib, ctx = N.lib(), N.ctx()
     stream = torch.cuda.current_stream()
 
-    r_out = torch.empty((nn, nn), dtype=torch.float64, device=device)
-    if world > 1:
-        if cfg["keys"] is not None:
-            raise SystemExit("multi-GPU bench covers the Cartesian configs (1, 4, 5)")
-        sums = torch.empty(n, dtype=torch.float64, device=device)
-        all_sums = torch.empty((world, n), dtype=torch.float64, device=device)
-        r_loc = torch.empty((nn, nn), dtype=torch.float64, device=device)
-        r_all = torch.empty((world, nn, nn), dtype=torch.float64, device=device)
+    if world > 1 and cfg["keys"] is not None:
+        raise SystemExit("multi-GPU bench covers the Cartesian configs (1, 4, 5)")
 
     def step():
         N.use_torch_stream(A)
         if world == 1:
             if cfg.get("want_v"):
-                res = P.figaro_svd(P.Table(A, ka), P.Table(B, kb), want_vectors=True)
-                return res.values
+                return P.figaro_svd(P.Table(A, ka), P.Table(B, kb), want_vectors=True).values
             return P.figaro_r(P.Table(A, ka), P.Table(B, kb))
-        rows = A.shape[0]
-        N.check(lib.jq_colsums(ctx, N.ptr(B), rows, n, N.ptr(sums)))
-        dist.all_gather_into_tensor(all_sums, sums)                 # carry exchange (NCCL)
-        prefix = all_sums[:rank].sum(0) if rank else torch.zeros(n, dtype=torch.float64, device=device)
-        total = all_sums.sum(0)
-        N.check(lib.jq_figaro_r_shard(ctx, N.ptr(A), rows, n, m, N.ptr(B), rows, n, m, a0,
-                                      N.ptr(prefix.contiguous()), N.ptr(total.contiguous()), N.ptr(r_loc)))
-        dist.all_gather_into_tensor(r_all, r_loc)                   # R all-gather (NCCL)
-        N.check(lib.jq_tsqr_stack(ctx, N.ptr(r_all), world, nn, N.ptr(r_out)))
-        return r_out
+        from paper_2503_23385_b200 import sharded
+        return sharded.figaro_r_sharded(A, B, m, m, a0)   # carry + R all-gathers over NCCL
 
     for _ in range(args.warmup):
         step()

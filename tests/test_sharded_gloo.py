@@ -1,0 +1,82 @@
+"""Multi-process (gloo, world_size 2 and 3) check of the row-sharded orchestration
+(paper_2503_23385_b200/sharded.py): carry exchange of B column sums, per-rank local
+R, R all-gather and the TSQR tree must reproduce the unsharded oracle R.
+
+The per-rank compute is injected as a CPU restatement (this container has no GPU);
+on a B200 box the same orchestration runs with the native callbacks (bench.py).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def cpu_colsums(x):
+    return x.sum(0)
+
+
+def cpu_shard_r(a, b, m1, m2, b_row0, prefix, total):
+    """Local reduced rows of a Cartesian shard (SPEC.md:189-200 with a global prefix)."""
+    a, b = a.numpy(), b.numpy()
+    n1, n2 = a.shape[1], b.shape[1]
+    top = np.hstack([a * np.sqrt(m2), np.repeat((total.numpy() / np.sqrt(m2))[None], len(a), 0)])
+    s = prefix.numpy().copy()
+    rows = []
+    for k in range(len(b)):
+        i = b_row0 + k
+        if i == 0:
+            s = b[k].copy()
+            continue
+        rows.append(np.concatenate([np.zeros(n1), (np.sqrt(i) * b[k] - s / np.sqrt(i)) / np.sqrt(i + 1) * np.sqrt(m1)]))
+        s = s + b[k]
+    red = np.vstack([top] + ([np.array(rows)] if rows else []))
+    return torch.from_numpy(O.householder_r_lapack(red))
+
+
+def cpu_stack(rs):
+    return torch.from_numpy(O.canonicalize(O.householder_r_lapack(rs.reshape(-1, rs.shape[-1]).numpy())))
+
+
+def _worker(rank, world, port, m1, m2, n1, n2, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_23385_b200 import sharded
+    rng = np.random.default_rng(0)
+    A, B = rng.random((m1, n1)), rng.random((m2, n2))
+    a0, a1 = sharded.shard_range(m1, world, rank)
+    b0, b1 = sharded.shard_range(m2, world, rank)
+    r = sharded.figaro_r_sharded(torch.from_numpy(A[a0:a1].copy()), torch.from_numpy(B[b0:b1].copy()),
+                                 m1, m2, b0, colsums=cpu_colsums, shard_r=cpu_shard_r, stack=cpu_stack)
+    out[rank] = r.numpy().tolist()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m1,m2,n1,n2", [(2, 50, 37, 3, 4), (3, 11, 40, 2, 5), (2, 3, 2, 2, 2)])
+def test_sharded_matches_single(world, m1, m2, n1, n2):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), m1, m2, n1, n2, out), nprocs=world, join=True)
+    rng = np.random.default_rng(0)
+    A, B = rng.random((m1, n1)), rng.random((m2, n2))
+    ref = O.figaro_r(O.Table(A), O.Table(B), lapack=True)
+    rs = [np.array(out[r]) for r in range(world)]
+    for r in rs[1:]:
+        assert np.array_equal(r, rs[0]), "ranks must hold the identical R"
+    g = O.gram(O.reduce_cartesian(A, B).matrix)
+    assert np.abs(rs[0].T @ rs[0] - g).max() <= 1e-10 * np.abs(g).max()
+    if m1 + m2 - 1 >= n1 + n2:
+        assert np.linalg.norm(np.abs(rs[0]) - np.abs(ref)) <= 1e-10 * np.linalg.norm(ref)
