@@ -4,24 +4,32 @@
 // householder_r :250-258, figaro_r :278-286).  Design:
 //
 //  * Streaming leaves.  Each CTA owns a contiguous range of rows of the (virtual)
-//    reduced matrix and keeps a running upper-triangular R (NP x NP, in shared
-//    memory for NP <= 128, in its L2-resident global slab for NP = 256).  It
-//    absorbs the range K rows at a time: R <- qr([R; C]).  Every reflector of
-//    [R; C] is v = [e_j ; y_j] (it touches one row of R and all K chunk rows), so
-//    the block reflector of a panel is V = [I; Y] and the compact-WY trailing
-//    update is
+//    reduced matrix and keeps a running upper-triangular R (NP x NP: packed by
+//    8-row panels in shared memory for NP <= 128, in its L2-resident global slab
+//    for NP = 256).  It absorbs the range K rows at a time: R <- qr([R; C]).  Every
+//    reflector of [R; C] is v = [e_j ; y_j] (it touches one row of R and all K
+//    chunk rows), so the block reflector of a panel is V = [I; Y] and the
+//    compact-WY trailing update is
 //        Z = R[panel rows, trail] + Y^T C[:, trail];  W = T^T Z;
 //        R[panel rows, trail] -= W;                     C[:, trail] -= Y W.
-//  * Register-resident chunk.  C lives in registers in the DMMA (m8n8k4 f64)
-//    accumulator layout, transposed: warp w owns column tiles w and NLT-1-w
-//    (balanced triangular work) and holds C^T[l][i] for all K rows.  Both GEMMs
-//    of the trailing update take their A operand straight from those registers by
-//    permuting the reduction index of each DMMA (k = t  <->  i = 8*it + 2*t + b),
-//    so the only shared-memory operands are Y, Y^T and T.
+//  * Asynchronous input.  The raw input rows of the NEXT chunk (A or B rows of the
+//    join, or dense rows) are fetched by one TMA bulk copy (cp.async.bulk + an
+//    mbarrier) into a shared-memory buffer while the current chunk is being
+//    factored; the Claim-1 rows are then formed in place from shared memory.
+//  * Register-resident chunk.  C (K = 128 rows for NP <= 128) lives in registers
+//    in the DMMA (m8n8k4 f64) accumulator layout, transposed: warp w owns column
+//    tiles w and NLT-1-w (balanced triangular work) and holds C^T[l][i] for all K
+//    rows.  Both GEMMs of the trailing update take their A operand straight from
+//    those registers by permuting the reduction index of each DMMA
+//    (k = t  <->  i = 8*it + 2*t + b), so the only shared-memory operands are Y,
+//    Y^T and T.
 //  * Panels of 8 columns (one column tile) are factored by the warp that owns the
-//    tile, from registers, with 4-lane (quad) reductions; the owner of the next
-//    panel updates that tile first, so panel factorisation overlaps the other
-//    warps' trailing updates (one __syncthreads per panel).
+//    tile, from registers, with ONE quad reduction per column (the raw column x is
+//    broadcast through shared memory and every quad forms x . c_g at once: for
+//    g = j that is |x|^2, for g > j the reflector dot product, for g < j the T
+//    entries); reflector scaling is deferred to the end of the panel.  The owner
+//    of the next panel updates that tile first, so panel factorisation overlaps
+//    the other warps' trailing updates (one __syncthreads per panel).
 //  * Tree.  The P leaf R's are combined by a fixed binary tree of the same kernel
 //    (R_init = R_a, rows = R_b), so results are deterministic for a given P.
 //
@@ -44,26 +52,49 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// 1/x and 1/sqrt(x) from the MUFU approximations plus two Newton steps (<= 1 ulp;
+// the CUDA IEEE division/sqrt sequences cost ~180 cycles on the panel's critical path).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 template <int NP_>
 struct Cfg {
   static constexpr int NP = NP_;
   static constexpr int WARPS = NP / 16;     // 2 column tiles per warp
   static constexpr int THREADS = WARPS * 32;
   static constexpr int NLT = NP / 8;        // column tiles
-  static constexpr int K = NP >= 256 ? 32 : 64;  // chunk rows
+  static constexpr int K = NP >= 256 ? 64 : 128;  // chunk rows held in registers
   static constexpr int KT = K / 8;          // row tiles per chunk
   static constexpr bool R_SMEM = NP <= 128;
-  static constexpr int LDS = NP + 2;        // stage row stride   (== 2 mod 16: conflict-free)
-  static constexpr int LDR = R_SMEM ? NP + 2 : NP;
+  // R packed by 8-row panels: panel p holds rows 8p..8p+7, columns 8p..NP-1,
+  // row stride NP - 8p + 2 (== 2 or 10 mod 16: conflict-free DMMA fragment access)
+  static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
   static constexpr int LDY = 10;            // Ys  (K x 8)
   static constexpr int LDYT = K + 2;        // Yt  (8 x K)
   static constexpr int LDT = 10;            // T   (8 x 8)
-  // shared memory carve-up (doubles)
-  static constexpr int OFF_STAGE = 0;
-  static constexpr int SZ_STAGE = K * LDS;
-  static constexpr int OFF_R = OFF_STAGE + SZ_STAGE;
-  static constexpr int SZ_R = R_SMEM ? NP * LDR : 0;
-  static constexpr int OFF_YS = OFF_R + SZ_R;
+  static constexpr int RAW = NP * 64;       // raw-row buffer (NP * 512 bytes)
+  // shared memory carve-up (doubles; every offset even -> 16-byte aligned)
+  static constexpr int OFF_R = 0;
+  static constexpr int SZ_R = R_SMEM ? rp_off(NLT) : 0;
+  static constexpr int OFF_RAW = OFF_R + SZ_R;
+  static constexpr int OFF_YS = OFF_RAW + RAW;
   static constexpr int SZ_YS = K * LDY;
   static constexpr int OFF_YT = OFF_YS + 2 * SZ_YS;
   static constexpr int SZ_YT = 8 * LDYT;
@@ -71,27 +102,46 @@ struct Cfg {
   static constexpr int SZ_T = 8 * LDT;
   static constexpr int OFF_U = OFF_T + 2 * SZ_T;
   static constexpr int OFF_TAU = OFF_U + 64;
-  static constexpr int OFF_S = OFF_TAU + 8;   // running prefix sums (Figaro source, <= NP)
-  static constexpr int TOTAL = OFF_S + NP;
+  static constexpr int OFF_SC = OFF_TAU + 8;  // reflector scales of the panel
+  static constexpr int OFF_X = OFF_SC + 8;    // raw panel column broadcast (K)
+  static constexpr int OFF_S = OFF_X + K;     // running prefix sums (Figaro source, <= NP)
+  static constexpr int OFF_LD = OFF_S + NP;   // loader scratch: 3 per-row coefficients + 2 per thread
+  static constexpr int SZ_LD = 3 * K + 2 * THREADS;
+  static constexpr int OFF_BAR = OFF_LD + SZ_LD;  // mbarrier (8 bytes)
+  static constexpr int TOTAL = OFF_BAR + 2;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
+// R element (r, c), c >= 8 * (r / 8), in the packed (smem) or dense (global) layout
+template <class C>
+__device__ __forceinline__ int rix(int r, int c) {
+  if constexpr (C::R_SMEM) {
+    const int p = r >> 3;
+    return C::rp_off(p) + (r & 7) * (C::NP - 8 * p + 2) + (c - 8 * p);
+  } else {
+    return r * C::NP + c;
+  }
+}
+
 // ------------------------------------------------------------------ row sources
-// A source fills stage[i * LDS + c] for i < K, c < NP with rows row0 .. row0+K-1
-// of its virtual matrix (zero beyond its rows / columns).
+// A source describes, for the pass starting at virtual row v0, the contiguous raw
+// rows to fetch (ptr, raw columns rc, rows available), turns the fetched raw rows
+// into Claim-1 rows in place (prep) and yields C[i][l] for the register load.
 
 struct DenseSrc {
   const double* m;
-  int64_t rows, cols, ld;
+  int64_t rows, cols;
   template <class C>
   __device__ void begin(double*, int64_t) const {}
+  __device__ int rc(int64_t) const { return (int)cols; }
+  __device__ const double* ptr(int64_t v0) const { return m + v0 * cols; }
+  __device__ int64_t avail(int64_t v0) const { return rows - v0; }
   template <class C>
-  __device__ void load(double* stage, double*, int64_t row0) const {
-    for (int idx = threadIdx.x; idx < C::K * C::NP; idx += C::THREADS) {
-      int i = idx / C::NP, c = idx - i * C::NP;
-      int64_t r = row0 + i;
-      stage[i * C::LDS + c] = (r < rows && c < cols) ? __ldg(m + r * ld + c) : 0.0;
-    }
+  __device__ void prep(double*, double*, double*, int64_t, int) const {}
+  template <class C>
+  __device__ double value(const double* raw, const double*, int64_t, int i, int l, int nrows, int rcols) const {
+    return (i < nrows && l < rcols) ? raw[i * rcols + l] : 0.0;
   }
 };
 
@@ -113,139 +163,235 @@ struct FigaroSrc {
       S[c] = s;
     }
   }
+  __device__ int rc(int64_t v0) const { return v0 < m1pad ? (int)fa.n1 : (int)fa.n2; }
+  __device__ const double* ptr(int64_t v0) const {
+    return v0 < m1pad ? fa.a + v0 * fa.n1 : fa.b + (v0 - m1pad) * fa.n2;
+  }
+  __device__ int64_t avail(int64_t v0) const { return v0 < m1pad ? fa.m1 - v0 : fa.m2 - (v0 - m1pad); }
 
+  // Per-row scalars once per row into scratch; B-part: in-place tail transform of
+  // the raw rows by a segmented scan over (segment, column) threads.
   template <class C>
-  __device__ void load(double* stage, double* S, int64_t row0) const {
-    const int n1 = (int)fa.n1, n2 = (int)fa.n2;
-    if (row0 < m1pad) {
+  __device__ void prep(double* raw, double* S, double* scratch, int64_t v0, int nrows) const {
+    const int n2 = (int)fa.n2;
+    double* c1 = scratch;                // K
+    double* c2 = scratch + C::K;         // K
+    double* mode = scratch + 2 * C::K;   // K: B-part 0 zero row / 1 group start / 2 tail row; A-part gid
+    double* ls = scratch + 3 * C::K;     // THREADS
+    double* rs = ls + C::THREADS;        // THREADS
+    if (v0 < m1pad) {
       // ---- top block rows: [sqrt(m2g) A_i | head(B_g)]
-      for (int idx = threadIdx.x; idx < C::K * C::NP; idx += C::THREADS) {
-        int i = idx / C::NP, c = idx - i * C::NP;
-        int64_t r = row0 + i;
-        double v = 0.0;
-        if (r < fa.m1 && c < n) {
-          int g = fa.gid_a ? fa.gid_a[r] : 0;
-          if (g >= 0) {
-            double m2g = fa.gid_a ? (double)fa.b_count[g] : (double)fa.m2_global;
-            if (c < n1) v = __ldg(fa.a + r * n1 + c) * sqrt(m2g);
-            else        v = fa.b_totals[(int64_t)g * n2 + (c - n1)] / sqrt(m2g);
-          }
+      for (int i = threadIdx.x; i < C::K; i += C::THREADS) {
+        int g = -1;
+        double m2g = 0.0;
+        if (i < nrows) {
+          const int64_t r = v0 + i;
+          g = fa.gid_a ? fa.gid_a[r] : 0;
+          if (g >= 0) m2g = fa.gid_a ? (double)fa.b_count[g] : (double)fa.m2_global;
         }
-        stage[i * C::LDS + c] = v;
+        c1[i] = sqrt(m2g);
+        c2[i] = g >= 0 ? rsqrt(m2g) : 0.0;
+        mode[i] = (double)g;
       }
       return;
     }
     // ---- bottom block rows: [0 | sqrt(m1g) tail(B_g)]
-    const int64_t b0 = row0 - m1pad;
-    for (int idx = threadIdx.x; idx < C::K * C::NP; idx += C::THREADS) {
-      int i = idx / C::NP, c = idx - i * C::NP;
-      if (c < n1 || c >= n) stage[i * C::LDS + c] = 0.0;
-    }
-    for (int c = threadIdx.x; c < n2; c += C::THREADS) {
-      double s = S[c];
-#pragma unroll 8
-      for (int i = 0; i < C::K; ++i) {
-        int64_t br = b0 + i;
-        double out = 0.0;
-        if (br < fa.m2) {
-          double x = __ldg(fa.b + br * n2 + c);
-          int64_t rr;       // index of this row inside its key group
-          double m1g;
-          bool valid = true;
-          if (fa.gid_b) {
-            int g = fa.gid_b[br];
-            valid = g >= 0;
-            rr = valid ? br - fa.b_start[g] : 0;
-            m1g = valid ? (double)fa.a_count[g] : 0.0;
+    //   tail_r = (sqrt(r) x - S / sqrt(r)) / sqrt(r+1) * sqrt(m1g) = c1 x - c2 S
+    const int64_t b0 = v0 - m1pad;
+    for (int i = threadIdx.x; i < C::K; i += C::THREADS) {
+      double md = 0.0, a1 = 0.0, a2 = 0.0;
+      if (i < nrows) {
+        const int64_t br = b0 + i;
+        int64_t rr = 0;
+        double m1g = 0.0;
+        bool valid = true;
+        if (fa.gid_b) {
+          const int g = fa.gid_b[br];
+          valid = g >= 0;
+          if (valid) { rr = br - fa.b_start[g]; m1g = (double)fa.a_count[g]; }
+        } else {
+          rr = fa.b_row0 + br;
+          m1g = (double)fa.m1_global;
+        }
+        if (valid) {
+          if (rr == 0) {
+            md = 1.0;
           } else {
-            rr = fa.b_row0 + br;
-            m1g = (double)fa.m1_global;
-          }
-          if (valid) {
-            if (rr == 0) {
-              s = x;  // group's first row: it only feeds the head
-            } else {
-              double si = sqrt((double)rr);
-              out = (si * x - s / si) / sqrt((double)rr + 1.0) * sqrt(m1g);
-              s += x;
-            }
+            const double si = sqrt((double)rr), si1 = sqrt((double)rr + 1.0), sm = sqrt(m1g);
+            md = 2.0;
+            a1 = si / si1 * sm;
+            a2 = sm / (si * si1);
           }
         }
-        stage[i * C::LDS + n1 + c] = out;
       }
-      S[c] = s;
+      c1[i] = a1; c2[i] = a2; mode[i] = md;
     }
+    __syncthreads();
+    if (n2 == 0) return;
+    constexpr int MAXSEG = 8;
+    const int nseg = min(MAXSEG, max(1, C::THREADS / n2));
+    const int rps = (nrows + nseg - 1) / nseg;
+    const int c = threadIdx.x % n2, seg = threadIdx.x / n2;
+    const bool active = threadIdx.x < nseg * n2;
+    double loc = 0.0, reset = 0.0;
+    if (active) {
+      for (int k = 0; k < rps; ++k) {
+        const int i = seg * rps + k;
+        if (i >= nrows) break;
+        const double xv = raw[i * n2 + c];
+        const int md = (int)mode[i];
+        if (md == 1) { loc = xv; reset = 1.0; }
+        else if (md == 2) loc += xv;
+      }
+      ls[seg * n2 + c] = loc;
+      rs[seg * n2 + c] = reset;
+    }
+    __syncthreads();
+    double sv = 0.0;
+    if (active) {
+      sv = S[c];
+      for (int k = 0; k < seg; ++k) sv = rs[k * n2 + c] != 0.0 ? ls[k * n2 + c] : sv + ls[k * n2 + c];
+    }
+    __syncthreads();  // every thread of a column has read S before the last segment rewrites it
+    if (active) {
+      for (int k = 0; k < rps; ++k) {
+        const int i = seg * rps + k;
+        if (i >= nrows) break;
+        const double xv = raw[i * n2 + c];
+        const int md = (int)mode[i];
+        double out = 0.0;
+        if (md == 1) sv = xv;
+        else if (md == 2) { out = fma(c1[i], xv, -c2[i] * sv); sv += xv; }
+        raw[i * n2 + c] = out;
+      }
+      if (seg == nseg - 1) S[c] = sv;
+    }
+  }
+
+  template <class C>
+  __device__ double value(const double* raw, const double* scratch, int64_t v0, int i, int l, int nrows,
+                          int rcols) const {
+    if (i >= nrows || l >= n) return 0.0;
+    const int n1 = (int)fa.n1;
+    if (v0 < m1pad) {
+      const int g = (int)scratch[2 * C::K + i];
+      if (g < 0) return 0.0;
+      return l < n1 ? raw[i * rcols + l] * scratch[i]
+                    : fa.b_totals[(int64_t)g * fa.n2 + (l - n1)] * scratch[C::K + i];
+    }
+    return l < n1 ? 0.0 : raw[i * rcols + (l - n1)];
   }
 };
 
+// ------------------------------------------------------------------ TMA bulk copy + mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Bounded wait: a lost transaction traps (launch error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (spin > (1u << 26)) __trap();
+  }
+}
+// thread 0: fetch `bytes16` (multiple of 16) bytes, or just complete the phase
+__device__ __forceinline__ void bulk_fetch(uint64_t* bar, void* dst, const void* src, uint32_t bytes16) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (bytes16) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes16)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(__cvta_generic_to_global(src)), "r"(bytes16), "r"(smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ panel factorisation
 // Householder factorisation of one 8-column panel held in registers by its owner
-// warp (LAPACK dlarfg convention: beta = -sign(alpha) |x|, tau = (beta-alpha)/beta,
-// v = [1; x2 / (alpha - beta)]).  Lane (g, t) holds column j0+g, rows 8*it+2*t+b.
+// warp (LAPACK dlarfg convention: beta = -sign(alpha) |x|, tau = (beta-alpha)/beta
+// = 1 + |alpha| / |x|, v = [1; x2 / (alpha - beta)]).  Lane (g, t) holds column
+// j0+g, rows 8*it+2*t+b.  Columns keep their UNscaled values x during the panel
+// (y_g = scale_g x_g); one quad reduction per column gives d_g = x_j . c_g.
 // Writes Y (both layouts), T (forward accumulation) and the panel's R rows.
 template <class C>
-__device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, const int LDR, const int j0,
-                                             double* Ys, double* Yt, double* T, double* U, double* taus,
-                                             const int lane) {
+__device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, const int j0, double* Ys,
+                                             double* Yt, double* T, double* U, double* taus, double* scs,
+                                             double* Xs, const int lane) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll 1
   for (int jj = 0; jj < 8; ++jj) {
-    double sq = 0.0;
-#pragma unroll
-    for (int it = 0; it < C::KT; ++it)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) sq = fma(cc[it][b], cc[it][b], sq);
-    sq += __shfl_xor_sync(FULL, sq, 1);
-    sq += __shfl_xor_sync(FULL, sq, 2);
-    const double sj = __shfl_sync(FULL, sq, jj * 4);
-    const double alpha = R[(j0 + jj) * LDR + j0 + jj];
-    double tau = 0.0, beta = alpha, scale = 0.0;
-    if (sj != 0.0) {
-      const double nrm = sqrt(fma(alpha, alpha, sj));
-      beta = alpha >= 0.0 ? -nrm : nrm;
-      tau = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
+    const double alpha = R[rix<C>(j0 + jj, j0 + jj)];
+    const double rjg = R[rix<C>(j0 + jj, j0 + g)];
     if (g == jj) {
 #pragma unroll
       for (int it = 0; it < C::KT; ++it)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const double y = cc[it][b] * scale;
-          cc[it][b] = y;
-          const int i = 8 * it + 2 * t + b;
-          Ys[i * C::LDY + jj] = y;
-          Yt[jj * C::LDYT + i] = y;
-        }
+        *reinterpret_cast<double2*>(Xs + 8 * it + 2 * t) = make_double2(cc[it][0], cc[it][1]);
     }
-    // R row entries of the panel, read before lane (g,0) rewrites them
-    const double rjg = R[(j0 + jj) * LDR + j0 + g];
     __syncwarp();
-    if (lane == 0) {
-      R[(j0 + jj) * LDR + j0 + jj] = beta;
-      taus[jj] = tau;
+    double xv[C::KT][2];
+    double dp[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int it = 0; it < C::KT; ++it) {
+      const double2 x2 = *reinterpret_cast<const double2*>(Xs + 8 * it + 2 * t);
+      xv[it][0] = x2.x;
+      xv[it][1] = x2.y;
+      dp[(2 * it) & 3] = fma(xv[it][0], cc[it][0], dp[(2 * it) & 3]);
+      dp[(2 * it + 1) & 3] = fma(xv[it][1], cc[it][1], dp[(2 * it + 1) & 3]);
     }
-    double d = 0.0;
-    double yv[C::KT][2];
+    double d = (dp[0] + dp[1]) + (dp[2] + dp[3]);
+    d += __shfl_xor_sync(FULL, d, 1);
+    d += __shfl_xor_sync(FULL, d, 2);
+    const double sj = __shfl_sync(FULL, d, jj * 4);
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (sj != 0.0) {
+      const double s2 = fma(alpha, alpha, sj);
+      const double rn = rsqrt_nr(s2);                  // 1 / |[alpha; x]|
+      const double nrm = s2 * rn;
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = fma(fabs(alpha), rn, 1.0);                 // (beta - alpha) / beta
+      scale = rcp_nr(alpha - beta);                    // 1 / (alpha - beta), no cancellation
+    }
+    // g > jj: c_g <- c_g - tau (R[j][g] + y_j . c_g) y_j,  y_j = scale x_j
+    const double tw = tau * fma(scale, d, rjg);
+    const double a = g > jj ? -tw * scale : 0.0;
 #pragma unroll
     for (int it = 0; it < C::KT; ++it)
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        yv[it][b] = Ys[(8 * it + 2 * t + b) * C::LDY + jj];
-        d = fma(cc[it][b], yv[it][b], d);
-      }
-    d += __shfl_xor_sync(FULL, d, 1);
-    d += __shfl_xor_sync(FULL, d, 2);
-    if (g > jj) {
-      const double tw = tau * (rjg + d);
-#pragma unroll
-      for (int it = 0; it < C::KT; ++it)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) cc[it][b] = fma(-tw, yv[it][b], cc[it][b]);
-      if (t == 0) R[(j0 + jj) * LDR + j0 + g] = rjg - tw;
-    } else if (g < jj) {
-      if (t == 0) U[g * 8 + jj] = d;  // y_g . y_jj  (for T)
+      for (int b = 0; b < 2; ++b) cc[it][b] = fma(a, xv[it][b], cc[it][b]);
+    if (t == 0) {
+      if (g > jj) R[rix<C>(j0 + jj, j0 + g)] = rjg - tw;
+      else if (g < jj) U[g * 8 + jj] = d;  // x_g . x_jj  (scaled below)
+    }
+    if (lane == 0) {
+      R[rix<C>(j0 + jj, j0 + jj)] = beta;
+      taus[jj] = tau;
+      scs[jj] = scale;
     }
     __syncwarp();
+  }
+  // Y = X diag(scale) in both layouts, written once per panel by all lanes
+  const double sg = scs[g];
+#pragma unroll
+  for (int it = 0; it < C::KT; ++it) {
+    const int i = 8 * it + 2 * t;
+    const double y0 = cc[it][0] * sg, y1 = cc[it][1] * sg;
+    Ys[i * C::LDY + g] = y0;
+    Ys[(i + 1) * C::LDY + g] = y1;
+    *reinterpret_cast<double2*>(Yt + g * C::LDYT + i) = make_double2(y0, y1);
   }
   // T (8 x 8 upper triangular): T[r][r] = tau_r,
   // T[r][j] = -tau_j sum_{m=r}^{j-1} T[r][m] (y_m . y_j); lane r builds row r.
@@ -256,10 +402,14 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
     for (int m = 0; m < 8; ++m) trow[m] = (m == r) ? taus[m] : 0.0;
 #pragma unroll
     for (int j = 1; j < 8; ++j) {
-      double acc = 0.0;
+      double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-      for (int m = 0; m < j; ++m) acc = fma(trow[m], U[m * 8 + j], acc);  // trow[m] = 0 for m < r
-      if (j > r) trow[j] = -taus[j] * acc;
+      for (int m = 0; m < j; ++m) {  // trow[m] = 0 for m < r
+        const double u = U[m * 8 + j] * (scs[m] * scs[j]);
+        if (m & 1) acc1 = fma(trow[m], u, acc1);
+        else       acc0 = fma(trow[m], u, acc0);
+      }
+      if (j > r) trow[j] = -taus[j] * (acc0 + acc1);
     }
 #pragma unroll
     for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
@@ -271,25 +421,36 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
 // of `src`, then writes R (NP x NP, row-major, zeros below the diagonal) to
 // r_out + cta * NP * NP.  For the combine step, CTA c absorbs rows of stack
 // element 2c+1 into R = element 2c.
+#ifndef JQ_PROBE
+#define JQ_PROBE 0
+#endif
+template <class C>
+__device__ __forceinline__ int pass_rows(int rcol) {
+  return rcol > 0 ? min(C::K, (C::RAW / rcol) & ~7) : C::K;
+}
+
 template <class C, class Src, bool COMBINE>
 __global__ void __launch_bounds__(C::THREADS, 1)
 tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __restrict__ r_init,
-            int64_t init_count, double* __restrict__ r_out) {
-  extern __shared__ double smem_dyn[];
-  double* stage = smem_dyn + C::OFF_STAGE;
+            int64_t init_count, double* __restrict__ r_out, int use_tma) {
+  extern __shared__ __align__(16) double smem_dyn[];
+  double* raw = smem_dyn + C::OFF_RAW;
   double* Ys0 = smem_dyn + C::OFF_YS;
   double* Yt0 = smem_dyn + C::OFF_YT;
   double* T0 = smem_dyn + C::OFF_T;
   double* U = smem_dyn + C::OFF_U;
   double* taus = smem_dyn + C::OFF_TAU;
+  double* scs = smem_dyn + C::OFF_SC;
+  double* Xs = smem_dyn + C::OFF_X;
   double* S = smem_dyn + C::OFF_S;
+  double* scratch = smem_dyn + C::OFF_LD;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int64_t cta = blockIdx.x;
 
   double* R;
-  constexpr int LDR = C::LDR;
   if constexpr (C::R_SMEM) R = smem_dyn + C::OFF_R;
   else R = r_out + cta * C::NP * C::NP;
 
@@ -298,7 +459,6 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   Src s = src;
   int64_t row_begin, row_end;
   if constexpr (COMBINE) {
-    // stack element 2c is R_init, element 2c+1 supplies the rows
     rinit = r_init + (2 * cta) * C::NP * C::NP;
     if (2 * cta + 1 < init_count) {
       s.m = r_init + (2 * cta + 1) * C::NP * C::NP;
@@ -311,26 +471,71 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
     row_end = min(total_rows, row_begin + rows_per_cta);
   }
   for (int idx = tid; idx < C::NP * C::NP; idx += C::THREADS) {
-    int r = idx / C::NP, c = idx - r * C::NP;
-    R[r * LDR + c] = rinit ? rinit[idx] : 0.0;
+    const int r = idx / C::NP, c = idx - r * C::NP;
+    if (c >= 8 * (r >> 3)) R[rix<C>(r, c)] = rinit ? rinit[idx] : 0.0;
   }
   s.template begin<C>(S, row_begin);
+  if (tid == 0) mbar_init(bar);
   __syncthreads();
 
-  // balanced column-tile ownership: warp w owns tiles w and NLT-1-w
+  // geometry of the pass starting at virtual row v0 (chunks never straddle parts)
+  auto pass_nrows = [&](int64_t v0, int rb) -> int {
+    int64_t nr = row_end - v0 < (int64_t)rb ? row_end - v0 : (int64_t)rb;
+    const int64_t av = s.avail(v0);
+    nr = av < nr ? av : nr;
+    return nr > 0 ? (int)nr : 0;
+  };
+  auto issue = [&](int64_t v0) {  // thread 0 only
+    const int rcol = s.rc(v0);
+    const int nr = pass_nrows(v0, pass_rows<C>(rcol));
+    const uint32_t bytes = uint32_t(nr) * uint32_t(rcol) * 8u;
+    bulk_fetch(bar, raw, s.ptr(v0), bytes & ~15u);
+  };
+  if (use_tma && tid == 0 && row_begin < row_end) issue(row_begin);
+
   const int lt_idx[2] = {warp, C::NLT - 1 - warp};
   double c[2][C::KT][2];
+  uint32_t phase = 0;
 
   for (int64_t row0 = row_begin; row0 < row_end; row0 += C::K) {
-    s.template load<C>(stage, S, row0);
-    __syncthreads();
+    const int rcol = s.rc(row0);
+    const int rb = pass_rows<C>(rcol);
+    const int npass = (C::K + rb - 1) / rb;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int l0 = lt_idx[q] * 8;
+    for (int q = 0; q < 2; ++q)
 #pragma unroll
-      for (int it = 0; it < C::KT; ++it)
+      for (int it = 0; it < C::KT; ++it) c[q][it][0] = c[q][it][1] = 0.0;  // rows past the range stay zero
+    for (int h = 0; h < npass && row0 + (int64_t)h * rb < row_end; ++h) {
+      const int64_t pv0 = row0 + (int64_t)h * rb;
+      const int nr = pass_nrows(pv0, rb);
+      const int nel = nr * rcol;
+      if (use_tma) {
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        if ((nel & 1) && tid == 0) raw[nel - 1] = __ldg(s.ptr(pv0) + nel - 1);  // 8-byte tail
+      } else {
+        const double* src_rows = s.ptr(pv0);
+        for (int e = tid; e < nel; e += C::THREADS) raw[e] = __ldg(src_rows + e);
+      }
+      __syncthreads();
+      s.template prep<C>(raw, S, scratch, pv0, nr);
+      __syncthreads();
 #pragma unroll
-        for (int b = 0; b < 2; ++b) c[q][it][b] = stage[(8 * it + 2 * t + b) * C::LDS + l0 + g];
+      for (int q = 0; q < 2; ++q) {
+        const int l = lt_idx[q] * 8 + g;
+#pragma unroll
+        for (int it = 0; it < C::KT; ++it)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int li = 8 * it + 2 * t + b - h * rb;
+            if (li >= 0 && li < rb) c[q][it][b] = s.template value<C>(raw, scratch, pv0, li, l, nr, rcol);
+          }
+      }
+      __syncthreads();  // raw consumed: prefetch the next pass / chunk behind the panel loop
+      if (use_tma && tid == 0) {
+        const int64_t nv0 = (h + 1 < npass) ? pv0 + rb : row0 + C::K;
+        if (nv0 < row_end) issue(nv0);
+      }
     }
 
     for (int p = 0; p < C::NLT; ++p) {
@@ -340,9 +545,9 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
       double* Yt = Yt0 + buf * C::SZ_YT;
       double* T = T0 + buf * C::SZ_T;
       const int owner = p < C::WARPS ? p : C::NLT - 1 - p;
-      if (warp == owner) {
-        if (p < C::WARPS) factor_panel<C>(c[0], R, LDR, j0, Ys, Yt, T, U, taus, lane);
-        else              factor_panel<C>(c[1], R, LDR, j0, Ys, Yt, T, U, taus, lane);
+      if (JQ_PROBE != 2 && JQ_PROBE != 3 && warp == owner) {
+        if (p < C::WARPS) factor_panel<C>(c[0], R, j0, Ys, Yt, T, U, taus, scs, Xs, lane);
+        else              factor_panel<C>(c[1], R, j0, Ys, Yt, T, U, taus, scs, Xs, lane);
       }
       __syncthreads();
 
@@ -350,21 +555,25 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int lt = lt_idx[q];
-        if (lt <= p) continue;
+        if (lt <= p || JQ_PROBE == 1 || JQ_PROBE == 3) continue;
         const int l0 = lt * 8;
-        double z[2];
-        z[0] = R[(j0 + 2 * t) * LDR + l0 + g];
-        z[1] = R[(j0 + 2 * t + 1) * LDR + l0 + g];
+        const int r0i = rix<C>(j0 + 2 * t, l0 + g), r1i = rix<C>(j0 + 2 * t + 1, l0 + g);
+        double za[2], zb[2] = {0.0, 0.0};
+        za[0] = R[r0i];
+        za[1] = R[r1i];
 #pragma unroll
-        for (int it = 0; it < C::KT; ++it) {
-          dmma(z, c[q][it][0], Ys[(8 * it + 2 * t) * C::LDY + g]);
-          dmma(z, c[q][it][1], Ys[(8 * it + 2 * t + 1) * C::LDY + g]);
+        for (int it = 0; it < C::KT; it += 2) {
+          dmma(za, c[q][it][0], Ys[(8 * it + 2 * t) * C::LDY + g]);
+          dmma(za, c[q][it][1], Ys[(8 * it + 2 * t + 1) * C::LDY + g]);
+          dmma(zb, c[q][it + 1][0], Ys[(8 * (it + 1) + 2 * t) * C::LDY + g]);
+          dmma(zb, c[q][it + 1][1], Ys[(8 * (it + 1) + 2 * t + 1) * C::LDY + g]);
         }
+        const double z0 = za[0] + zb[0], z1 = za[1] + zb[1];
         double w[2] = {0.0, 0.0};
-        dmma(w, z[0], T[(2 * t) * C::LDT + g]);
-        dmma(w, z[1], T[(2 * t + 1) * C::LDT + g]);
-        R[(j0 + 2 * t) * LDR + l0 + g] -= w[0];
-        R[(j0 + 2 * t + 1) * LDR + l0 + g] -= w[1];
+        dmma(w, z0, T[(2 * t) * C::LDT + g]);
+        dmma(w, z1, T[(2 * t + 1) * C::LDT + g]);
+        R[r0i] -= w[0];
+        R[r1i] -= w[1];
         const double nw0 = -w[0], nw1 = -w[1];
 #pragma unroll
         for (int it = 0; it < C::KT; ++it) {
@@ -377,16 +586,16 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   }
 
   // ---- write R (zeros strictly below the diagonal)
+  double* out = r_out + cta * C::NP * C::NP;
   if constexpr (C::R_SMEM) {
-    double* out = r_out + cta * C::NP * C::NP;
     for (int idx = tid; idx < C::NP * C::NP; idx += C::THREADS) {
-      int r = idx / C::NP, c2 = idx - r * C::NP;
-      out[idx] = c2 >= r ? R[r * LDR + c2] : 0.0;
+      const int r = idx / C::NP, c2 = idx - r * C::NP;
+      out[idx] = c2 >= r ? R[rix<C>(r, c2)] : 0.0;
     }
   } else {
     for (int idx = tid; idx < C::NP * C::NP; idx += C::THREADS) {
-      int r = idx / C::NP, c2 = idx - r * C::NP;
-      if (c2 < r) R[idx] = 0.0;
+      const int r = idx / C::NP, c2 = idx - r * C::NP;
+      if (c2 < r) out[idx] = 0.0;
     }
   }
 }
@@ -420,18 +629,26 @@ static int np_for(int64_t n) {
   return -1;
 }
 
-template <class C>
+template <class C, class Src>
 static int ctas_per_sm() {
-  return C::R_SMEM ? std::max(1, int((227 * 1024) / (C::SMEM + 1024))) : 1;
+  int n = 0;
+  cudaFuncSetAttribute(tsqr_kernel<C, Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tsqr_kernel<C, Src, false>, C::THREADS, C::SMEM) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    n = 1;
+  }
+  return std::max(1, n);
 }
 
 template <class C, class Src, bool COMBINE>
 static int launch_tsqr(jq_ctx* ctx, int grid, const Src& src, int64_t rows_per_cta,
-                       int64_t total_rows, const double* r_init, int64_t init_count, double* r_out) {
+                       int64_t total_rows, const double* r_init, int64_t init_count, double* r_out,
+                       int use_tma) {
   auto kern = tsqr_kernel<C, Src, COMBINE>;
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, rows_per_cta, total_rows, r_init,
-                                                   init_count, r_out);
+                                                   init_count, r_out, use_tma);
   JQ_CHECK_LAUNCH(ctx);
   return JQ_OK;
 }
@@ -442,8 +659,8 @@ template <class C>
 static int tree_combine(jq_ctx* ctx, double* a, double* b, int64_t count, double** result) {
   while (count > 1) {
     int64_t half = (count + 1) / 2;
-    DenseSrc ds{nullptr, C::NP, C::NP, C::NP};
-    JQ_TRY((launch_tsqr<C, DenseSrc, true>(ctx, (int)half, ds, 0, 0, a, count, b)));
+    DenseSrc ds{nullptr, C::NP, C::NP};
+    JQ_TRY((launch_tsqr<C, DenseSrc, true>(ctx, (int)half, ds, 0, 0, a, count, b, 1)));
     std::swap(a, b);
     count = half;
   }
@@ -464,8 +681,10 @@ size_t figaro_tsqr_ws_bytes(int64_t m1, int64_t m2, int64_t n, int sms) {
 
 template <class C, class Src>
 static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
-                      bool canonical, double* r_out) {
-  int64_t max_leaves = int64_t(ctx->sms) * ctas_per_sm<C>();
+                      bool canonical, double* r_out, int use_tma) {
+  align = std::max<int64_t>(align, C::K);
+  if (align % C::K) return fail(JQ_E_INVALID, "row alignment must be a multiple of the TSQR chunk");
+  int64_t max_leaves = int64_t(ctx->sms) * ctas_per_sm<C, Src>();
   int64_t units = std::max<int64_t>(1, cdiv(vrows, align));
   int64_t leaves = std::min(max_leaves, units);
   int64_t rows_per_cta = cdiv(units, leaves) * align;
@@ -476,7 +695,7 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   ctx->timing.tsqr_ctas = leaves;
   ctx->timing.reduced_rows = vrows;
   cudaEventRecord(ctx->ev[3], ctx->stream);
-  JQ_TRY((launch_tsqr<C, Src, false>(ctx, (int)leaves, src, rows_per_cta, vrows, nullptr, 0, a)));
+  JQ_TRY((launch_tsqr<C, Src, false>(ctx, (int)leaves, src, rows_per_cta, vrows, nullptr, 0, a, use_tma)));
   cudaEventRecord(ctx->ev[4], ctx->stream);
   double* fin = nullptr;
   JQ_TRY(tree_combine<C>(ctx, a, b, leaves, &fin));
@@ -488,21 +707,22 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
 
 template <class Src>
 static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
-                           bool canonical, double* r_out) {
+                           bool canonical, double* r_out, int use_tma) {
   switch (np_for(n)) {
-    case 16: return run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out);
-    case 32: return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out);
-    case 64: return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out);
-    case 128: return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out);
-    case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out);
+    case 16: return run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+    case 32: return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+    case 64: return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+    case 128: return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+    case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
   }
   return fail(JQ_E_INVALID, "column count above 256 is not supported by the TSQR kernels");
 }
 
 int tsqr_dense_dev(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, double* r_out,
                    bool canonical) {
-  DenseSrc src{m, rows, cols, cols};
-  return dispatch_stream(ctx, src, std::max<int64_t>(rows, 1), 64, (int)cols, canonical, r_out);
+  DenseSrc src{m, rows, cols};
+  const int tma = (reinterpret_cast<uintptr_t>(m) & 15) == 0;
+  return dispatch_stream(ctx, src, std::max<int64_t>(rows, 1), 64, (int)cols, canonical, r_out, tma);
 }
 
 __global__ void pad_stack_kernel(const double* __restrict__ rs, int64_t count, int n, int np,
@@ -551,7 +771,8 @@ int figaro_tsqr_dev(jq_ctx* ctx, const FigaroArgs& fa, double* r_out, bool canon
   src.m1pad = cdiv(fa.m1, TILE_ROWS) * TILE_ROWS;
   src.n = (int)(fa.n1 + fa.n2);
   int64_t vrows = src.m1pad + fa.m2;
-  return dispatch_stream(ctx, src, std::max<int64_t>(vrows, 1), TILE_ROWS, src.n, canonical, r_out);
+  const int tma = ((reinterpret_cast<uintptr_t>(fa.a) | reinterpret_cast<uintptr_t>(fa.b)) & 15) == 0;
+  return dispatch_stream(ctx, src, std::max<int64_t>(vrows, 1), TILE_ROWS, src.n, canonical, r_out, tma);
 }
 
 int canonicalize_dev(jq_ctx* ctx, const double* r, int64_t n, double* out) {
