@@ -284,15 +284,18 @@ def main():
                         "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
                         "algorithmic": f"8*m2*n2 = {8 * m * n} bytes read"}
 
-    # ---- end-to-end through the public API with host buffers (rank 0 view, N=1)
+    # ---- end-to-end through the public API with host buffers (N=1)
     e2e = None
     if world == 1 and not args.no_e2e:
-        e2e = run_e2e(args, cfg, A, B, ka, kb, jrows)
+        host = to_host(A, B, ka, kb)
+        del A, B
         A = B = None
+        torch.cuda.empty_cache()
+        e2e = run_e2e(args, host, jrows)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        del A, B
+        A = B = None
         torch.cuda.empty_cache()
         try:
             ra = argparse.Namespace(**vars(args))
@@ -317,26 +320,32 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(args, cfg, A, B, ka, kb, jrows):
-    """figaro_r(Table(host), Table(host)): H2D of both tables from pinned host memory
-    and the D2H of R inside the timed region, every step."""
+def to_host(A, B, ka, kb):
+    """Copy the device tables into page-locked host memory (outside any timing)."""
+    import torch
+    cudart = torch.cuda.cudart()
+    host = {}
+    for name, t in (("A", A), ("B", B)):
+        h = np.empty(tuple(t.shape), dtype=np.float64)
+        rc = cudart.cudaHostRegister(h.ctypes.data, h.nbytes, 0)
+        pinned = (int(rc) if not hasattr(rc, "value") else rc.value) == 0
+        torch.cuda.synchronize()
+        torch.from_numpy(h).copy_(t)
+        host[name] = (h, pinned)
+    host["ka"] = ka.cpu().numpy() if ka is not None else None
+    host["kb"] = kb.cpu().numpy() if kb is not None else None
+    return host
+
+
+def run_e2e(args, host, jrows):
+    """figaro_r(Table(host), Table(host)) through the public API: the H2D copy of both
+    tables (page-locked host memory) and the D2H of R are inside the timed region."""
     import torch
     import paper_2503_23385_b200 as P
-    host = {}
     cudart = torch.cuda.cudart()
     try:
-        for name, t in (("A", A), ("B", B)):
-            h = np.empty(tuple(t.shape), dtype=np.float64)
-            rc = cudart.cudaHostRegister(h.ctypes.data, h.nbytes, 0)
-            pinned = int(rc) == 0 if not hasattr(rc, "value") else rc.value == 0
-            torch.cuda.synchronize()
-            torch.from_numpy(h).copy_(t)      # D2H once (outside timing)
-            host[name] = (h, pinned)
-        hka = ka.cpu().numpy() if ka is not None else None
-        hkb = kb.cpu().numpy() if kb is not None else None
-        del A, B
-        torch.cuda.empty_cache()
-        ta, tb = P.Table(host["A"][0], hka), P.Table(host["B"][0], hkb)
+        ta = P.Table(host["A"][0], host["ka"])
+        tb = P.Table(host["B"][0], host["kb"])
         nsteps = max(1, min(args.steps, 3))
         P.figaro_r(ta, tb)                     # warm-up (workspace sizing)
         times = []
@@ -345,13 +354,16 @@ def run_e2e(args, cfg, A, B, ka, kb, jrows):
             r = P.figaro_r(ta, tb)              # returns after the D2H of R
             times.append(time.perf_counter() - t0)
         t = float(np.mean(times))
-        h2d = sum(h.nbytes for h, _ in host.values()) + (hka.nbytes + hkb.nbytes if hka is not None else 0)
+        h2d = host["A"][0].nbytes + host["B"][0].nbytes
+        if host["ka"] is not None:
+            h2d += host["ka"].nbytes + host["kb"].nbytes
         return {"value": jrows / t, "unit": "join rows/s", "ms_per_step": t * 1e3, "steps": nsteps,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(r.nbytes),
-                "pinned": all(p for _, p in host.values()),
+                "pinned": bool(host["A"][1] and host["B"][1]),
                 "api": "paper_2503_23385_b200.figaro_r(Table(numpy), Table(numpy)) -> jq_figaro_r"}
     finally:
-        for h, pinned in host.values():
+        for key in ("A", "B"):
+            h, pinned = host[key]
             if pinned:
                 cudart.cudaHostUnregister(h.ctypes.data)
 

@@ -85,7 +85,7 @@ struct Cfg {
   static constexpr bool R_SMEM = NP <= 128;
   // R packed by 8-row panels: panel p holds rows 8p..8p+7, columns 8p..NP-1,
   // row stride NP - 8p + 2 (== 2 or 10 mod 16: conflict-free DMMA fragment access)
-  static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
+  __host__ __device__ static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
   static constexpr int LDY = 10;            // Ys  (K x 8)
   static constexpr int LDYT = K + 2;        // Yt  (8 x K)
   static constexpr int LDT = 10;            // T   (8 x 8)
@@ -321,6 +321,17 @@ __device__ __forceinline__ void bulk_fetch(uint64_t* bar, void* dst, const void*
 }
 
 // ------------------------------------------------------------------ panel factorisation
+#ifdef JQ_PANEL_TIMING
+__device__ long long g_ptime[16];
+#define PT(i)                                                   \
+  do {                                                          \
+    long long now_ = clock64();                                 \
+    if (threadIdx.x == 0) g_ptime[i] += now_ - pt_last;         \
+    pt_last = now_;                                             \
+  } while (0)
+#else
+#define PT(i) do {} while (0)
+#endif
 // Householder factorisation of one 8-column panel held in registers by its owner
 // warp (LAPACK dlarfg convention: beta = -sign(alpha) |x|, tau = (beta-alpha)/beta
 // = 1 + |alpha| / |x|, v = [1; x2 / (alpha - beta)]).  Lane (g, t) holds column
@@ -332,6 +343,9 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
                                              double* Yt, double* T, double* U, double* taus, double* scs,
                                              double* Xs, const int lane) {
   const int g = lane >> 2, t = lane & 3;
+#ifdef JQ_PANEL_TIMING
+  long long pt_last = clock64();
+#endif
 #pragma unroll 1
   for (int jj = 0; jj < 8; ++jj) {
     const double alpha = R[rix<C>(j0 + jj, j0 + jj)];
@@ -342,6 +356,7 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
         *reinterpret_cast<double2*>(Xs + 8 * it + 2 * t) = make_double2(cc[it][0], cc[it][1]);
     }
     __syncwarp();
+    PT(0);
     double xv[C::KT][2];
     double dp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -355,6 +370,7 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
     double d = (dp[0] + dp[1]) + (dp[2] + dp[3]);
     d += __shfl_xor_sync(FULL, d, 1);
     d += __shfl_xor_sync(FULL, d, 2);
+    PT(1);
     const double sj = __shfl_sync(FULL, d, jj * 4);
     double tau = 0.0, beta = alpha, scale = 0.0;
     if (sj != 0.0) {
@@ -365,6 +381,7 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
       tau = fma(fabs(alpha), rn, 1.0);                 // (beta - alpha) / beta
       scale = rcp_nr(alpha - beta);                    // 1 / (alpha - beta), no cancellation
     }
+    PT(3);
     // g > jj: c_g <- c_g - tau (R[j][g] + y_j . c_g) y_j,  y_j = scale x_j
     const double tw = tau * fma(scale, d, rjg);
     const double a = g > jj ? -tw * scale : 0.0;
@@ -382,6 +399,7 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
       scs[jj] = scale;
     }
     __syncwarp();
+    PT(4);
   }
   // Y = X diag(scale) in both layouts, written once per panel by all lanes
   const double sg = scs[g];
@@ -414,6 +432,7 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
 #pragma unroll
     for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
   }
+  PT(5);
 }
 
 // ------------------------------------------------------------------ the kernel
