@@ -44,6 +44,7 @@ _EXPORTS = {
     "GenSpec": ".datagen",
     "gen_uniform": ".datagen",
     "set_device": "._native",
+    "set_variant": "._native",
     "last_timing": "._native",
 }
 

@@ -104,6 +104,21 @@ def set_device(device: int) -> None:
         _tls.ctx = None
 
 
+VARIANTS = {"dense": 0, "footnote": 1}
+_variant = VARIANTS[os.environ.get("JOINQR_VARIANT", "dense")]
+
+
+def set_variant(name: str) -> None:
+    """figaro_r / figaro_svd internal reduction: "dense" = the Claim-1 reduced matrix
+    (north star), "footnote" = head/tail of BOTH sides (PAPER.md:59
+    footnote, 4x fewer TSQR flops at n1 = n2).  Same R (Gram-identical), parity-tested."""
+    global _variant
+    _variant = VARIANTS[name]
+    c = getattr(_tls, "ctx", None)
+    if c is not None:
+        check(load_library().jq_ctx_set_variant(c, _variant))
+
+
 def ctx():
     """This thread's library context (created on first use)."""
     c = getattr(_tls, "ctx", None)
@@ -111,6 +126,7 @@ def ctx():
         lib = load_library()
         h = _P()
         check(lib.jq_ctx_create(_device, C.byref(h)))
+        check(lib.jq_ctx_set_variant(h, _variant))
         _tls.ctx, _tls.device = h, _device
         c = h
     return c

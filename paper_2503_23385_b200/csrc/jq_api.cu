@@ -8,7 +8,11 @@
 //           -> canonical R, exact zeros below the diagonal.
 // Validation flags (unsorted keys, Jacobi non-convergence) are raised on the
 // device and read once at the end of the call.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <utility>
 #include <string>
 
 #include "jq_internal.cuh"
@@ -82,14 +86,152 @@ static float ev_ms(jq_ctx* ctx, int a, int b) {
 // Workspace needed by figaro_r_dev for these sizes (inputs already on device).
 static size_t figaro_ws(int64_t m1, int64_t n1, int64_t m2, int64_t n2, bool keyed, int sms) {
   const int64_t cap = keyed ? std::max<int64_t>(1, std::min(m1, m2)) : 1;
-  return (keyed ? group_ws_bytes(m1, m2) : 0) + segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) +
-         figaro_tsqr_ws_bytes(m1, m2, n1 + n2, sms) + ws_bytes(size_t(n1 + n2) * (n1 + n2), 8);
+  const int64_t n = n1 + n2;
+  size_t dense = (keyed ? group_ws_bytes(m1, m2) : 0) + segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) +
+                 figaro_tsqr_ws_bytes(m1, m2, n, sms) + ws_bytes(size_t(n) * n, 8);
+  size_t foot = (keyed ? group_ws_bytes(m1, m2) : 0) + segscan_ws_bytes(m1, std::max<int64_t>(n1, 1), cap) +
+                segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) + tsqr_ws_bytes(m1 + TILE_ROWS, n1, sms) +
+                tsqr_ws_bytes(m2 + TILE_ROWS, n2, sms) + tsqr_ws_bytes(cap, n, sms) +
+                tsqr_ws_bytes(3 * n, n, sms) + ws_bytes(size_t(cap) * n, 8) + 8 * ws_bytes(size_t(n) * n, 8);
+  return std::max(dense, foot);
+}
+
+// ---- footnote variant (PAPER.md:59 footnote) -------------
+// Head/tail BOTH sides per key group.  With hA_g = colsum(A_g)/sqrt(m1g) and
+// hB_g = colsum(B_g)/sqrt(m2g), J^T J = sum_g hr_g^T hr_g + diag(sum_g m2g TA_g^T TA_g,
+// sum_g m1g TB_g^T TB_g) with the head row hr_g = [sqrt(m2g) hA_g | sqrt(m1g) hB_g]
+// (same Gram as the Claim-1 matrix, hence the same canonical R).  TSQR work drops
+// from 2 (m1+m2) N^2 to 2 (m1 n1^2 + m2 n2^2) + 2 G N^2.
+__global__ void head_rows_kernel(const double* __restrict__ totA, int n1, const double* __restrict__ totB, int n2,
+                                 const int64_t* __restrict__ a_count, const int64_t* __restrict__ b_count,
+                                 int64_t ng, int64_t m1_all, int64_t m2_all, double* __restrict__ out) {
+  const int n = n1 + n2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < ng * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = idx / n;
+    const int c = (int)(idx - g * n);
+    const double m1g = a_count ? (double)a_count[g] : (double)m1_all;
+    const double m2g = b_count ? (double)b_count[g] : (double)m2_all;
+    out[idx] = c < n1 ? sqrt(m2g) * (totA[g * n1 + c] / sqrt(m1g))
+                      : sqrt(m1g) * (totB[g * n2 + (c - n1)] / sqrt(m2g));
+  }
+}
+
+// stack [R_H ; R_A (top-left) ; R_B (bottom-right)] as three n x n factors
+__global__ void footnote_stack_kernel(const double* __restrict__ rh, const double* __restrict__ ra, int n1,
+                                      const double* __restrict__ rb, int n2, double* __restrict__ out) {
+  const int n = n1 + n2;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 3 * n * n; idx += gridDim.x * blockDim.x) {
+    const int k = idx / (n * n), rem = idx - k * n * n, r = rem / n, c = rem - r * n;
+    double v = 0.0;
+    if (k == 0) v = rh ? rh[rem] : 0.0;
+    else if (k == 1) v = (r < n1 && c < n1) ? ra[r * n1 + c] : 0.0;
+    else v = (r >= n1 && c >= n1) ? rb[(r - n1) * n2 + (c - n1)] : 0.0;
+    out[idx] = v;
+  }
+}
+
+static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
+                                 const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
+  const bool keyed = ka != nullptr;
+  const int64_t n = n1 + n2;
+  cudaEventRecord(ctx->ev[0], ctx->stream);
+  Groups gr;
+  int64_t ng = 1;
+  if (keyed) {
+    JQ_TRY(group_keys_dev(ctx, ka, m1, kb, m2, &gr));
+    int64_t hn[2];
+    JQ_CUDA(cudaMemcpyAsync(hn, gr.d_n, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    JQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    ng = hn[0];
+  }
+  cudaEventRecord(ctx->ev[1], ctx->stream);
+  const int64_t cap = keyed ? gr.cap : 1;
+  SegScan sa{}, sb{};
+  if (n1 > 0)
+    JQ_TRY(segscan_dev(ctx, a, m1, n1, keyed ? gr.gid_a : nullptr, keyed ? gr.a_start : nullptr,
+                       keyed ? gr.a_count : nullptr, keyed ? gr.d_n : nullptr, cap, &sa));
+  if (n2 > 0)
+    JQ_TRY(segscan_dev(ctx, b, m2, n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
+                       keyed ? gr.b_count : nullptr, keyed ? gr.d_n : nullptr, cap, &sb));
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  double* ra = ws_alloc<double>(ctx, std::max<int64_t>(n1 * n1, 1));
+  double* rb = ws_alloc<double>(ctx, std::max<int64_t>(n2 * n2, 1));
+  double* rh = ws_alloc<double>(ctx, n * n);
+  double* stack = ws_alloc<double>(ctx, 3 * n * n);
+  double* heads = ws_alloc<double>(ctx, std::max<int64_t>(ng, 1) * n);
+  if (!ra || !rb || !rh || !stack || !heads) return fail(JQ_E_OOM, "workspace exhausted (footnote variant)");
+  ctx->record_tsqr_events = false;
+  ctx->timing.tsqr_ctas = 0;
+  ctx->timing.reduced_rows = 0;
+  cudaEventRecord(ctx->ev[3], ctx->stream);
+  // tails of A scaled by sqrt(m2g): the "B-part" of a source with an empty A-part
+  FigaroArgs fa{};
+  if (n1 > 0) {
+    fa.b = a; fa.m2 = m1; fa.n2 = n1;
+    fa.gid_b = keyed ? gr.gid_a : nullptr;
+    fa.b_start = keyed ? gr.a_start : nullptr;
+    fa.a_count = keyed ? gr.b_count : nullptr;
+    fa.b_carry = sa.carry;
+    fa.m1_global = m2; fa.m2_global = m1; fa.b_row0 = 0;
+    int rc = figaro_tsqr_dev(ctx, fa, ra, false);
+    if (rc) { ctx->record_tsqr_events = true; return rc; }
+  }
+  if (n2 > 0) {
+    FigaroArgs fb{};
+    fb.b = b; fb.m2 = m2; fb.n2 = n2;
+    fb.gid_b = keyed ? gr.gid_b : nullptr;
+    fb.b_start = keyed ? gr.b_start : nullptr;
+    fb.a_count = keyed ? gr.a_count : nullptr;
+    fb.b_carry = sb.carry;
+    fb.m1_global = m1; fb.m2_global = m2; fb.b_row0 = 0;
+    int rc = figaro_tsqr_dev(ctx, fb, rb, false);
+    if (rc) { ctx->record_tsqr_events = true; return rc; }
+  }
+  cudaEventRecord(ctx->ev[4], ctx->stream);
+  // head rows (G x n) -> R_H, then the final 3-factor stack -> canonical R
+  const double* zeros_dummy = nullptr;
+  (void)zeros_dummy;
+  if (ng > 0) {
+    head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng * n, 256), 4096), 256, 0, ctx->stream>>>(
+        sa.totals, (int)n1, sb.totals, (int)n2, keyed ? gr.a_count : nullptr, keyed ? gr.b_count : nullptr,
+        ng, m1, m2, heads);
+    JQ_CHECK_LAUNCH(ctx);
+    int rc = tsqr_dense_dev(ctx, heads, ng, n, rh, false);
+    if (rc) { ctx->record_tsqr_events = true; return rc; }
+  } else {
+    JQ_CUDA(cudaMemsetAsync(rh, 0, n * n * 8, ctx->stream));
+  }
+  if (getenv("JQ_DEBUG_FOOTNOTE")) {
+    cudaStreamSynchronize(ctx->stream);
+    auto nan_count = [&](const double* d, int64_t cnt) {
+      std::vector<double> h(cnt);
+      cudaMemcpy(h.data(), d, cnt * 8, cudaMemcpyDeviceToHost);
+      int64_t k = 0; double mx = 0;
+      for (double v : h) { k += (v != v); mx = std::max(mx, std::fabs(v)); }
+      return std::make_pair(k, mx);
+    };
+    auto a1 = nan_count(ra, n1 * n1), b1 = nan_count(rb, n2 * n2), h1 = nan_count(rh, n * n),
+         hh = nan_count(heads, ng * n);
+    fprintf(stderr, "footnote debug: R_A nan=%ld max=%g  R_B nan=%ld max=%g  R_H nan=%ld max=%g  heads nan=%ld max=%g\n",
+            (long)a1.first, a1.second, (long)b1.first, b1.second, (long)h1.first, h1.second, (long)hh.first, hh.second);
+  }
+  footnote_stack_kernel<<<(unsigned)cdiv(3 * n * n, 256), 256, 0, ctx->stream>>>(
+      rh, n1 > 0 ? ra : nullptr, (int)n1, n2 > 0 ? rb : nullptr, (int)n2, stack);
+  JQ_CHECK_LAUNCH(ctx);
+  int rc = tsqr_stack_dev(ctx, stack, 3, n, r_out, true);
+  ctx->record_tsqr_events = true;
+  cudaEventRecord(ctx->ev[5], ctx->stream);
+  return rc;
 }
 
 // Device-resident figaro_r: R (n x n, canonical) into r_out (device).
 static int figaro_r_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
                         const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
+  if (ctx->variant == 1) return figaro_r_footnote_dev(ctx, a, m1, n1, ka, b, m2, n2, kb, r_out);
   const bool keyed = ka != nullptr;
+  ctx->timing.tsqr_ctas = 0;
+  ctx->timing.reduced_rows = 0;
   cudaEventRecord(ctx->ev[0], ctx->stream);
   Groups gr;
   if (keyed) JQ_TRY(group_keys_dev(ctx, ka, m1, kb, m2, &gr));
@@ -196,7 +338,7 @@ int jq_ctx_sync(jq_ctx* ctx) {
 
 int jq_ctx_set_variant(jq_ctx* ctx, int variant) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
-  if (variant != 0) return fail(JQ_E_INVALID, "only variant 0 (dense Claim-1 reduction) is built");
+  if (variant != 0 && variant != 1) return fail(JQ_E_INVALID, "variant must be 0 (dense) or 1 (footnote)");
   ctx->variant = variant;
   return JQ_OK;
 }

@@ -326,7 +326,7 @@ __device__ long long g_ptime[16];
 #define PT(i)                                                   \
   do {                                                          \
     long long now_ = clock64();                                 \
-    if (threadIdx.x == 0) g_ptime[i] += now_ - pt_last;         \
+    pt_acc[i] += now_ - pt_last;                                \
     pt_last = now_;                                             \
   } while (0)
 #else
@@ -343,13 +343,20 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
                                              double* Yt, double* T, double* U, double* taus, double* scs,
                                              double* Xs, const int lane) {
   const int g = lane >> 2, t = lane & 3;
+  // The panel's R rows are final at panel start (reflector jj rewrites only row
+  // j0+jj), so the next column's entries are prefetched one column ahead.
+  double alpha_n = R[rix<C>(j0, j0)], rg_n = R[rix<C>(j0, j0 + g)];
 #ifdef JQ_PANEL_TIMING
-  long long pt_last = clock64();
+  long long pt_last = clock64(), pt_acc[6] = {0, 0, 0, 0, 0, 0};
 #endif
+  double tau_r = 0.0, scale_r = 0.0;  // lane r < 8 keeps tau_r / scale_r of column r
 #pragma unroll 1
   for (int jj = 0; jj < 8; ++jj) {
-    const double alpha = R[rix<C>(j0 + jj, j0 + jj)];
-    const double rjg = R[rix<C>(j0 + jj, j0 + g)];
+    const double alpha = alpha_n, rgj = rg_n;
+    if (jj < 7) {
+      alpha_n = R[rix<C>(j0 + jj + 1, j0 + jj + 1)];
+      rg_n = R[rix<C>(j0 + jj + 1, j0 + g)];
+    }
     if (g == jj) {
 #pragma unroll
       for (int it = 0; it < C::KT; ++it)
@@ -358,16 +365,18 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
     __syncwarp();
     PT(0);
     double xv[C::KT][2];
-    double dp[4] = {0.0, 0.0, 0.0, 0.0};
+    double dp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dp[u] = 0.0;
 #pragma unroll
     for (int it = 0; it < C::KT; ++it) {
       const double2 x2 = *reinterpret_cast<const double2*>(Xs + 8 * it + 2 * t);
       xv[it][0] = x2.x;
       xv[it][1] = x2.y;
-      dp[(2 * it) & 3] = fma(xv[it][0], cc[it][0], dp[(2 * it) & 3]);
-      dp[(2 * it + 1) & 3] = fma(xv[it][1], cc[it][1], dp[(2 * it + 1) & 3]);
+      dp[(2 * it) & 7] = fma(xv[it][0], cc[it][0], dp[(2 * it) & 7]);
+      dp[(2 * it + 1) & 7] = fma(xv[it][1], cc[it][1], dp[(2 * it + 1) & 7]);
     }
-    double d = (dp[0] + dp[1]) + (dp[2] + dp[3]);
+    double d = ((dp[0] + dp[1]) + (dp[2] + dp[3])) + ((dp[4] + dp[5]) + (dp[6] + dp[7]));
     d += __shfl_xor_sync(FULL, d, 1);
     d += __shfl_xor_sync(FULL, d, 2);
     PT(1);
@@ -375,32 +384,37 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
     double tau = 0.0, beta = alpha, scale = 0.0;
     if (sj != 0.0) {
       const double s2 = fma(alpha, alpha, sj);
-      const double rn = rsqrt_nr(s2);                  // 1 / |[alpha; x]|
-      const double nrm = s2 * rn;
-      beta = alpha >= 0.0 ? -nrm : nrm;
-      tau = fma(fabs(alpha), rn, 1.0);                 // (beta - alpha) / beta
-      scale = rcp_nr(alpha - beta);                    // 1 / (alpha - beta), no cancellation
+      if (s2 > 1e-280 && s2 < 1e280) {                 // warp-uniform: fast MUFU + Newton path
+        const double rn = rsqrt_nr(s2);                // 1 / |[alpha; x]|
+        const double nrm = s2 * rn;
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = fma(fabs(alpha), rn, 1.0);               // (beta - alpha) / beta
+        scale = rcp_nr(alpha - beta);                  // 1 / (alpha - beta), no cancellation
+      } else {                                         // IEEE path (ftz approximations would flush)
+        const double nrm = sqrt(alpha * alpha + sj);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
     }
     PT(3);
     // g > jj: c_g <- c_g - tau (R[j][g] + y_j . c_g) y_j,  y_j = scale x_j
-    const double tw = tau * fma(scale, d, rjg);
+    const double tw = tau * fma(scale, d, rgj);
     const double a = g > jj ? -tw * scale : 0.0;
 #pragma unroll
     for (int it = 0; it < C::KT; ++it)
 #pragma unroll
       for (int b = 0; b < 2; ++b) cc[it][b] = fma(a, xv[it][b], cc[it][b]);
     if (t == 0) {
-      if (g > jj) R[rix<C>(j0 + jj, j0 + g)] = rjg - tw;
-      else if (g < jj) U[g * 8 + jj] = d;  // x_g . x_jj  (scaled below)
+      if (g > jj) R[rix<C>(j0 + jj, j0 + g)] = rgj - tw;
+      else if (g < jj) U[g * 8 + jj] = d;  // x_g . x_jj  (scaled in T below)
+      else R[rix<C>(j0 + jj, j0 + jj)] = beta;
     }
-    if (lane == 0) {
-      R[rix<C>(j0 + jj, j0 + jj)] = beta;
-      taus[jj] = tau;
-      scs[jj] = scale;
-    }
-    __syncwarp();
+    if (lane == jj) { tau_r = tau; scale_r = scale; }
     PT(4);
   }
+  if (lane < 8) { taus[lane] = tau_r; scs[lane] = scale_r; }
+  __syncwarp();
   // Y = X diag(scale) in both layouts, written once per panel by all lanes
   const double sg = scs[g];
 #pragma unroll
@@ -415,24 +429,26 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
   // T[r][j] = -tau_j sum_{m=r}^{j-1} T[r][m] (y_m . y_j); lane r builds row r.
   if (lane < 8) {
     const int r = lane;
-    double trow[8];
+    double trow[8], sc[8], tu[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) trow[m] = (m == r) ? taus[m] : 0.0;
+    for (int m = 0; m < 8; ++m) { sc[m] = scs[m]; tu[m] = taus[m]; }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) trow[m] = (m == r) ? tu[m] : 0.0;
 #pragma unroll
     for (int j = 1; j < 8; ++j) {
-      double acc0 = 0.0, acc1 = 0.0;
+      double acc = 0.0;
 #pragma unroll
-      for (int m = 0; m < j; ++m) {  // trow[m] = 0 for m < r
-        const double u = U[m * 8 + j] * (scs[m] * scs[j]);
-        if (m & 1) acc1 = fma(trow[m], u, acc1);
-        else       acc0 = fma(trow[m], u, acc0);
-      }
-      if (j > r) trow[j] = -taus[j] * (acc0 + acc1);
+      for (int m = 0; m < j; ++m) acc = fma(trow[m], (U[m * 8 + j] * sc[m]) * sc[j], acc);  // trow[m] = 0 for m < r
+      if (j > r) trow[j] = -tu[j] * acc;
     }
 #pragma unroll
     for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
   }
   PT(5);
+#ifdef JQ_PANEL_TIMING
+  if (lane == 0)
+    for (int i = 0; i < 6; ++i) g_ptime[i] += pt_acc[i];
+#endif
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -498,19 +514,22 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   __syncthreads();
 
   // geometry of the pass starting at virtual row v0 (chunks never straddle parts)
-  auto pass_nrows = [&](int64_t v0, int rb) -> int {
-    int64_t nr = row_end - v0 < (int64_t)rb ? row_end - v0 : (int64_t)rb;
+  // rows of the pass starting at v0: never past its chunk (the prefix state S must
+  // not run ahead), the CTA range or the source
+  auto pass_nrows = [&](int64_t v0, int rb, int64_t chunk0) -> int {
+    int64_t lim = chunk0 + C::K < row_end ? chunk0 + C::K : row_end;
+    int64_t nr = lim - v0 < (int64_t)rb ? lim - v0 : (int64_t)rb;
     const int64_t av = s.avail(v0);
     nr = av < nr ? av : nr;
     return nr > 0 ? (int)nr : 0;
   };
-  auto issue = [&](int64_t v0) {  // thread 0 only
+  auto issue = [&](int64_t v0, int64_t chunk0) {  // thread 0 only
     const int rcol = s.rc(v0);
-    const int nr = pass_nrows(v0, pass_rows<C>(rcol));
+    const int nr = pass_nrows(v0, pass_rows<C>(rcol), chunk0);
     const uint32_t bytes = uint32_t(nr) * uint32_t(rcol) * 8u;
     bulk_fetch(bar, raw, s.ptr(v0), bytes & ~15u);
   };
-  if (use_tma && tid == 0 && row_begin < row_end) issue(row_begin);
+  if (use_tma && tid == 0 && row_begin < row_end) issue(row_begin, row_begin);
 
   const int lt_idx[2] = {warp, C::NLT - 1 - warp};
   double c[2][C::KT][2];
@@ -526,7 +545,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
       for (int it = 0; it < C::KT; ++it) c[q][it][0] = c[q][it][1] = 0.0;  // rows past the range stay zero
     for (int h = 0; h < npass && row0 + (int64_t)h * rb < row_end; ++h) {
       const int64_t pv0 = row0 + (int64_t)h * rb;
-      const int nr = pass_nrows(pv0, rb);
+      const int nr = pass_nrows(pv0, rb, row0);
       const int nel = nr * rcol;
       if (use_tma) {
         mbar_wait(bar, phase);
@@ -552,8 +571,9 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
       }
       __syncthreads();  // raw consumed: prefetch the next pass / chunk behind the panel loop
       if (use_tma && tid == 0) {
-        const int64_t nv0 = (h + 1 < npass) ? pv0 + rb : row0 + C::K;
-        if (nv0 < row_end) issue(nv0);
+        const bool same = h + 1 < npass && pv0 + rb < row_end;
+        const int64_t nv0 = same ? pv0 + rb : row0 + C::K;
+        if (nv0 < row_end) issue(nv0, same ? row0 : nv0);
       }
     }
 
@@ -711,16 +731,16 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   double* a = ws_alloc<double>(ctx, size_t(leaves) * C::NP * C::NP);
   double* b = ws_alloc<double>(ctx, size_t((leaves + 1) / 2) * C::NP * C::NP + 1);
   if (!a || !b) return fail(JQ_E_OOM, "workspace exhausted (TSQR leaves)");
-  ctx->timing.tsqr_ctas = leaves;
-  ctx->timing.reduced_rows = vrows;
-  cudaEventRecord(ctx->ev[3], ctx->stream);
+  ctx->timing.tsqr_ctas += leaves;
+  ctx->timing.reduced_rows += vrows;
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
   JQ_TRY((launch_tsqr<C, Src, false>(ctx, (int)leaves, src, rows_per_cta, vrows, nullptr, 0, a, use_tma)));
-  cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
   double* fin = nullptr;
   JQ_TRY(tree_combine<C>(ctx, a, b, leaves, &fin));
   finalize_r_kernel<<<(int)cdiv(int64_t(n) * n, 256), 256, 0, ctx->stream>>>(fin, C::NP, n, canonical, r_out);
   JQ_CHECK_LAUNCH(ctx);
-  cudaEventRecord(ctx->ev[5], ctx->stream);
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[5], ctx->stream);
   return JQ_OK;
 }
 

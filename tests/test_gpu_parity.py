@@ -160,12 +160,20 @@ def test_householder_r(P, rows, cols):
         check_r(P.canonicalize(r), O.canonicalize(ref))
 
 
+@pytest.fixture(params=["dense", "footnote"])
+def variant(request, P):
+    P.set_variant(request.param)
+    yield request.param
+    P.set_variant("dense")
+
+
 @pytest.mark.parametrize("m1,n1,m2,n2,groups", [
     (2, 1, 2, 1, None), (1, 3, 1, 2, None), (1, 1, 9, 4, None), (7, 4, 1, 3, None),
     (1000, 4, 1000, 4, None), (3000, 8, 2000, 8, None), (4000, 32, 5000, 32, None),
-    (2500, 64, 2500, 64, None), (3000, 100, 2000, 120, None),
-    (400, 5, 300, 6, 40), (6000, 16, 7000, 16, 600), (20000, 32, 20000, 32, 100)])
-def test_figaro_r_matches_oracle(P, m1, n1, m2, n2, groups):
+    (2500, 64, 2500, 64, None), (3000, 100, 2000, 120, None), (5000, 128, 4000, 128, None),
+    (400, 5, 300, 6, 40), (6000, 16, 7000, 16, 600), (20000, 32, 20000, 32, 100),
+    (3000, 7, 2000, 3, 2500)])
+def test_figaro_r_matches_oracle(P, variant, m1, n1, m2, n2, groups):
     rng = np.random.default_rng(m1 + 3 * m2 + n1 + (groups or 0))
     a, b = rand_tables(rng, m1, n1, m2, n2, groups)
     r = np.asarray(P.figaro_r(to_p(P, a), to_p(P, b)))
@@ -176,7 +184,7 @@ def test_figaro_r_matches_oracle(P, m1, n1, m2, n2, groups):
     assert np.abs(r.T @ r - g).max() <= 1e-10 * max(1, np.abs(g).max())
 
 
-def test_figaro_r_empty_join_and_materialised(P):
+def test_figaro_r_empty_join_and_materialised(P, variant):
     a = P.Table(np.ones((2, 2)), [1, 1])
     b = P.Table(np.ones((3, 1)), [2, 2, 2])
     assert np.array_equal(P.figaro_r(a, b), np.zeros((3, 3)))
@@ -215,7 +223,7 @@ def test_svd_rank_deficient_and_zero(P):
 
 
 @pytest.mark.parametrize("m,n,groups", [(1000, 4, None), (3000, 16, None), (5000, 64, None), (4000, 16, 300)])
-def test_figaro_svd_matches_oracle(P, m, n, groups):
+def test_figaro_svd_matches_oracle(P, variant, m, n, groups):
     rng = np.random.default_rng(m + n)
     a, b = rand_tables(rng, m, n, m + 17, n, groups)
     s = P.figaro_svd(to_p(P, a), to_p(P, b), True)
@@ -288,7 +296,7 @@ def test_device_tensors_in_place(P):
     check_r(r.cpu().numpy(), np.asarray(P.figaro_r(P.Table(A), P.Table(B))), 1e-14)
 
 
-def test_determinism(P):
+def test_determinism(P, variant):
     rng = np.random.default_rng(8)
     a, b = P.Table(rng.random((30000, 16))), P.Table(rng.random((30000, 16)))
     r1, r2 = P.figaro_r(a, b), P.figaro_r(a, b)
