@@ -159,6 +159,22 @@ def make_inputs(cfg_id, rank, world, device):
     return A, B, ka, kb, a0
 
 
+def tsqr_flops(variant, cfg, m, n, st):
+    """Algorithmic TSQR flops of one step (2*rows*N^2 - 2/3 N^3 per Householder QR)."""
+    nn = 2 * n
+    if cfg["keys"] is None:
+        rows_a = rows_b = m - 1   # tails of each side (one group); dense: m1 + m2 - 1 rows
+    else:
+        rows_a = rows_b = None
+    if variant == "dense":
+        mr = (2 * m - 1) if cfg["keys"] is None else float(st["reduced_rows"])
+        return 2.0 * mr * nn * nn - 2.0 / 3.0 * nn ** 3, f"2*M*N^2 - 2/3*N^3, M={int(mr)}, N={nn}"
+    if rows_a is None:
+        rows_a = rows_b = float(st["reduced_rows"]) / 2
+    f = 2.0 * rows_a * n * n - 2.0 / 3.0 * n ** 3 + 2.0 * rows_b * n * n - 2.0 / 3.0 * n ** 3
+    return f, f"footnote: 2*(m1-G)*n1^2 + 2*(m2-G)*n2^2 (-2/3 n^3 each), n1=n2={n}"
+
+
 def join_rows(cfg_id, ka, kb):
     cfg = CONFIGS[cfg_id]
     if ka is None:
@@ -176,6 +192,9 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-rows", type=int, default=1_000_000)
+    ap.add_argument("--variant", default="footnote", choices=["footnote", "dense"],
+                    help="figaro reduction timed as the headline (the other one is timed too and "
+                         "reported under 'variants')")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -185,6 +204,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = CONFIGS[args.config]
+    if world > 1:
+        args.variant = "dense"   # the row-sharded path (sharded.py) is built on the dense reduction
 
     if args.impl == "reference":
         if rank != 0:
@@ -233,56 +254,61 @@ def main():
         from paper_2503_23385_b200 import sharded
         return sharded.figaro_r_sharded(A, B, m, m, a0)   # carry + R all-gathers over NCCL
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = Clocks(local)
-    clocks.start()
-    launches0 = N.kernel_launches()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stage = []
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        ev[i][0].record(stream)
-        step()
-        ev[i][1].record(stream)
-        if world == 1:
-            stage.append(N.last_timing())
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = N.kernel_launches() - launches0
-    clk = clocks.stop()
-    step_ms = [s.elapsed_time(e) for s, e in ev]
-    ms = float(np.mean(step_ms))
-    if world > 1:
-        t = torch.tensor([ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    def timed(variant, steps):
+        N.set_variant(variant)
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = Clocks(local)
+        clocks.start()
+        launches0 = N.kernel_launches()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        stage = []
+        torch.cuda.synchronize()
+        for i in range(steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            if world == 1:
+                stage.append(N.last_timing())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches = N.kernel_launches() - launches0
+        clk = clocks.stop()
+        step_ms = [s_.elapsed_time(e_) for s_, e_ in ev]
+        ms = float(np.mean(step_ms))
+        if world > 1:
+            t = torch.tensor([ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, step_ms, stage, launches, clk
+
+    other = "dense" if args.variant == "footnote" else "footnote"
+    ms_o, _, stage_o, _, _ = timed(other, max(1, min(args.steps, 3))) if world == 1 else (None, None, [], 0, None)
+    ms, step_ms, stage, launches, clk = timed(args.variant, args.steps)
     value = jrows / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (TSQR leaves, FP64 tensor pipe)
     roof, roof_hbm, stage_avg = None, None, None
     if stage:
         stage_avg = {k: float(np.mean([s[k] for s in stage])) for k in ("group_ms", "scan_ms", "tsqr_ms", "tree_ms", "svd_ms", "total_ms")}
-        M = float(stage[0]["reduced_rows"])
-        m_red = (m + m - 1) if cfg["keys"] is None else M
-        flops = 2.0 * m_red * nn * nn - 2.0 / 3.0 * nn ** 3
+        flops, alg = tsqr_flops(args.variant, cfg, m, n, stage[0])
         achieved = flops / (stage_avg["tsqr_ms"] / 1e3) / 1e12
-        roof = {"kernel": "tsqr_kernel (fused Claim-1 assembly + Householder TSQR leaves)",
+        roof = {"kernel": "tsqr_kernel (Claim-1 rows generated in the loader + Householder TSQR on DMMA)",
                 "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
                 "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 figure",
-                "algorithmic": f"2*M*N^2 - 2/3*N^3 with M={int(m_red)}, N={nn}",
-                "share_of_step": stage_avg["tsqr_ms"] / ms}
+                "algorithmic": alg, "share_of_step": stage_avg["tsqr_ms"] / ms}
         pk = peaks()
-        gbs = (8.0 * m * n) / (stage_avg["scan_ms"] / 1e3) / 1e9 if stage_avg["scan_ms"] > 0 else None
+        sides = 2 if args.variant == "footnote" else 1
+        gbs = (8.0 * m * n * sides) / (stage_avg["scan_ms"] / 1e3) / 1e9 if stage_avg["scan_ms"] > 0 else None
         if gbs:
-            roof_hbm = {"kernel": "segscan (head/tail prefix pass over B)", "bound": "hbm", "achieved": gbs,
-                        "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
-                        "algorithmic": f"8*m2*n2 = {8 * m * n} bytes read"}
+            roof_hbm = {"kernel": "segscan (head/tail prefix pass, tile sums + carry scan)", "bound": "hbm",
+                        "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                        "algorithmic": f"8*m*n per scanned side x {sides} = {8 * m * n * sides} bytes read"}
 
     # ---- end-to-end through the public API with host buffers (N=1)
     e2e = None
@@ -314,7 +340,10 @@ def main():
                            "join_rows": jrows, "parallelism": f"rows{world}",
                            "l2": "inputs 16*m*n bytes >> 126 MB L2 (no flush needed)" if m * n * 16 > 2**28 else "small config: L2-resident"},
                 "gpu_launches": launches, "clocks": clk, "roofline": roof, "roofline_hbm": roof_hbm,
-                "stages_ms": stage_avg, "step_ms_all": step_ms, "e2e": e2e, "cpu_baseline": cpu}
+                "stages_ms": stage_avg, "step_ms_all": step_ms, "e2e": e2e, "cpu_baseline": cpu,
+                "variant": args.variant,
+                "variants": {args.variant: {"ms_per_step": ms, "value": value},
+                             other: ({"ms_per_step": ms_o, "value": jrows / (ms_o / 1e3)} if ms_o else None)}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -72,27 +72,55 @@ __global__ void __launch_bounds__(256) segscan_tile_kernel(
   if (lane == 0) flag[t] = any_start;
 }
 
-// carry[0] = 0; carry[t+1] = flag[t] ? agg[t] : carry[t] + agg[t]   (fixed order)
-__global__ void segscan_carry_kernel(const double* __restrict__ agg, const int* __restrict__ flag,
-                                     int64_t ntiles, int cols, double* __restrict__ carry) {
+// Segmented carry over tiles, two-level with FIXED association (deterministic):
+//   carry[0] = 0; carry[t+1] = flag[t] ? agg[t] : carry[t] + agg[t]
+// Level 1: thread (column, block of CB tiles) folds its block into (flag, sum);
+// level 2: one thread per column scans the block aggregates; level 3: each
+// (column, block) thread replays its block from the block's carry-in.
+constexpr int CB = 64;
+
+__global__ void carry_block_kernel(const double* __restrict__ agg, const int* __restrict__ flag, int64_t ntiles,
+                                   int cols, int64_t nblk, double* __restrict__ bagg, int* __restrict__ bflag) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nblk * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / cols;
+    const int c = (int)(idx - b * cols);
+    double cur = 0.0;
+    int f = 0;
+    const int64_t t1 = min(ntiles, (b + 1) * CB);
+    for (int64_t t = b * CB; t < t1; ++t) {
+      const double a = agg[t * cols + c];
+      if (flag[t]) { cur = a; f = 1; } else cur += a;
+    }
+    bagg[b * cols + c] = cur;
+    if (c == 0) bflag[b] = f;
+  }
+}
+
+__global__ void carry_top_kernel(double* __restrict__ bagg, const int* __restrict__ bflag, int64_t nblk, int cols) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
-  double cur = 0.0;
-  int64_t t = 0;
-  for (; t + 8 <= ntiles; t += 8) {
-    double a[8];
-    int f[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) { a[u] = agg[(t + u) * cols + c]; f[u] = flag[t + u]; }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      carry[(t + u) * cols + c] = cur;
-      cur = f[u] ? a[u] : cur + a[u];
-    }
+  double cur = 0.0;  // exclusive carry into block b, written in place
+  for (int64_t b = 0; b < nblk; ++b) {
+    const double a = bagg[b * cols + c];
+    bagg[b * cols + c] = cur;
+    cur = bflag[b] ? a : cur + a;
   }
-  for (; t < ntiles; ++t) {
-    carry[t * cols + c] = cur;
-    cur = flag[t] ? agg[t * cols + c] : cur + agg[t * cols + c];
+}
+
+__global__ void carry_apply_kernel(const double* __restrict__ agg, const int* __restrict__ flag, int64_t ntiles,
+                                   int cols, int64_t nblk, const double* __restrict__ bin, double* __restrict__ carry) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nblk * cols;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / cols;
+    const int c = (int)(idx - b * cols);
+    double cur = bin[b * cols + c];
+    const int64_t t1 = min(ntiles, (b + 1) * CB);
+    for (int64_t t = b * CB; t < t1; ++t) {
+      carry[t * cols + c] = cur;
+      const double a = agg[t * cols + c];
+      cur = flag[t] ? a : cur + a;
+    }
   }
 }
 
@@ -115,7 +143,8 @@ __global__ void group_fixup_kernel(const int64_t* __restrict__ gstart, const int
 
 size_t segscan_ws_bytes(int64_t rows, int64_t cols, int64_t groups_cap) {
   int64_t nt = std::max<int64_t>(1, cdiv(rows, TILE_ROWS));
-  return 2 * ws_bytes(size_t(nt) * cols, 8) + ws_bytes(nt, 4) +
+  int64_t nb = cdiv(nt, CB);
+  return 2 * ws_bytes(size_t(nt) * cols, 8) + ws_bytes(nt, 4) + ws_bytes(size_t(nb) * cols, 8) + ws_bytes(nb, 4) +
          ws_bytes(size_t(std::max<int64_t>(groups_cap, 1)) * cols, 8);
 }
 
@@ -139,9 +168,20 @@ int segscan_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const 
   segscan_tile_kernel<<<(unsigned)cdiv(s->ntiles, wpb), 32 * wpb, 0, ctx->stream>>>(
       x, rows, (int)cols, gid, s->ntiles, s->tile_agg, s->tile_flag, s->totals);
   JQ_CHECK_LAUNCH(ctx);
-  segscan_carry_kernel<<<(unsigned)cdiv(cols, 64), 64, 0, ctx->stream>>>(s->tile_agg, s->tile_flag,
-                                                                         s->ntiles, (int)cols, s->carry);
-  JQ_CHECK_LAUNCH(ctx);
+  {
+    const int64_t nblk = cdiv(s->ntiles, CB);
+    double* bagg = ws_alloc<double>(ctx, size_t(nblk) * cols);
+    int* bflag = ws_alloc<int>(ctx, nblk);
+    if (!bagg || !bflag) return fail(JQ_E_OOM, "workspace exhausted (carry scan)");
+    const unsigned gb = (unsigned)std::min<int64_t>(cdiv(nblk * cols, 128), 148 * 16);
+    carry_block_kernel<<<gb, 128, 0, ctx->stream>>>(s->tile_agg, s->tile_flag, s->ntiles, (int)cols, nblk, bagg, bflag);
+    JQ_CHECK_LAUNCH(ctx);
+    carry_top_kernel<<<(unsigned)cdiv(cols, 64), 64, 0, ctx->stream>>>(bagg, bflag, nblk, (int)cols);
+    JQ_CHECK_LAUNCH(ctx);
+    carry_apply_kernel<<<gb, 128, 0, ctx->stream>>>(s->tile_agg, s->tile_flag, s->ntiles, (int)cols, nblk, bagg,
+                                                   s->carry);
+    JQ_CHECK_LAUNCH(ctx);
+  }
   group_fixup_kernel<<<(unsigned)std::min<int64_t>(cdiv(std::max<int64_t>(groups_cap, 1) * cols, 256), 4096),
                        256, 0, ctx->stream>>>(gstart, gcount, d_ngroups, rows, (int)cols, s->carry,
                                               s->totals);

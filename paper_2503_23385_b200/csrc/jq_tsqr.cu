@@ -459,6 +459,17 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
 #ifndef JQ_PROBE
 #define JQ_PROBE 0
 #endif
+#ifdef JQ_KTIME
+__device__ unsigned long long g_ktime[8];
+#define KT_DECL long long kt_acc[5] = {0, 0, 0, 0, 0}; long long kt_t = clock64();
+#define KT_MARK(i) do { long long n_ = clock64(); kt_acc[i] += n_ - kt_t; kt_t = n_; } while (0)
+#define KT_FLUSH() do { if (lane == 0) for (int i_ = 0; i_ < 5; ++i_) atomicAdd(&g_ktime[i_], (unsigned long long)kt_acc[i_]); \
+                        if (tid == 0) atomicAdd(&g_ktime[7], 1ull); } while (0)
+#else
+#define KT_DECL
+#define KT_MARK(i) do {} while (0)
+#define KT_FLUSH() do {} while (0)
+#endif
 template <class C>
 __device__ __forceinline__ int pass_rows(int rcol) {
   return rcol > 0 ? min(C::K, (C::RAW / rcol) & ~7) : C::K;
@@ -534,6 +545,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   const int lt_idx[2] = {warp, C::NLT - 1 - warp};
   double c[2][C::KT][2];
   uint32_t phase = 0;
+  KT_DECL
 
   for (int64_t row0 = row_begin; row0 < row_end; row0 += C::K) {
     const int rcol = s.rc(row0);
@@ -576,6 +588,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
         if (nv0 < row_end) issue(nv0, same ? row0 : nv0);
       }
     }
+    KT_MARK(0);  // 0: load (wait + prep + register load)
 
     for (int p = 0; p < C::NLT; ++p) {
       const int j0 = 8 * p;
@@ -588,7 +601,9 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
         if (p < C::WARPS) factor_panel<C>(c[0], R, j0, Ys, Yt, T, U, taus, scs, Xs, lane);
         else              factor_panel<C>(c[1], R, j0, Ys, Yt, T, U, taus, scs, Xs, lane);
       }
+      KT_MARK(1);  // 1: panel factorisation (owner) / idle arrival
       __syncthreads();
+      KT_MARK(2);  // 2: barrier wait (deferred-blocking: mostly lands in the next phase)
 
       // ---------------- trailing update of my column tiles right of the panel
 #pragma unroll
@@ -620,9 +635,12 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
           dmma(c[q][it], nw1, Yt[(2 * t + 1) * C::LDYT + 8 * it + g]);
         }
       }
+      KT_MARK(3);  // 3: trailing update
     }
     __syncthreads();
+    KT_MARK(4);  // 4: end-of-chunk barrier
   }
+  KT_FLUSH();
 
   // ---- write R (zeros strictly below the diagonal)
   double* out = r_out + cta * C::NP * C::NP;
@@ -821,3 +839,15 @@ int canonicalize_dev(jq_ctx* ctx, const double* r, int64_t n, double* out) {
 }
 
 }  // namespace jq
+
+#ifdef JQ_KTIME
+extern "C" JQ_API int jq_debug_ktime(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, jq::g_ktime, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(jq::g_ktime, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

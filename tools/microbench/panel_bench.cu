@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) panel_bench(long long* cyc, dou
 }
 }  // namespace jq
 
-int main() {
-  using C = jq::Cfg<128>;
+template <class C>
+void run(const char* name) {
   long long* cyc; double* sink;
   cudaMallocManaged(&cyc, 64); cudaMalloc(&sink, 8 * 4096);
   cudaFuncSetAttribute(jq::panel_bench<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -46,6 +46,23 @@ int main() {
   long long pt[16]; cudaMemcpyFromSymbol(pt, jq::g_ptime, sizeof(pt));
   const char* nm[6] = {"R ld + Xs publish + syncwarp", "x loads + dots + quad reduce", "-", "bcast + scalars", "update + writes", "Y + T tail (per panel)"};
   for (int i = 0; i < 6; ++i) if (i != 2) printf("  %-32s %8.1f cycles\n", nm[i], pt[i] / (double)reps / (i == 5 ? 1 : 8));
-  printf("factor_panel<128>: %lld cycles per panel (%.0f per column) status %s\n", cyc[0], cyc[0] / 8.0,
+  printf("%s: %lld cycles per panel (%.0f per column) status %s\n", name, cyc[0], cyc[0] / 8.0,
          cudaGetErrorString(cudaGetLastError()));
+}
+
+namespace jq {
+template <int NP_, int K_>
+struct CfgK : Cfg<NP_> {
+  static constexpr int K = K_;
+  static constexpr int KT = K_ / 8;
+  static constexpr int LDYT = K_ + 2;
+};
+}
+
+int main() {
+  run<jq::Cfg<128>>("NP=128 K=128");
+  run<jq::CfgK<128, 64>>("NP=128 K=64 ");
+  run<jq::CfgK<128, 32>>("NP=128 K=32 ");
+  run<jq::CfgK<128, 16>>("NP=128 K=16 ");
+  run<jq::Cfg<64>>("NP=64  K=128");
 }
