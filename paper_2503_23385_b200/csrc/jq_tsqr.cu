@@ -77,40 +77,42 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 template <int NP_>
 struct Cfg {
   static constexpr int NP = NP_;
-  static constexpr int WARPS = NP / 16;     // 2 column tiles per warp
+  static constexpr int NLT = NP / 8;        // column tiles of 8
+  static constexpr int WARPS = 8;           // row-split: warp w holds rows [w*KW, (w+1)*KW) of every tile
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int NLT = NP / 8;        // column tiles
   static constexpr int K = NP >= 256 ? 64 : 128;  // chunk rows held in registers
-  static constexpr int KT = K / 8;          // row tiles per chunk
+  static constexpr int KW = K / WARPS;      // rows per warp
+  static constexpr int KWT = KW / 8;        // row tiles per warp
   static constexpr bool R_SMEM = NP <= 128;
+  static constexpr int MIN_CTAS = NP <= 64 ? 2 : 1;  // two independent chains per SM when they fit
   // R packed by 8-row panels: panel p holds rows 8p..8p+7, columns 8p..NP-1,
   // row stride NP - 8p + 2 (== 2 or 10 mod 16: conflict-free DMMA fragment access)
   __host__ __device__ static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
-  static constexpr int LDY = 10;            // Ys  (K x 8)
-  static constexpr int LDYT = K + 2;        // Yt  (8 x K)
   static constexpr int LDT = 10;            // T   (8 x 8)
-  static constexpr int RAW = NP * 64;       // raw-row buffer (NP * 512 bytes)
+  static constexpr int LDYT = KW + 2;       // per-warp Y^T (8 x KW), == 2 mod 16
+  static constexpr int RAW = NP >= 256 ? NP * 32 : NP * 64;  // raw-row buffer
   // shared memory carve-up (doubles; every offset even -> 16-byte aligned)
   static constexpr int OFF_R = 0;
   static constexpr int SZ_R = R_SMEM ? rp_off(NLT) : 0;
   static constexpr int OFF_RAW = OFF_R + SZ_R;
-  static constexpr int OFF_YS = OFF_RAW + RAW;
-  static constexpr int SZ_YS = K * LDY;
-  static constexpr int OFF_YT = OFF_YS + 2 * SZ_YS;
+  static constexpr int OFF_YT = OFF_RAW + RAW;            // [WARPS][8][LDYT]
   static constexpr int SZ_YT = 8 * LDYT;
-  static constexpr int OFF_T = OFF_YT + 2 * SZ_YT;
-  static constexpr int SZ_T = 8 * LDT;
-  static constexpr int OFF_U = OFF_T + 2 * SZ_T;
+  static constexpr int OFF_ZP = OFF_YT + WARPS * SZ_YT;   // partial Z^T [WARPS][NLT][64]
+  static constexpr int OFF_WS = OFF_ZP + WARPS * NLT * 64;  // W^T [NLT][64]
+  static constexpr int OFF_T = OFF_WS + NLT * 64;
+  static constexpr int OFF_U = OFF_T + 8 * LDT;
   static constexpr int OFF_TAU = OFF_U + 64;
   static constexpr int OFF_SC = OFF_TAU + 8;  // reflector scales of the panel
-  static constexpr int OFF_X = OFF_SC + 8;    // raw panel column broadcast (K)
-  static constexpr int OFF_S = OFF_X + K;     // running prefix sums (Figaro source, <= NP)
+  static constexpr int OFF_P = OFF_SC + 8;    // column dot partials [2 parity][WARPS][8]
+  static constexpr int OFF_X = OFF_P + 2 * WARPS * 8;  // per-warp raw column broadcast [WARPS][KW]
+  static constexpr int OFF_S = OFF_X + WARPS * KW;     // running prefix sums (Figaro source, <= NP)
   static constexpr int OFF_LD = OFF_S + NP;   // loader scratch: 3 per-row coefficients + 2 per thread
   static constexpr int SZ_LD = 3 * K + 2 * THREADS;
   static constexpr int OFF_BAR = OFF_LD + SZ_LD;  // mbarrier (8 bytes)
   static constexpr int TOTAL = OFF_BAR + 2;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(KW % 8 == 0, "whole row tiles per warp");
 };
 
 // R element (r, c), c >= 8 * (r / 8), in the packed (smem) or dense (global) layout
@@ -332,59 +334,63 @@ __device__ long long g_ptime[16];
 #else
 #define PT(i) do {} while (0)
 #endif
-// Householder factorisation of one 8-column panel held in registers by its owner
-// warp (LAPACK dlarfg convention: beta = -sign(alpha) |x|, tau = (beta-alpha)/beta
-// = 1 + |alpha| / |x|, v = [1; x2 / (alpha - beta)]).  Lane (g, t) holds column
-// j0+g, rows 8*it+2*t+b.  Columns keep their UNscaled values x during the panel
-// (y_g = scale_g x_g); one quad reduction per column gives d_g = x_j . c_g.
-// Writes Y (both layouts), T (forward accumulation) and the panel's R rows.
+
+// Householder factorisation of one 8-column panel by ALL warps of the CTA.  Warp w
+// holds rows [w*KW, (w+1)*KW) of the panel tile in `cp` (lane (g,t): column j0+g,
+// local rows 8*it + 2*t + b).  LAPACK dlarfg convention: beta = -sign(alpha)|x|,
+// tau = (beta - alpha)/beta = 1 + |alpha|/|x|, v = [1; x2/(alpha - beta)].  Columns keep
+// their UNscaled values during the panel (y_g = scale_g x_g).  Per column: the owner
+// quad publishes its rows of x inside the warp, every quad forms its partial
+// x . c_g, one quad reduction, and a CTA-wide fixed-order sum of the WARPS partials
+// gives d_g (g = j: |x|^2; g > j: reflector dot product; g < j: T entries).
+// On return cp holds Y (scaled) and Yt (this warp's rows) / T / R rows are written.
 template <class C>
-__device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, const int j0, double* Ys,
-                                             double* Yt, double* T, double* U, double* taus, double* scs,
-                                             double* Xs, const int lane) {
+__device__ __forceinline__ void factor_panel_all(double (&cp)[C::KWT][2], double* R, const int j0, double* Ytw,
+                                                 double* T, double* U, double* taus, double* scs, double* Xw,
+                                                 double* P, const int warp, const int lane) {
   const int g = lane >> 2, t = lane & 3;
+  (void)Xw;
   // The panel's R rows are final at panel start (reflector jj rewrites only row
-  // j0+jj), so the next column's entries are prefetched one column ahead.
+  // j0+jj): the next column's entries are prefetched one column ahead.
   double alpha_n = R[rix<C>(j0, j0)], rg_n = R[rix<C>(j0, j0 + g)];
-#ifdef JQ_PANEL_TIMING
-  long long pt_last = clock64(), pt_acc[6] = {0, 0, 0, 0, 0, 0};
-#endif
-  double tau_r = 0.0, scale_r = 0.0;  // lane r < 8 keeps tau_r / scale_r of column r
-#pragma unroll 1
+  double scale_g = 0.0;  // scale of my own column g
+#pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     const double alpha = alpha_n, rgj = rg_n;
     if (jj < 7) {
       alpha_n = R[rix<C>(j0 + jj + 1, j0 + jj + 1)];
       rg_n = R[rix<C>(j0 + jj + 1, j0 + g)];
     }
-    if (g == jj) {
+    // x_jj broadcast inside the warp: lane (g,t) needs rows (it, t, b) held by lane (jj, t)
+    double xv[C::KWT][2];
 #pragma unroll
-      for (int it = 0; it < C::KT; ++it)
-        *reinterpret_cast<double2*>(Xs + 8 * it + 2 * t) = make_double2(cc[it][0], cc[it][1]);
+    for (int it = 0; it < C::KWT; ++it) {
+      xv[it][0] = __shfl_sync(FULL, cp[it][0], jj * 4 + t);
+      xv[it][1] = __shfl_sync(FULL, cp[it][1], jj * 4 + t);
     }
-    __syncwarp();
-    PT(0);
-    double xv[C::KT][2];
-    double dp[8];
+    double dp0 = 0.0, dp1 = 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) dp[u] = 0.0;
-#pragma unroll
-    for (int it = 0; it < C::KT; ++it) {
-      const double2 x2 = *reinterpret_cast<const double2*>(Xs + 8 * it + 2 * t);
-      xv[it][0] = x2.x;
-      xv[it][1] = x2.y;
-      dp[(2 * it) & 7] = fma(xv[it][0], cc[it][0], dp[(2 * it) & 7]);
-      dp[(2 * it + 1) & 7] = fma(xv[it][1], cc[it][1], dp[(2 * it + 1) & 7]);
+    for (int it = 0; it < C::KWT; ++it) {
+      dp0 = fma(xv[it][0], cp[it][0], dp0);
+      dp1 = fma(xv[it][1], cp[it][1], dp1);
     }
-    double d = ((dp[0] + dp[1]) + (dp[2] + dp[3])) + ((dp[4] + dp[5]) + (dp[6] + dp[7]));
+    double d = dp0 + dp1;
     d += __shfl_xor_sync(FULL, d, 1);
     d += __shfl_xor_sync(FULL, d, 2);
-    PT(1);
-    const double sj = __shfl_sync(FULL, d, jj * 4);
+    double* Pj = P + (jj & 1) * (C::WARPS * 8);
+    if (t == 0) Pj[warp * 8 + g] = d;
+    __syncthreads();
+    d = 0.0;
+    double sj = 0.0;
+#pragma unroll
+    for (int w = 0; w < C::WARPS; ++w) {  // fixed order: bit-identical in every warp
+      d += Pj[w * 8 + g];
+      sj += Pj[w * 8 + jj];
+    }
     double tau = 0.0, beta = alpha, scale = 0.0;
     if (sj != 0.0) {
       const double s2 = fma(alpha, alpha, sj);
-      if (s2 > 1e-280 && s2 < 1e280) {                 // warp-uniform: fast MUFU + Newton path
+      if (s2 > 1e-280 && s2 < 1e280) {                 // uniform branch: MUFU + Newton fast path
         const double rn = rsqrt_nr(s2);                // 1 / |[alpha; x]|
         const double nrm = s2 * rn;
         beta = alpha >= 0.0 ? -nrm : nrm;
@@ -397,58 +403,49 @@ __device__ __forceinline__ void factor_panel(double (&cc)[C::KT][2], double* R, 
         scale = 1.0 / (alpha - beta);
       }
     }
-    PT(3);
     // g > jj: c_g <- c_g - tau (R[j][g] + y_j . c_g) y_j,  y_j = scale x_j
     const double tw = tau * fma(scale, d, rgj);
     const double a = g > jj ? -tw * scale : 0.0;
 #pragma unroll
-    for (int it = 0; it < C::KT; ++it)
+    for (int it = 0; it < C::KWT; ++it)
 #pragma unroll
-      for (int b = 0; b < 2; ++b) cc[it][b] = fma(a, xv[it][b], cc[it][b]);
-    if (t == 0) {
-      if (g > jj) R[rix<C>(j0 + jj, j0 + g)] = rgj - tw;
-      else if (g < jj) U[g * 8 + jj] = d;  // x_g . x_jj  (scaled in T below)
-      else R[rix<C>(j0 + jj, j0 + jj)] = beta;
+      for (int b = 0; b < 2; ++b) cp[it][b] = fma(a, xv[it][b], cp[it][b]);
+    if (g == jj) scale_g = scale;
+    if (warp == 0 && t == 0) {  // off the chain: plain predicated stores
+      if (g >= jj) R[rix<C>(j0 + jj, j0 + g)] = g > jj ? rgj - tw : beta;
+      else U[g * 8 + jj] = d;   // x_g . x_jj  (scaled in T below)
+      if (g == jj) { taus[jj] = tau; scs[jj] = scale; }
     }
-    if (lane == jj) { tau_r = tau; scale_r = scale; }
-    PT(4);
   }
-  if (lane < 8) { taus[lane] = tau_r; scs[lane] = scale_r; }
-  __syncwarp();
-  // Y = X diag(scale) in both layouts, written once per panel by all lanes
-  const double sg = scs[g];
+  // Y = X diag(scale): registers (B operand of Z) and this warp's rows of Y^T
 #pragma unroll
-  for (int it = 0; it < C::KT; ++it) {
-    const int i = 8 * it + 2 * t;
-    const double y0 = cc[it][0] * sg, y1 = cc[it][1] * sg;
-    Ys[i * C::LDY + g] = y0;
-    Ys[(i + 1) * C::LDY + g] = y1;
-    *reinterpret_cast<double2*>(Yt + g * C::LDYT + i) = make_double2(y0, y1);
+  for (int it = 0; it < C::KWT; ++it) {
+    cp[it][0] *= scale_g;
+    cp[it][1] *= scale_g;
+    *reinterpret_cast<double2*>(Ytw + g * C::LDYT + 8 * it + 2 * t) = make_double2(cp[it][0], cp[it][1]);
   }
-  // T (8 x 8 upper triangular): T[r][r] = tau_r,
-  // T[r][j] = -tau_j sum_{m=r}^{j-1} T[r][m] (y_m . y_j); lane r builds row r.
-  if (lane < 8) {
-    const int r = lane;
-    double trow[8], sc[8], tu[8];
+  if (warp == 0) {
+    __syncwarp();
+    // T (8 x 8 upper triangular): T[r][r] = tau_r,
+    // T[r][j] = -tau_j sum_{m=r}^{j-1} T[r][m] (y_m . y_j),  y_m . y_j = sc_m sc_j x_m . x_j
+    if (lane < 8) {
+      const int r = lane;
+      double sc[8], tu[8], trow[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) { sc[m] = scs[m]; tu[m] = taus[m]; }
+      for (int m = 0; m < 8; ++m) { sc[m] = scs[m]; tu[m] = taus[m]; }
 #pragma unroll
-    for (int m = 0; m < 8; ++m) trow[m] = (m == r) ? tu[m] : 0.0;
+      for (int m = 0; m < 8; ++m) trow[m] = (m == r) ? tu[m] : 0.0;
 #pragma unroll
-    for (int j = 1; j < 8; ++j) {
-      double acc = 0.0;
+      for (int j = 1; j < 8; ++j) {
+        double acc = 0.0;
 #pragma unroll
-      for (int m = 0; m < j; ++m) acc = fma(trow[m], (U[m * 8 + j] * sc[m]) * sc[j], acc);  // trow[m] = 0 for m < r
-      if (j > r) trow[j] = -tu[j] * acc;
+        for (int m = 0; m < j; ++m) acc = fma(trow[m], (U[m * 8 + j] * sc[m]) * sc[j], acc);  // trow[m] = 0 for m < r
+        if (j > r) trow[j] = -tu[j] * acc;
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
     }
-#pragma unroll
-    for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
   }
-  PT(5);
-#ifdef JQ_PANEL_TIMING
-  if (lane == 0)
-    for (int i = 0; i < 6; ++i) g_ptime[i] += pt_acc[i];
-#endif
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -476,18 +473,18 @@ __device__ __forceinline__ int pass_rows(int rcol) {
 }
 
 template <class C, class Src, bool COMBINE>
-__global__ void __launch_bounds__(C::THREADS, 1)
+__global__ void __launch_bounds__(C::THREADS, C::MIN_CTAS)
 tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __restrict__ r_init,
             int64_t init_count, double* __restrict__ r_out, int use_tma) {
   extern __shared__ __align__(16) double smem_dyn[];
   double* raw = smem_dyn + C::OFF_RAW;
-  double* Ys0 = smem_dyn + C::OFF_YS;
-  double* Yt0 = smem_dyn + C::OFF_YT;
-  double* T0 = smem_dyn + C::OFF_T;
+  double* T = smem_dyn + C::OFF_T;
   double* U = smem_dyn + C::OFF_U;
   double* taus = smem_dyn + C::OFF_TAU;
   double* scs = smem_dyn + C::OFF_SC;
-  double* Xs = smem_dyn + C::OFF_X;
+  double* P = smem_dyn + C::OFF_P;
+  double* Zp = smem_dyn + C::OFF_ZP;
+  double* Ws = smem_dyn + C::OFF_WS;
   double* S = smem_dyn + C::OFF_S;
   double* scratch = smem_dyn + C::OFF_LD;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
@@ -495,6 +492,8 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int64_t cta = blockIdx.x;
+  double* Ytw = smem_dyn + C::OFF_YT + warp * C::SZ_YT;
+  double* Xw = smem_dyn + C::OFF_X + warp * C::KW;
 
   double* R;
   if constexpr (C::R_SMEM) R = smem_dyn + C::OFF_R;
@@ -524,7 +523,6 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   if (tid == 0) mbar_init(bar);
   __syncthreads();
 
-  // geometry of the pass starting at virtual row v0 (chunks never straddle parts)
   // rows of the pass starting at v0: never past its chunk (the prefix state S must
   // not run ahead), the CTA range or the source
   auto pass_nrows = [&](int64_t v0, int rb, int64_t chunk0) -> int {
@@ -542,8 +540,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   };
   if (use_tma && tid == 0 && row_begin < row_end) issue(row_begin, row_begin);
 
-  const int lt_idx[2] = {warp, C::NLT - 1 - warp};
-  double c[2][C::KT][2];
+  double c[C::NLT][C::KWT][2];  // this warp's rows of every column tile (C^T accumulator layout)
   uint32_t phase = 0;
   KT_DECL
 
@@ -552,9 +549,9 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
     const int rb = pass_rows<C>(rcol);
     const int npass = (C::K + rb - 1) / rb;
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int q = 0; q < C::NLT; ++q)
 #pragma unroll
-      for (int it = 0; it < C::KT; ++it) c[q][it][0] = c[q][it][1] = 0.0;  // rows past the range stay zero
+      for (int it = 0; it < C::KWT; ++it) c[q][it][0] = c[q][it][1] = 0.0;  // rows past the range stay zero
     for (int h = 0; h < npass && row0 + (int64_t)h * rb < row_end; ++h) {
       const int64_t pv0 = row0 + (int64_t)h * rb;
       const int nr = pass_nrows(pv0, rb, row0);
@@ -571,13 +568,13 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
       s.template prep<C>(raw, S, scratch, pv0, nr);
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int l = lt_idx[q] * 8 + g;
+      for (int q = 0; q < C::NLT; ++q) {
+        const int l = q * 8 + g;
 #pragma unroll
-        for (int it = 0; it < C::KT; ++it)
+        for (int it = 0; it < C::KWT; ++it)
 #pragma unroll
           for (int b = 0; b < 2; ++b) {
-            const int li = 8 * it + 2 * t + b - h * rb;
+            const int li = warp * C::KW + 8 * it + 2 * t + b - h * rb;
             if (li >= 0 && li < rb) c[q][it][b] = s.template value<C>(raw, scratch, pv0, li, l, nr, rcol);
           }
       }
@@ -588,57 +585,78 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
         if (nv0 < row_end) issue(nv0, same ? row0 : nv0);
       }
     }
-    KT_MARK(0);  // 0: load (wait + prep + register load)
+    KT_MARK(0);
 
+#pragma unroll 1
     for (int p = 0; p < C::NLT; ++p) {
       const int j0 = 8 * p;
-      const int buf = p & 1;
-      double* Ys = Ys0 + buf * C::SZ_YS;
-      double* Yt = Yt0 + buf * C::SZ_YT;
-      double* T = T0 + buf * C::SZ_T;
-      const int owner = p < C::WARPS ? p : C::NLT - 1 - p;
-      if (JQ_PROBE != 2 && JQ_PROBE != 3 && warp == owner) {
-        if (p < C::WARPS) factor_panel<C>(c[0], R, j0, Ys, Yt, T, U, taus, scs, Xs, lane);
-        else              factor_panel<C>(c[1], R, j0, Ys, Yt, T, U, taus, scs, Xs, lane);
+      // ---------------- panel factorisation by all warps (panel tile copied out of c[])
+      double cp[C::KWT][2];
+#pragma unroll
+      for (int q = 0; q < C::NLT; ++q)
+        if (q == p)
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it) { cp[it][0] = c[q][it][0]; cp[it][1] = c[q][it][1]; }
+      if (JQ_PROBE != 2 && JQ_PROBE != 3)
+        factor_panel_all<C>(cp, R, j0, Ytw, T, U, taus, scs, Xw, P, warp, lane);
+      KT_MARK(1);
+      // ---------------- trailing update:  Z = R_rows + Y^T C,  W = T^T Z,  R_rows -= W,  C -= Y W
+      // (1) partial Z^T over this warp's rows, B operand = Y straight from registers
+      if (JQ_PROBE != 1 && JQ_PROBE != 3) {
+#pragma unroll
+        for (int q = 0; q < C::NLT; ++q) {
+          if (q > p) {
+            double z[2] = {0.0, 0.0};
+#pragma unroll
+            for (int it = 0; it < C::KWT; ++it) {
+              dmma(z, c[q][it][0], cp[it][0]);
+              dmma(z, c[q][it][1], cp[it][1]);
+            }
+            *reinterpret_cast<double2*>(Zp + (warp * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0], z[1]);
+          }
+        }
       }
-      KT_MARK(1);  // 1: panel factorisation (owner) / idle arrival
       __syncthreads();
-      KT_MARK(2);  // 2: barrier wait (deferred-blocking: mostly lands in the next phase)
-
-      // ---------------- trailing update of my column tiles right of the panel
+      KT_MARK(2);
+      // (2) tile q is reduced by warp q % WARPS: fixed-order sum + R rows, W = T^T Z, R -= W
+      if (JQ_PROBE != 1 && JQ_PROBE != 3) {
+        for (int q = p + 1 + ((warp - (p + 1)) % C::WARPS + C::WARPS) % C::WARPS; q < C::NLT; q += C::WARPS) {
+          const int l0 = q * 8;
+          const int r0i = rix<C>(j0 + 2 * t, l0 + g), r1i = rix<C>(j0 + 2 * t + 1, l0 + g);
+          double z0 = R[r0i], z1 = R[r1i];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int lt = lt_idx[q];
-        if (lt <= p || JQ_PROBE == 1 || JQ_PROBE == 3) continue;
-        const int l0 = lt * 8;
-        const int r0i = rix<C>(j0 + 2 * t, l0 + g), r1i = rix<C>(j0 + 2 * t + 1, l0 + g);
-        double za[2], zb[2] = {0.0, 0.0};
-        za[0] = R[r0i];
-        za[1] = R[r1i];
-#pragma unroll
-        for (int it = 0; it < C::KT; it += 2) {
-          dmma(za, c[q][it][0], Ys[(8 * it + 2 * t) * C::LDY + g]);
-          dmma(za, c[q][it][1], Ys[(8 * it + 2 * t + 1) * C::LDY + g]);
-          dmma(zb, c[q][it + 1][0], Ys[(8 * (it + 1) + 2 * t) * C::LDY + g]);
-          dmma(zb, c[q][it + 1][1], Ys[(8 * (it + 1) + 2 * t + 1) * C::LDY + g]);
-        }
-        const double z0 = za[0] + zb[0], z1 = za[1] + zb[1];
-        double w[2] = {0.0, 0.0};
-        dmma(w, z0, T[(2 * t) * C::LDT + g]);
-        dmma(w, z1, T[(2 * t + 1) * C::LDT + g]);
-        R[r0i] -= w[0];
-        R[r1i] -= w[1];
-        const double nw0 = -w[0], nw1 = -w[1];
-#pragma unroll
-        for (int it = 0; it < C::KT; ++it) {
-          dmma(c[q][it], nw0, Yt[(2 * t) * C::LDYT + 8 * it + g]);
-          dmma(c[q][it], nw1, Yt[(2 * t + 1) * C::LDYT + 8 * it + g]);
+          for (int w = 0; w < C::WARPS; ++w) {
+            const double2 zz = *reinterpret_cast<const double2*>(Zp + (w * C::NLT + q) * 64 + 2 * lane);
+            z0 += zz.x;
+            z1 += zz.y;
+          }
+          double wv[2] = {0.0, 0.0};
+          dmma(wv, z0, T[(2 * t) * C::LDT + g]);
+          dmma(wv, z1, T[(2 * t + 1) * C::LDT + g]);
+          R[r0i] -= wv[0];
+          R[r1i] -= wv[1];
+          *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-wv[0], -wv[1]);
         }
       }
-      KT_MARK(3);  // 3: trailing update
+      __syncthreads();
+      // (3) C -= Y W on this warp's rows (A = -W^T from smem, B = Y^T rows of this warp)
+      if (JQ_PROBE != 1 && JQ_PROBE != 3) {
+#pragma unroll
+        for (int q = 0; q < C::NLT; ++q) {
+          if (q > p) {
+            const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+#pragma unroll
+            for (int it = 0; it < C::KWT; ++it) {
+              dmma(c[q][it], nw.x, Ytw[(2 * t) * C::LDYT + 8 * it + g]);
+              dmma(c[q][it], nw.y, Ytw[(2 * t + 1) * C::LDYT + 8 * it + g]);
+            }
+          }
+        }
+      }
+      KT_MARK(3);
     }
     __syncthreads();
-    KT_MARK(4);  // 4: end-of-chunk barrier
+    KT_MARK(4);
   }
   KT_FLUSH();
 

@@ -13,19 +13,18 @@ __global__ void __launch_bounds__(C::THREADS, 1) panel_bench(long long* cyc, dou
   for (int i = tid; i < C::SZ_R; i += C::THREADS) R[i] = 0.0;
   for (int i = 0; i < 8; ++i) if (tid == 0) R[rix<C>(i, i)] = 1.0;
   __syncthreads();
-  double c[C::KT][2];
-  for (int it = 0; it < C::KT; ++it) { c[it][0] = 0.001 * (tid + it); c[it][1] = 0.002 * (tid - it); }
+  double c[C::KWT][2];
+  for (int it = 0; it < C::KWT; ++it) { c[it][0] = 0.001 * (tid + it); c[it][1] = 0.002 * (tid - it); }
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
-    if (warp == 0)
-      factor_panel<C>(c, R, 0, smem_dyn + C::OFF_YS, smem_dyn + C::OFF_YT, smem_dyn + C::OFF_T,
-                      smem_dyn + C::OFF_U, smem_dyn + C::OFF_TAU, smem_dyn + C::OFF_SC, smem_dyn + C::OFF_X,
-                      lane);
+    factor_panel_all<C>(c, R, 0, smem_dyn + C::OFF_YT + warp * C::SZ_YT, smem_dyn + C::OFF_T, smem_dyn + C::OFF_U,
+                        smem_dyn + C::OFF_TAU, smem_dyn + C::OFF_SC, smem_dyn + C::OFF_X + warp * C::KW,
+                        smem_dyn + C::OFF_P, warp, lane);
     __syncthreads();
   }
   long long t1 = clock64();
   double s = 0;
-  for (int it = 0; it < C::KT; ++it) s += c[it][0] + c[it][1];
+  for (int it = 0; it < C::KWT; ++it) s += c[it][0] + c[it][1];
   sink[tid] = s;
   if (tid == 0) cyc[0] = (t1 - t0) / reps;
 }
@@ -44,25 +43,13 @@ void run(const char* name) {
     cudaDeviceSynchronize();
   }
   long long pt[16]; cudaMemcpyFromSymbol(pt, jq::g_ptime, sizeof(pt));
-  const char* nm[6] = {"R ld + Xs publish + syncwarp", "x loads + dots + quad reduce", "-", "bcast + scalars", "update + writes", "Y + T tail (per panel)"};
+  const char* nm[6] = {"publish + dots + quad reduce", "CTA barrier + partial sums", "-", "scalars", "update + writes", "Y + T tail (per panel)"};
   for (int i = 0; i < 6; ++i) if (i != 2) printf("  %-32s %8.1f cycles\n", nm[i], pt[i] / (double)reps / (i == 5 ? 1 : 8));
   printf("%s: %lld cycles per panel (%.0f per column) status %s\n", name, cyc[0], cyc[0] / 8.0,
          cudaGetErrorString(cudaGetLastError()));
 }
 
-namespace jq {
-template <int NP_, int K_>
-struct CfgK : Cfg<NP_> {
-  static constexpr int K = K_;
-  static constexpr int KT = K_ / 8;
-  static constexpr int LDYT = K_ + 2;
-};
-}
-
 int main() {
-  run<jq::Cfg<128>>("NP=128 K=128");
-  run<jq::CfgK<128, 64>>("NP=128 K=64 ");
-  run<jq::CfgK<128, 32>>("NP=128 K=32 ");
-  run<jq::CfgK<128, 16>>("NP=128 K=16 ");
-  run<jq::Cfg<64>>("NP=64  K=128");
+  run<jq::Cfg<128>>("NP=128 K=128 (8 warps x 16 rows)");
+  run<jq::Cfg<64>>("NP=64  K=128 (8 warps x 16 rows)");
 }
