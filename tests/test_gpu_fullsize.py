@@ -1,0 +1,142 @@
+"""Parity at the BASELINE.json configuration sizes (configs[1..4] = C2..C5).
+
+The SPEC pipeline itself (reduce -> Householder QR) is run on the CPU for C2; for
+C3-C5, where a CPU QR of up to 2e8 rows is infeasible, the checks go through
+size-independent identities against the factorised join Gram computed by the C
+oracle from the same SplitMix64 seeds (oracle/c/gram_oracle.c):
+  R^T R = J^T J  and  |R| = chol(J^T J)^T   (1e-10 relative Frobenius),
+  sigma = sqrt(eig(J^T J))                   (1e-10 relative to sigma_1),
+plus bit-exact grouping / key generation at full size.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle import cgram
+
+pytestmark = [pytest.mark.gpu]
+
+SEEDS = {c: (1000 * c + 1, 1000 * c + 2) for c in range(1, 6)}
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2503_23385_b200 as P
+    return P
+
+
+def rel(x, y):
+    return float(np.linalg.norm(np.asarray(x) - np.asarray(y)) / np.linalg.norm(np.asarray(y)))
+
+
+def device_tables(P, c, m, n, keys=None):
+    import torch
+    from paper_2503_23385_b200 import datagen
+    a = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    b = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    datagen.uniform(SEEDS[c][0], m, n, out=a)
+    datagen.uniform(SEEDS[c][1], m, n, out=b)
+    ka = kb = None
+    if keys is not None:
+        ka = torch.from_numpy(keys[0]).cuda()
+        kb = torch.from_numpy(keys[1]).cuda()
+    return P.Table(a, ka), P.Table(b, kb)
+
+
+def check_against_gram(r, g, tol=1e-10):
+    r = np.asarray(r)
+    assert np.all(np.tril(r, -1) == 0.0) and np.all(np.diag(r) >= 0)
+    assert rel(r.T @ r, g) <= tol
+    assert rel(r, O.gram_r(g)) <= tol
+
+
+@pytest.mark.parametrize("variant", ["footnote", "dense"])
+def test_c4_uniform_cartesian_full(P, variant):
+    """C4: 1e8 x 64 |x| 1e8 x 64 (1e16 join rows)."""
+    if not cgram.available():
+        pytest.skip("oracle/_build/libjqoracle.so not built")
+    import torch
+    m, n = 100_000_000, 64
+    a, b = device_tables(P, 4, m, n)
+    P.set_variant(variant)
+    try:
+        r = P.figaro_r(a, b).cpu().numpy()
+    finally:
+        P.set_variant("dense")
+        del a, b
+        torch.cuda.empty_cache()
+    g = cgram.join_gram(SEEDS[4][0], m, n, SEEDS[4][1], m, n)
+    check_against_gram(r, g)
+
+
+@pytest.fixture(scope="module")
+def c3_keys():
+    ka = np.sort(O.zipf_keys(3003, 10_000_000), kind="stable")
+    kb = np.sort(O.zipf_keys(3004, 10_000_000), kind="stable")
+    return ka, kb
+
+
+def test_c3_zipf_keys_bit_exact(P, c3_keys):
+    from paper_2503_23385_b200 import datagen
+    assert np.array_equal(datagen.zipf_sorted_keys(3003, 10_000_000), c3_keys[0])
+    assert np.array_equal(datagen.zipf_sorted_keys(3004, 10_000_000), c3_keys[1])
+
+
+def test_c3_grouping_bit_exact(P, c3_keys):
+    for x, y in zip(P.group_keys(*c3_keys), O.group_keys(*c3_keys)):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("variant", ["footnote", "dense"])
+def test_c3_zipf_join_full(P, c3_keys, variant):
+    """C3: Zipf(1.1) keys, 1e7 rows per side, 32 + 32 columns."""
+    m, n = 10_000_000, 32
+    a, b = device_tables(P, 3, m, n, c3_keys)
+    P.set_variant(variant)
+    try:
+        r = P.figaro_r(a, b).cpu().numpy()
+    finally:
+        P.set_variant("dense")
+    g = cgram.join_gram(SEEDS[3][0], m, n, SEEDS[3][1], m, n, *c3_keys)
+    check_against_gram(r, g)
+
+
+@pytest.mark.parametrize("variant", ["footnote", "dense"])
+def test_c5_full_svd(P, variant):
+    """C5: 1e6 x 128 |x| 1e6 x 128, singular values and right vectors."""
+    m, n = 1_000_000, 128
+    a, b = device_tables(P, 5, m, n)
+    P.set_variant(variant)
+    try:
+        s = P.figaro_svd(a, b, want_vectors=True)
+        r = P.figaro_r(a, b).cpu().numpy()
+    finally:
+        P.set_variant("dense")
+    g = cgram.join_gram(SEEDS[5][0], m, n, SEEDS[5][1], m, n)
+    check_against_gram(r, g)
+    vals = s.values.cpu().numpy()
+    v = s.right_vectors.cpu().numpy()
+    ref = O.gram_sigma(g)
+    assert np.max(np.abs(vals - ref)) <= 1e-10 * ref[0]
+    assert np.abs(v.T @ v - np.eye(2 * n)).max() <= 1e-10
+    assert rel(v @ np.diag(vals ** 2) @ v.T, r.T @ r) <= 1e-10
+
+
+def test_c2_natural_join_full_vs_spec_pipeline(P):
+    """C2: 10k keys x 100 rows per side, 16 + 16: against the SPEC pipeline itself."""
+    a, b = O.config_tables(2)
+    for variant in ("dense", "footnote"):
+        P.set_variant(variant)
+        try:
+            r = np.asarray(P.figaro_r(P.Table(a.data, a.keys), P.Table(b.data, b.keys)))
+            s = P.figaro_svd(P.Table(a.data, a.keys), P.Table(b.data, b.keys))
+        finally:
+            P.set_variant("dense")
+        if variant == "dense":
+            r_ref = O.figaro_r(a, b, lapack=True)
+            s_ref = np.linalg.svd(r_ref, compute_uv=False)
+        assert rel(np.abs(r), np.abs(r_ref)) <= 1e-10
+        assert rel(r.T @ r, r_ref.T @ r_ref) <= 1e-10
+        assert np.max(np.abs(np.asarray(s.values) - s_ref)) <= 1e-10 * s_ref[0]
+    for x, y in zip(P.group_keys(a.keys, b.keys), O.group_keys(a.keys, b.keys)):
+        assert np.array_equal(x, y)
