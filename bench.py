@@ -204,8 +204,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = CONFIGS[args.config]
-    if world > 1:
-        args.variant = "dense"   # the row-sharded path (sharded.py) is built on the dense reduction
+
 
     if args.impl == "reference":
         if rank != 0:
@@ -252,7 +251,7 @@ def main():
                 return P.figaro_svd(P.Table(A, ka), P.Table(B, kb), want_vectors=True).values
             return P.figaro_r(P.Table(A, ka), P.Table(B, kb))
         from paper_2503_23385_b200 import sharded
-        return sharded.figaro_r_sharded(A, B, m, m, a0)   # carry + R all-gathers over NCCL
+        return sharded.figaro_r_sharded(A, B, m, m, a0, a0)   # carry + R all-gathers over NCCL
 
     def timed(variant, steps):
         N.set_variant(variant)
@@ -287,7 +286,7 @@ def main():
         return ms, step_ms, stage, launches, clk
 
     other = "dense" if args.variant == "footnote" else "footnote"
-    ms_o, _, stage_o, _, _ = timed(other, max(1, min(args.steps, 3))) if world == 1 else (None, None, [], 0, None)
+    ms_o, _, stage_o, _, _ = timed(other, max(1, min(args.steps, 3)))
     ms, step_ms, stage, launches, clk = timed(args.variant, args.steps)
     value = jrows / (ms / 1e3)
 

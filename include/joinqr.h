@@ -137,12 +137,17 @@ JQ_API int jq_gen_zipf_sorted_keys(jq_ctx* ctx, uint64_t seed, int64_t rows, con
 JQ_API int jq_colsums(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, double* sums);
 /* Local R of one shard of a Cartesian product.  The shard holds A rows
  * [a_row0, a_row0 + a_rows) of an m1-row table and B rows [b_row0, b_row0 + b_rows)
- * of an m2-row table; b_prefix = sum of B rows [0, b_row0) and b_total = sum of
- * all B rows (n2 doubles each, from an all-gather of jq_colsums).  r_local is
- * n x n (n = n1 + n2), not canonical. */
+ * of an m2-row table; x_prefix = sum of the rows of X before the shard and
+ * x_total = sum of all rows of X (n1 / n2 doubles each, from an all-gather of
+ * jq_colsums).  Dense variant: the Claim-1 rows of the shard (a_prefix/a_total
+ * unused).  Footnote variant: tails of both sides plus, when include_head != 0,
+ * the single head row (exactly one rank passes 1).  r_local is n x n, not
+ * canonical; the stack of all ranks' r_local has the join's R (jq_tsqr_stack). */
 JQ_API int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1,
-                      const double* b, int64_t b_rows, int64_t n2, int64_t m2, int64_t b_row0,
-                      const double* b_prefix, const double* b_total, double* r_local);
+                             int64_t a_row0, const double* a_prefix, const double* a_total,
+                             const double* b, int64_t b_rows, int64_t n2, int64_t m2, int64_t b_row0,
+                             const double* b_prefix, const double* b_total, int include_head,
+                             double* r_local);
 /* Canonical R of the row stack [R_0; R_1; ...; R_{count-1}] (each n x n), by
  * the fixed binary TSQR tree — identical on every rank for the same input. */
 JQ_API int jq_tsqr_stack(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, double* r);

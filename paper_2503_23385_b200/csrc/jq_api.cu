@@ -225,6 +225,60 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   return rc;
 }
 
+// Footnote variant on one Cartesian row shard: tails of the local A rows (global
+// row index a_row0 + i, prefix a_prefix, scale sqrt(m2)) and of the local B rows,
+// plus the global head row when include_head.  Output: local R (n x n, not canonical).
+static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1, int64_t a_row0,
+                              const double* a_prefix, const double* a_total, const double* b, int64_t b_rows,
+                              int64_t n2, int64_t m2, int64_t b_row0, const double* b_prefix,
+                              const double* b_total, bool include_head, double* r_out) {
+  const int64_t n = n1 + n2;
+  SegScan sa{}, sb{};
+  if (n1 > 0) JQ_TRY(segscan_dev(ctx, a, a_rows, n1, nullptr, nullptr, nullptr, nullptr, 1, &sa));
+  if (n2 > 0) JQ_TRY(segscan_dev(ctx, b, b_rows, n2, nullptr, nullptr, nullptr, nullptr, 1, &sb));
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  double* ra = ws_alloc<double>(ctx, std::max<int64_t>(n1 * n1, 1));
+  double* rb = ws_alloc<double>(ctx, std::max<int64_t>(n2 * n2, 1));
+  double* rh = ws_alloc<double>(ctx, n * n);
+  double* stack = ws_alloc<double>(ctx, 3 * n * n);
+  double* heads = ws_alloc<double>(ctx, n);
+  if (!ra || !rb || !rh || !stack || !heads) return fail(JQ_E_OOM, "workspace exhausted (footnote shard)");
+  ctx->record_tsqr_events = false;
+  cudaEventRecord(ctx->ev[3], ctx->stream);
+  int rc = JQ_OK;
+  if (n1 > 0) {
+    FigaroArgs fa{};
+    fa.b = a; fa.m2 = a_rows; fa.n2 = n1;
+    fa.b_carry = sa.carry; fa.b_prefix0 = a_prefix;
+    fa.m1_global = m2; fa.m2_global = m1; fa.b_row0 = a_row0;
+    rc = figaro_tsqr_dev(ctx, fa, ra, false);
+  }
+  if (!rc && n2 > 0) {
+    FigaroArgs fb{};
+    fb.b = b; fb.m2 = b_rows; fb.n2 = n2;
+    fb.b_carry = sb.carry; fb.b_prefix0 = b_prefix;
+    fb.m1_global = m1; fb.m2_global = m2; fb.b_row0 = b_row0;
+    rc = figaro_tsqr_dev(ctx, fb, rb, false);
+  }
+  ctx->record_tsqr_events = true;
+  if (rc) return rc;
+  cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (include_head) {
+    head_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(a_total, (int)n1, b_total, (int)n2, nullptr,
+                                                                        nullptr, 1, m1, m2, heads);
+    JQ_CHECK_LAUNCH(ctx);
+    JQ_TRY(tsqr_dense_dev(ctx, heads, 1, n, rh, false));
+  } else {
+    JQ_CUDA(cudaMemsetAsync(rh, 0, n * n * 8, ctx->stream));
+  }
+  footnote_stack_kernel<<<(unsigned)cdiv(3 * n * n, 256), 256, 0, ctx->stream>>>(
+      rh, n1 > 0 ? ra : nullptr, (int)n1, n2 > 0 ? rb : nullptr, (int)n2, stack);
+  JQ_CHECK_LAUNCH(ctx);
+  rc = tsqr_stack_dev(ctx, stack, 3, n, r_out, false);
+  cudaEventRecord(ctx->ev[5], ctx->stream);
+  return rc;
+}
+
 // Device-resident figaro_r: R (n x n, canonical) into r_out (device).
 static int figaro_r_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
                         const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
@@ -438,42 +492,55 @@ int jq_figaro_svd(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const in
   return rc;
 }
 
-int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1,
-                      const double* b, int64_t b_rows, int64_t n2, int64_t m2, int64_t b_row0,
-                      const double* b_prefix, const double* b_total, double* r_local) {
+int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1, int64_t a_row0,
+                      const double* a_prefix, const double* a_total, const double* b, int64_t b_rows, int64_t n2,
+                      int64_t m2, int64_t b_row0, const double* b_prefix, const double* b_total, int include_head,
+                      double* r_local) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
   if (a_rows < 0 || b_rows < 0 || n1 < 0 || n2 < 0 || n1 + n2 == 0 || n1 + n2 > 256)
     return fail(JQ_E_INVALID, "bad shard geometry");
-  if (m1 <= 0 || m2 <= 0 || b_row0 < 0 || b_row0 + b_rows > m2)
+  if (m1 <= 0 || m2 <= 0 || b_row0 < 0 || b_row0 + b_rows > m2 || a_row0 < 0 || a_row0 + a_rows > m1)
     return fail(JQ_E_INVALID, "bad global sizes for the shard");
+  const bool foot = ctx->variant == 1;
+  if (foot && (!a_prefix || !a_total)) return fail(JQ_E_INVALID, "footnote shards need a_prefix and a_total");
   JQ_TRY(begin_call(ctx));
   const int64_t n = n1 + n2;
-  JQ_TRY(ws_reserve(ctx, stage_bytes(a, a_rows * n1) + stage_bytes(b, b_rows * n2) +
-                             stage_bytes(b_prefix, n2) + stage_bytes(b_total, n2) +
+  JQ_TRY(ws_reserve(ctx, stage_bytes(a, a_rows * n1) + stage_bytes(b, b_rows * n2) + stage_bytes(a_prefix, n1) +
+                             stage_bytes(a_total, n1) + stage_bytes(b_prefix, n2) + stage_bytes(b_total, n2) +
                              stage_bytes((const double*)r_local, n * n) +
                              figaro_ws(a_rows, n1, b_rows, n2, false, ctx->sms)));
-  const double *da, *db, *dpre, *dtot;
+  const double *da, *db, *dapre = nullptr, *datot = nullptr, *dpre, *dtot;
   double* dr;
   JQ_TRY(stage_in(ctx, a, a_rows * n1, &da));
   JQ_TRY(stage_in(ctx, b, b_rows * n2, &db));
+  JQ_TRY(stage_in(ctx, a_prefix, n1, &dapre));
+  JQ_TRY(stage_in(ctx, a_total, n1, &datot));
   JQ_TRY(stage_in(ctx, b_prefix, n2, &dpre));
   JQ_TRY(stage_in(ctx, b_total, n2, &dtot));
   JQ_TRY(stage_out(ctx, r_local, n * n, &dr));
+  ctx->timing.tsqr_ctas = 0;
+  ctx->timing.reduced_rows = 0;
   cudaEventRecord(ctx->ev[0], ctx->stream);
   cudaEventRecord(ctx->ev[1], ctx->stream);
-  SegScan ss{};
-  if (n2 > 0) JQ_TRY(segscan_dev(ctx, db, b_rows, n2, nullptr, nullptr, nullptr, nullptr, 1, &ss));
-  cudaEventRecord(ctx->ev[2], ctx->stream);
-  FigaroArgs fa{};
-  fa.a = da; fa.m1 = a_rows; fa.n1 = n1;
-  fa.b = db; fa.m2 = b_rows; fa.n2 = n2;
-  fa.b_totals = dtot;
-  fa.b_carry = n2 > 0 ? ss.carry : nullptr;
-  fa.b_prefix0 = dpre;
-  fa.m1_global = m1; fa.m2_global = m2; fa.b_row0 = b_row0;
-  JQ_TRY(figaro_tsqr_dev(ctx, fa, dr, false));
+  int rc = JQ_OK;
+  if (!foot) {
+    SegScan ss{};
+    if (n2 > 0) JQ_TRY(segscan_dev(ctx, db, b_rows, n2, nullptr, nullptr, nullptr, nullptr, 1, &ss));
+    cudaEventRecord(ctx->ev[2], ctx->stream);
+    FigaroArgs fa{};
+    fa.a = da; fa.m1 = a_rows; fa.n1 = n1;
+    fa.b = db; fa.m2 = b_rows; fa.n2 = n2;
+    fa.b_totals = dtot;
+    fa.b_carry = n2 > 0 ? ss.carry : nullptr;
+    fa.b_prefix0 = dpre;
+    fa.m1_global = m1; fa.m2_global = m2; fa.b_row0 = b_row0;
+    JQ_TRY(figaro_tsqr_dev(ctx, fa, dr, false));
+  } else {
+    JQ_TRY(footnote_shard_dev(ctx, da, a_rows, n1, m1, a_row0, dapre, datot, db, b_rows, n2, m2, b_row0, dpre,
+                              dtot, include_head != 0, dr));
+  }
   JQ_TRY(copy_out(ctx, r_local, (const double*)dr, n * n));
-  int rc = sync_and_check_flags(ctx);
+  rc = sync_and_check_flags(ctx);
   record_timing(ctx, false);
   return rc;
 }

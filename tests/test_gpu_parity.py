@@ -251,7 +251,8 @@ def test_zipf_keys_bit_exact(P):
 
 
 # ------------------------------------------------------------ shard building blocks
-def test_shard_r_and_stack_equal_single_device(P):
+@pytest.mark.parametrize("variant", ["dense", "footnote"])
+def test_shard_r_and_stack_equal_single_device(P, variant):
     """Row-sharded Cartesian figaro_r == unsharded figaro_r."""
     from paper_2503_23385_b200 import _native as N
     rng = np.random.default_rng(11)
@@ -259,22 +260,29 @@ def test_shard_r_and_stack_equal_single_device(P):
     A, B = rng.random((m1, n1)), rng.random((m2, n2))
     n = n1 + n2
     ref = np.asarray(P.figaro_r(P.Table(A), P.Table(B)))
-    for parts in (1, 2, 3, 5):
-        ab = np.linspace(0, m1, parts + 1).astype(int)
-        bb = np.linspace(0, m2, parts + 1).astype(int)
-        sums = np.stack([B[bb[p]:bb[p + 1]].sum(axis=0) for p in range(parts)])
-        total = sums.sum(axis=0)
-        rs = np.zeros((parts, n, n))
-        for p in range(parts):
-            pre = np.ascontiguousarray(sums[:p].sum(axis=0)) if p else np.zeros(n2)
-            a_sh = np.ascontiguousarray(A[ab[p]:ab[p + 1]])
-            b_sh = np.ascontiguousarray(B[bb[p]:bb[p + 1]])
-            N.check(N.lib().jq_figaro_r_shard(N.ctx(), a_sh.ctypes.data, len(a_sh), n1, m1,
-                                              b_sh.ctypes.data, len(b_sh), n2, m2, int(bb[p]),
-                                              pre.ctypes.data, total.ctypes.data, rs[p].ctypes.data))
-        r = np.zeros((n, n))
-        N.check(N.lib().jq_tsqr_stack(N.ctx(), rs.ctypes.data, parts, n, r.ctypes.data))
-        check_r(r, ref, 1e-12)
+    P.set_variant(variant)
+    try:
+        for parts in (1, 2, 3, 5):
+            ab = np.linspace(0, m1, parts + 1).astype(int)
+            bb = np.linspace(0, m2, parts + 1).astype(int)
+            sa = np.stack([A[ab[p]:ab[p + 1]].sum(axis=0) for p in range(parts)])
+            sb = np.stack([B[bb[p]:bb[p + 1]].sum(axis=0) for p in range(parts)])
+            ta, tb = sa.sum(axis=0), sb.sum(axis=0)
+            rs = np.zeros((parts, n, n))
+            for p in range(parts):
+                pa = np.ascontiguousarray(sa[:p].sum(axis=0)) if p else np.zeros(n1)
+                pb = np.ascontiguousarray(sb[:p].sum(axis=0)) if p else np.zeros(n2)
+                a_sh = np.ascontiguousarray(A[ab[p]:ab[p + 1]])
+                b_sh = np.ascontiguousarray(B[bb[p]:bb[p + 1]])
+                N.check(N.lib().jq_figaro_r_shard(N.ctx(), a_sh.ctypes.data, len(a_sh), n1, m1, int(ab[p]),
+                                                  pa.ctypes.data, ta.ctypes.data, b_sh.ctypes.data, len(b_sh), n2,
+                                                  m2, int(bb[p]), pb.ctypes.data, tb.ctypes.data, int(p == 0),
+                                                  rs[p].ctypes.data))
+            r = np.zeros((n, n))
+            N.check(N.lib().jq_tsqr_stack(N.ctx(), rs.ctypes.data, parts, n, r.ctypes.data))
+            check_r(r, ref, 1e-12)
+    finally:
+        P.set_variant("dense")
 
 
 def test_colsums(P):

@@ -29,7 +29,7 @@ def cpu_colsums(x):
     return x.sum(0)
 
 
-def cpu_shard_r(a, b, m1, m2, b_row0, prefix, total):
+def cpu_shard_r(a, b, m1, m2, a_row0, b_row0, a_prefix, a_total, prefix, total, include_head):
     """Local reduced rows of a Cartesian shard (SPEC.md:189-200 with a global prefix)."""
     a, b = a.numpy(), b.numpy()
     n1, n2 = a.shape[1], b.shape[1]
@@ -60,7 +60,7 @@ def _worker(rank, world, port, m1, m2, n1, n2, out):
     a0, a1 = sharded.shard_range(m1, world, rank)
     b0, b1 = sharded.shard_range(m2, world, rank)
     r = sharded.figaro_r_sharded(torch.from_numpy(A[a0:a1].copy()), torch.from_numpy(B[b0:b1].copy()),
-                                 m1, m2, b0, colsums=cpu_colsums, shard_r=cpu_shard_r, stack=cpu_stack)
+                                 m1, m2, a0, b0, colsums=cpu_colsums, shard_r=cpu_shard_r, stack=cpu_stack)
     out[rank] = r.numpy().tolist()
     dist.destroy_process_group()
 
