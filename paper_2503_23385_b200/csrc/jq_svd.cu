@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "jq_internal.cuh"
 
 namespace jq {
@@ -129,6 +131,105 @@ jacobi_kernel(double* __restrict__ A, double* __restrict__ V, int n, int want_v,
   }
 }
 
+// Multi-CTA variant: one CTA per column pair and round (np/2 CTAs, cooperative
+// launch, one grid-wide barrier per round).  Same pairs, rotation formula and
+// stopping rule as jacobi_kernel; the block reductions and the norm partials are
+// summed in a fixed order, so results are deterministic.  Thread i owns row i.
+constexpr int SVDC_THREADS = 256;
+
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* red) {
+  a = warp_sum(a); b = warp_sum(b); c = warp_sum(c);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) { red[warp] = a; red[32 + warp] = b; red[64 + warp] = c; }
+  __syncthreads();
+  a = b = c = 0.0;
+  for (int w = 0; w < nw; ++w) { a += red[w]; b += red[32 + w]; c += red[64 + w]; }
+}
+
+__global__ void __launch_bounds__(SVDC_THREADS)
+jacobi_coop_kernel(double* __restrict__ A, double* __restrict__ V, int n, int want_v, double tol, int max_sweeps,
+                   int* flags, double* __restrict__ part, int* __restrict__ rotated_sweep, double* __restrict__ values,
+                   double* __restrict__ vout, int n_out) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[96];
+  __shared__ double sig[256];
+  __shared__ int perm[256];
+  const int pi = blockIdx.x, i = threadIdx.x;
+  // |R|_F^2 (fixed-order two-level sum) -> negligible-column threshold
+  {
+    double f = 0.0;
+    for (int j = pi; j < n; j += gridDim.x)
+      if (i < n) f = fma(A[(size_t)j * n + i], A[(size_t)j * n + i], f);
+    double z1 = 0.0, z2 = 0.0;
+    block_sum3(f, z1, z2, red);
+    if (i == 0) part[pi] = f;
+  }
+  grid.sync();
+  double fro = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) fro += part[b];
+  const double eps = 2.220446049250313e-16;
+  const double tiny = (double(n) * eps) * (double(n) * eps) * fro;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int r = 0; r < n - 1; ++r) {
+      int p = rr_player(pi, r, n), q = rr_player(n - 1 - pi, r, n);
+      if (p > q) { const int tmp = p; p = q; q = tmp; }
+      double* ap = A + (size_t)p * n;
+      double* aq = A + (size_t)q * n;
+      const double x = i < n ? ap[i] : 0.0, y = i < n ? aq[i] : 0.0;
+      double al = x * x, be = y * y, ga = x * y;
+      block_sum3(al, be, ga, red);
+      const bool rot = !(al <= tiny || be <= tiny || ga == 0.0 || fabs(ga) < tol * (sqrt(al) * sqrt(be)));
+      if (rot) {
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = zeta >= 0.0 ? 1.0 / (zeta + sqrt(1.0 + zeta * zeta))
+                                     : -1.0 / (-zeta + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        if (i < n) {
+          ap[i] = c * x - s * y;
+          aq[i] = s * x + c * y;
+          if (want_v) {
+            double* vp = V + (size_t)p * n;
+            double* vq = V + (size_t)q * n;
+            const double u = vp[i], w = vq[i];
+            vp[i] = c * u - s * w;
+            vq[i] = s * u + c * w;
+          }
+        }
+        if (i == 0) rotated_sweep[sweep] = 1;  // benign race: every writer stores 1
+      }
+      grid.sync();
+    }
+    if (!*(volatile int*)&rotated_sweep[sweep]) break;
+  }
+  if (sweep == max_sweeps && pi == 0 && i == 0) atomicOr(flags, FLAG_NOCONV);
+  // sigma = column norms (CTA pi: columns pi, pi + grid, ...), then CTA 0 sorts
+  for (int j = pi; j < n; j += gridDim.x) {
+    double s = (i < n) ? A[(size_t)j * n + i] * A[(size_t)j * n + i] : 0.0, z1 = 0.0, z2 = 0.0;
+    block_sum3(s, z1, z2, red);
+    if (i == 0) part[j] = sqrt(s);
+  }
+  grid.sync();
+  if (pi != 0) return;
+  for (int j = i; j < n; j += blockDim.x) sig[j] = part[j];
+  __syncthreads();
+  for (int j = i; j < n; j += blockDim.x) {
+    int rank = 0;
+    const double sj = sig[j];
+    for (int k = 0; k < n; ++k) rank += (sig[k] > sj) || (sig[k] == sj && k < j);
+    perm[rank] = j;
+  }
+  __syncthreads();
+  for (int k = i; k < n_out; k += blockDim.x) values[k] = sig[perm[k]];
+  if (want_v && vout)
+    for (int idx = i; idx < n_out * n_out; idx += blockDim.x) {
+      const int r = idx / n_out, k = idx - r * n_out;
+      vout[idx] = V[(size_t)perm[k] * n + r];
+    }
+}
+
 // A_cm[j*np + i] = R[i*n + j] (zero padded to np), V = I
 __global__ void svd_init_kernel(const double* __restrict__ r, int n, int np, double* __restrict__ A,
                                 double* __restrict__ V) {
@@ -141,7 +242,7 @@ __global__ void svd_init_kernel(const double* __restrict__ r, int n, int np, dou
 
 size_t svd_ws_bytes(int64_t n) {
   const int64_t np = n + (n & 1);
-  return 2 * ws_bytes(size_t(np) * np, 8);
+  return 2 * ws_bytes(size_t(np) * np, 8) + ws_bytes(512, 8) + ws_bytes(128, 4);
 }
 
 int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values, double* v) {
@@ -153,6 +254,22 @@ int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values,
   if (!A || !V) return fail(JQ_E_OOM, "workspace exhausted (svd)");
   svd_init_kernel<<<(unsigned)cdiv(int64_t(np) * np, 256), 256, 0, ctx->stream>>>(r, (int)n, np, A, V);
   JQ_CHECK_LAUNCH(ctx);
+  if (np >= 32) {
+    // cooperative multi-CTA sweep: np/2 CTAs (<= 128, co-resident on 148 SMs)
+    double* part = ws_alloc<double>(ctx, 512);
+    int* rot = ws_alloc<int>(ctx, 128);
+    if (!part || !rot) return fail(JQ_E_OOM, "workspace exhausted (svd)");
+    JQ_CUDA(cudaMemsetAsync(rot, 0, 128 * sizeof(int), ctx->stream));
+    int npi = np, wv = want_v, ms = 64, nout = (int)n;
+    double tol = 1e-14;
+    double* vo = want_v ? v : nullptr;
+    int* fl = ctx->d_flags;
+    void* args[] = {&A, &V, &npi, &wv, &tol, &ms, &fl, &part, &rot, &values, &vo, &nout};
+    JQ_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_coop_kernel, dim3(np / 2), dim3(SVDC_THREADS), args, 0,
+                                        ctx->stream));
+    JQ_CHECK_LAUNCH(ctx);
+    return JQ_OK;
+  }
   jacobi_kernel<<<1, SVD_THREADS, 0, ctx->stream>>>(A, V, np, want_v, 1e-14, 64, ctx->d_flags, values,
                                                     want_v ? v : nullptr, (int)n);
   JQ_CHECK_LAUNCH(ctx);
