@@ -312,6 +312,146 @@ static int figaro_r_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, co
   return JQ_OK;
 }
 
+// ---- host-resident Cartesian inputs: streamed pipeline ------------------------
+// Each table is copied in row pieces (~512 MB, TILE_ROWS multiples) on a copy
+// stream into two alternating device buffers while the previous piece's
+// head/tail scan and TSQR run on the compute stream, so the PCIe transfer (the
+// bound of an end-to-end call from host memory) overlaps the compute.  Per piece:
+// segscan (carries relative to the piece) + prefix carried across pieces, the
+// piece's rows as a row shard of the virtual reduced matrix (FigaroArgs.b_row0 /
+// b_prefix0, exactly the multi-GPU shard machinery), one local R folded into a
+// running R by a 2-factor TSQR.  Deterministic for a fixed piece size.
+__global__ void vec_add_kernel(double* __restrict__ acc, const double* __restrict__ x, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc[i] += x[i];
+}
+__global__ void pack2_kernel(const double* __restrict__ r0, const double* __restrict__ r1, int n,
+                             double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n * n; i += gridDim.x * blockDim.x)
+    out[i] = i < n * n ? r0[i] : r1[i - n * n];
+}
+
+static bool use_streamed(const double* a, int64_t m1, int64_t n1, const double* b, int64_t m2, int64_t n2,
+                         const int64_t* ka) {
+  if (ka) return false;
+  if (is_device_ptr(a) || is_device_ptr(b)) return false;
+  return (m1 * n1 + m2 * n2) * 8 >= (int64_t(1) << 30);  // >= 1 GiB of input
+}
+
+static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const double* b, int64_t m2,
+                             int64_t n2, double* dr /* device, n x n canonical */) {
+  const int64_t n = n1 + n2;
+  const bool foot = ctx->variant == 1;
+  const int64_t piece_bytes = int64_t(512) << 20;
+  auto prows = [&](int64_t cols) {
+    int64_t pr = piece_bytes / (8 * std::max<int64_t>(cols, 1));
+    return std::max<int64_t>(TILE_ROWS, pr / TILE_ROWS * TILE_ROWS);
+  };
+  const int64_t pa = prows(n1), pb = prows(n2);
+  const int64_t buf_elems = std::max(std::min(pa, m1) * n1, std::min(pb, m2) * n2);
+  if (!ctx->copy_stream) {
+    JQ_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->pev) JQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int64_t maxp = std::max(pa, pb);
+  JQ_TRY(ws_reserve(ctx, 2 * ws_bytes(buf_elems, 8) + 12 * ws_bytes(n * n, 8) + 8 * ws_bytes(n, 8) +
+                             segscan_ws_bytes(maxp, std::max<int64_t>(std::max(n1, n2), 1), 1) +
+                             figaro_tsqr_ws_bytes(maxp, TILE_ROWS, n, ctx->sms) +
+                             tsqr_ws_bytes(3 * n, n, ctx->sms) + tsqr_ws_bytes(TILE_ROWS, n, ctx->sms)));
+  double* buf[2] = {ws_alloc<double>(ctx, buf_elems), ws_alloc<double>(ctx, buf_elems)};
+  double* racc[2] = {ws_alloc<double>(ctx, n * n), ws_alloc<double>(ctx, n * n)};  // per side (dense: [0] only)
+  double* rpiece = ws_alloc<double>(ctx, n * n);
+  double* pair = ws_alloc<double>(ctx, 2 * n * n);
+  double* pre[2] = {ws_alloc<double>(ctx, std::max<int64_t>(n1, 1)), ws_alloc<double>(ctx, std::max<int64_t>(n2, 1))};
+  double* heads = ws_alloc<double>(ctx, n);
+  double* rh = ws_alloc<double>(ctx, n * n);
+  double* stack = ws_alloc<double>(ctx, 3 * n * n);
+  if (!buf[1] || !stack) return fail(JQ_E_OOM, "workspace exhausted (streamed figaro)");
+  JQ_CUDA(cudaMemsetAsync(pre[0], 0, std::max<int64_t>(n1, 1) * 8, ctx->stream));
+  JQ_CUDA(cudaMemsetAsync(pre[1], 0, std::max<int64_t>(n2, 1) * 8, ctx->stream));
+  const size_t mark = ctx->ws.used;
+  ctx->timing.tsqr_ctas = 0;
+  ctx->timing.reduced_rows = 0;
+  ctx->record_tsqr_events = false;
+  cudaEventRecord(ctx->ev[0], ctx->stream);
+  int64_t k = 0;  // global piece counter (buffer parity)
+  bool first[2] = {true, true};
+  // side 0 = A, side 1 = B.  Dense: B first (top rows need head(B)), footnote: any order.
+  const int order[2] = {foot ? 0 : 1, foot ? 1 : 0};
+  for (int oi = 0; oi < 2; ++oi) {
+    const int side = order[oi];
+    const double* host = side == 0 ? a : b;
+    const int64_t m = side == 0 ? m1 : m2, cols = side == 0 ? n1 : n2;
+    if (cols == 0) continue;
+    const int64_t pr = side == 0 ? pa : pb;
+    for (int64_t r0 = 0; r0 < m; r0 += pr, ++k) {
+      const int64_t rows = std::min(pr, m - r0);
+      const int bi = int(k & 1);
+      ctx->ws.used = mark;
+      // copy piece k into buf[bi] once piece k-2 (same buffer) has been consumed
+      if (k >= 2) JQ_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->pev[2 + bi], 0));
+      JQ_CUDA(cudaMemcpyAsync(buf[bi], host + r0 * cols, rows * cols * 8, cudaMemcpyHostToDevice,
+                              ctx->copy_stream));
+      JQ_CUDA(cudaEventRecord(ctx->pev[bi], ctx->copy_stream));
+      JQ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->pev[bi], 0));
+      SegScan ss{};
+      JQ_TRY(segscan_dev(ctx, buf[bi], rows, cols, nullptr, nullptr, nullptr, nullptr, 1, &ss));
+      FigaroArgs fa{};
+      const int rs = foot ? side : 0;  // running-R slot
+      double* pfx = pre[side];
+      const int64_t nn = foot ? cols : n;
+      if (!foot && side == 0) {
+        // dense top rows [sqrt(m2) A_i | head(B)]: head from the complete B total
+        fa.a = buf[bi]; fa.m1 = rows; fa.n1 = n1; fa.n2 = n2;
+        fa.b_totals = pre[1]; fa.m1_global = m1; fa.m2_global = m2;
+      } else {
+        // tails: the "B-part" of a source with an empty A-part (dense: n1 zero columns first)
+        fa.n1 = foot ? 0 : n1;
+        fa.b = buf[bi]; fa.m2 = rows; fa.n2 = cols;
+        fa.b_carry = ss.carry; fa.b_prefix0 = pfx; fa.b_row0 = r0;
+        fa.m1_global = side == 0 ? m2 : m1;   // tails of A scale by sqrt(m2), of B by sqrt(m1)
+        fa.m2_global = m;
+      }
+      JQ_TRY(figaro_tsqr_dev(ctx, fa, rpiece, false));
+      if (!(!foot && side == 0)) {
+        vec_add_kernel<<<1, 256, 0, ctx->stream>>>(pfx, ss.totals, (int)cols);  // prefix += piece sum
+        JQ_CHECK_LAUNCH(ctx);
+      }
+      JQ_CUDA(cudaEventRecord(ctx->pev[2 + bi], ctx->stream));
+      if (first[rs]) {
+        JQ_CUDA(cudaMemcpyAsync(racc[rs], rpiece, nn * nn * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        first[rs] = false;
+      } else {
+        pack2_kernel<<<(unsigned)cdiv(2 * nn * nn, 256), 256, 0, ctx->stream>>>(racc[rs], rpiece, (int)nn, pair);
+        JQ_CHECK_LAUNCH(ctx);
+        JQ_TRY(tsqr_stack_dev(ctx, pair, 2, nn, racc[rs], false));
+      }
+    }
+  }
+  ctx->ws.used = mark;
+  cudaEventRecord(ctx->ev[4], ctx->stream);
+  int rc = JQ_OK;
+  if (!foot) {
+    canonicalize_dev(ctx, racc[0], n, dr);
+  } else {
+    head_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(pre[0], (int)n1, pre[1], (int)n2, nullptr,
+                                                                        nullptr, 1, m1, m2, heads);
+    JQ_CHECK_LAUNCH(ctx);
+    rc = tsqr_dense_dev(ctx, heads, 1, n, rh, false);
+    if (!rc) {
+      footnote_stack_kernel<<<(unsigned)cdiv(3 * n * n, 256), 256, 0, ctx->stream>>>(
+          rh, n1 > 0 ? racc[0] : nullptr, (int)n1, n2 > 0 ? racc[1] : nullptr, (int)n2, stack);
+      JQ_CHECK_LAUNCH(ctx);
+      rc = tsqr_stack_dev(ctx, stack, 3, n, dr, true);
+    }
+  }
+  ctx->record_tsqr_events = true;
+  cudaEventRecord(ctx->ev[5], ctx->stream);
+  cudaEventRecord(ctx->ev[1], ctx->stream);
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  cudaEventRecord(ctx->ev[3], ctx->stream);
+  return rc;
+}
+
 static void record_timing(jq_ctx* ctx, bool svd) {
   jq_timing& t = ctx->timing;
   t.group_ms = ev_ms(ctx, 0, 1);
@@ -374,6 +514,8 @@ int jq_ctx_destroy(jq_ctx* ctx) {
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (auto& e : ctx->pev) if (e) cudaEventDestroy(e);
   delete ctx;
   return JQ_OK;
 }
@@ -442,6 +584,20 @@ int jq_figaro_r(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int6
   JQ_TRY(check_tables(m1, n1, ka, m2, n2, kb));
   JQ_TRY(begin_call(ctx));
   const int64_t n = n1 + n2;
+  if (use_streamed(a, m1, n1, b, m2, n2, ka)) {
+    double* dr = nullptr;
+    if (is_device_ptr(r)) {
+      dr = r;
+    } else {
+      JQ_CUDA(cudaMallocAsync(&dr, n * n * 8, ctx->stream));
+    }
+    int rc = figaro_r_streamed(ctx, a, m1, n1, b, m2, n2, dr);
+    if (rc == JQ_OK && dr != r) rc = copy_out(ctx, r, (const double*)dr, n * n);
+    int rc2 = sync_and_check_flags(ctx);
+    if (dr != r) cudaFreeAsync(dr, ctx->stream);
+    record_timing(ctx, false);
+    return rc ? rc : rc2;
+  }
   JQ_TRY(ws_reserve(ctx, stage_bytes(a, m1 * n1) + stage_bytes(b, m2 * n2) + stage_bytes(ka, m1) +
                              stage_bytes(kb, m2) + stage_bytes((const double*)r, n * n) +
                              figaro_ws(m1, n1, m2, n2, ka != nullptr, ctx->sms)));

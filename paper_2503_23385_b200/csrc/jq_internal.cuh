@@ -65,6 +65,8 @@ struct jq_ctx {
   int64_t launches = 0;
   jq_timing timing{};
   cudaEvent_t ev[8]{};
+  cudaStream_t copy_stream = nullptr;   // host -> device piece copies (streamed figaro)
+  cudaEvent_t pev[4]{};                 // piece copied / consumed events
 };
 
 namespace jq {

@@ -309,3 +309,21 @@ def test_determinism(P, variant):
     a, b = P.Table(rng.random((30000, 16))), P.Table(rng.random((30000, 16)))
     r1, r2 = P.figaro_r(a, b), P.figaro_r(a, b)
     assert np.array_equal(r1, r2)
+
+
+@pytest.mark.parametrize("variant", ["dense", "footnote"])
+def test_streamed_host_path_matches_device_path(P, variant):
+    """>= 1 GiB of host input takes the pipelined H2D path (pieces of 512 MB on a copy
+    stream overlapped with the per-piece scan + TSQR); same R as the device path."""
+    import torch
+    from paper_2503_23385_b200 import datagen
+    m, n = 1_100_000, 64                       # 2 x 563 MB of host input, 2 pieces per table
+    a = datagen.uniform(77, m, n)
+    b = datagen.uniform(78, m + 3, n)
+    P.set_variant(variant)
+    try:
+        r_host = np.asarray(P.figaro_r(P.Table(a), P.Table(b)))
+        r_dev = P.figaro_r(P.Table(torch.from_numpy(a).cuda()), P.Table(torch.from_numpy(b).cuda())).cpu().numpy()
+    finally:
+        P.set_variant("dense")
+    check_r(r_host, r_dev, 1e-12)
