@@ -39,6 +39,7 @@
 // (jq_headtail.cu), so the reduced matrix never exists in HBM.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "jq_internal.cuh"
 
@@ -104,11 +105,13 @@ struct Cfg {
   static constexpr int OFF_TAU = OFF_U + 64;
   static constexpr int OFF_SC = OFF_TAU + 8;  // reflector scales of the panel
   static constexpr int OFF_P = OFF_SC + 8;    // column dot partials [2 parity][WARPS][8]
-  static constexpr int OFF_X = OFF_P + 2 * WARPS * 8;  // per-warp raw column broadcast [WARPS][KW]
-  static constexpr int OFF_S = OFF_X + WARPS * KW;     // running prefix sums (Figaro source, <= NP)
+  static constexpr int OFF_S = OFF_P + 2 * WARPS * 8;  // running prefix sums (Figaro source, <= NP)
   static constexpr int OFF_LD = OFF_S + NP;   // loader scratch: 3 per-row coefficients + 2 per thread
   static constexpr int SZ_LD = 3 * K + 2 * THREADS;
-  static constexpr int OFF_BAR = OFF_LD + SZ_LD;  // mbarrier (8 bytes)
+  static constexpr int OFF_M = OFF_LD + SZ_LD;    // M' (8 x LDT): Y = X M' of the Gram panel
+  static constexpr int OFF_RST = OFF_M + 8 * LDT; // staged R rows of the Gram panel (8 x 8)
+  static constexpr int OFF_FLAG = OFF_RST + 64;   // Gram panel accepted (1) / explicit fallback (0)
+  static constexpr int OFF_BAR = OFF_FLAG + 2;    // mbarrier (8 bytes)
   static constexpr int TOTAL = OFF_BAR + 2;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
@@ -346,10 +349,9 @@ __device__ long long g_ptime[16];
 // On return cp holds Y (scaled) and Yt (this warp's rows) / T / R rows are written.
 template <class C>
 __device__ __forceinline__ void factor_panel_all(double (&cp)[C::KWT][2], double* R, const int j0, double* Ytw,
-                                                 double* T, double* U, double* taus, double* scs, double* Xw,
+                                                 double* T, double* U, double* taus, double* scs,
                                                  double* P, const int warp, const int lane) {
   const int g = lane >> 2, t = lane & 3;
-  (void)Xw;
   // The panel's R rows are final at panel start (reflector jj rewrites only row
   // j0+jj): the next column's entries are prefetched one column ahead.
   double alpha_n = R[rix<C>(j0, j0)], rg_n = R[rix<C>(j0, j0 + g)];
@@ -448,6 +450,112 @@ __device__ __forceinline__ void factor_panel_all(double (&cp)[C::KWT][2], double
   }
 }
 
+// ------------------------------------------------------------------ Gram panel
+// Householder factorisation of the stacked panel [R_p; X] (R_p: the panel's 8 R rows,
+// X: the chunk's K rows of the panel columns, CTA-wide) computed from the 8 x 8 Gram
+// G = X^T X alone.  Reflector i (alpha = R[i][i], |x_i'|^2 = G[i][i]) only needs inner
+// products of the current columns, and applying it is the rank-2 update
+//   x_c <- x_c + a_c x_i  =>  G[g][c] += a_g G[i][c] + a_c G[g][i] + a_g a_c G[i][i],
+// so the 8-step chain runs on registers (two Gram entries per lane, accumulator
+// layout) with no row data, no CTA barrier and a latency independent of K.  The
+// columns are tracked as x' = X M; the trailing update uses Y = X M' (M' = M diag(scale))
+// through 8 x 8 products.  Cancellation guard: step i is accepted only if
+//   alpha^2 + G[i][i] >= 1e-2 (alpha^2 + P_i),   P_i = G0[i][i] + sum a_i^2 |x_k'|^2,
+// which bounds the relative rounding error of |[alpha; x_i']|^2 by ~1e-13; otherwise the
+// panel is redone by factor_panel_all (explicit row data).  Run by warp 0 only.
+template <class C>
+__device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double* R, const int j0, double* T,
+                                                  double* Mg, double* Rst, const int lane) {
+  const int g = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
+  double M0 = (g == c0) ? 1.0 : 0.0, M1 = (g == c1) ? 1.0 : 0.0;
+  double T0 = 0.0, T1 = 0.0;  // T[g][c0], T[g][c1], built one column per step
+  double P = __shfl_sync(FULL, (g & 1) ? G[1] : G[0], 4 * g + (g >> 1));  // G0[g][g]
+  double sc0 = 0.0, sc1 = 0.0;
+  bool ok = true;
+  double alpha_n = R[rix<C>(j0, j0)], rg_n = R[rix<C>(j0, j0 + g)];
+  double r0_n = R[rix<C>(j0, j0 + c0)], r1_n = R[rix<C>(j0, j0 + c1)];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double alpha = alpha_n, rg = rg_n, r0 = r0_n, r1 = r1_n;
+    if (i < 7) {
+      alpha_n = R[rix<C>(j0 + i + 1, j0 + i + 1)];
+      rg_n = R[rix<C>(j0 + i + 1, j0 + g)];
+      r0_n = R[rix<C>(j0 + i + 1, j0 + c0)];
+      r1_n = R[rix<C>(j0 + i + 1, j0 + c1)];
+    }
+    const double e = (i & 1) ? G[1] : G[0];
+    const double d0 = __shfl_sync(FULL, G[0], 4 * i + t);        // G[i][c0]
+    const double d1 = __shfl_sync(FULL, G[1], 4 * i + t);        // G[i][c1]
+    const double dg = __shfl_sync(FULL, e, 4 * g + (i >> 1));    // G[g][i]
+    const double sj = __shfl_sync(FULL, e, 4 * i + (i >> 1));    // G[i][i]
+    const double Pi = __shfl_sync(FULL, P, 4 * i);
+    const double mgi = __shfl_sync(FULL, (i & 1) ? M1 : M0, 4 * g + (i >> 1));  // M[g][i]
+    const double s2 = fma(alpha, alpha, sj);
+    ok = ok && (s2 >= 1e-2 * fma(alpha, alpha, Pi));
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (sj > 0.0) {
+      if (s2 > 1e-280 && s2 < 1e280) {
+        const double rn = rsqrt_nr(s2);
+        const double nrm = s2 * rn;
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = fma(fabs(alpha), rn, 1.0);
+        scale = rcp_nr(alpha - beta);
+      } else {
+        const double nrm = sqrt(s2);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+    }
+    const double twg = tau * fma(scale, dg, rg), tw0 = tau * fma(scale, d0, r0), tw1 = tau * fma(scale, d1, r1);
+    const double ag = g > i ? -twg * scale : 0.0;
+    const double a0 = c0 > i ? -tw0 * scale : 0.0;
+    const double a1 = c1 > i ? -tw1 * scale : 0.0;
+    if (t == 0 && g >= i) Rst[i * 8 + g] = g > i ? rg - twg : beta;
+    // T column i: T[g][i] = -tau_i sum_m T[g][m] (y_m . y_i),  y_m . y_i = sc_m sc_i G[m][i]
+    // (entries of T for columns >= i and scales of columns > i are still zero)
+    double tp = fma(T1 * sc1, d1, T0 * sc0 * d0);
+    tp += __shfl_xor_sync(FULL, tp, 1);
+    tp += __shfl_xor_sync(FULL, tp, 2);
+    const double tgi = g < i ? -tau * scale * tp : (g == i ? tau : 0.0);
+    if (c0 == i) { sc0 = scale; T0 = tgi; }
+    if (c1 == i) { sc1 = scale; T1 = tgi; }
+    G[0] = fma(ag * a0, sj, fma(a0, dg, fma(ag, d0, G[0])));
+    G[1] = fma(ag * a1, sj, fma(a1, dg, fma(ag, d1, G[1])));
+    M0 = fma(a0, mgi, M0);
+    M1 = fma(a1, mgi, M1);
+    P = fma(ag * ag, sj, P);
+  }
+  *reinterpret_cast<double2*>(Mg + g * C::LDT + c0) = make_double2(M0 * sc0, M1 * sc1);
+  *reinterpret_cast<double2*>(T + g * C::LDT + c0) = make_double2(T0, T1);
+  return ok;
+}
+
+// T (8 x 8 upper triangular) of the compact WY form from U[m][j] = x_m . x_j (m < j),
+// taus and scales: T[r][r] = tau_r, T[r][j] = -tau_j sum_{m=r}^{j-1} T[r][m] (y_m . y_j).
+// Lanes 0..7 of the calling warp (U / taus / scs visible to them).
+template <class C>
+__device__ __forceinline__ void compute_T(double* T, const double* U, const double* taus, const double* scs,
+                                          const int lane) {
+  if (lane < 8) {
+    const int r = lane;
+    double sc[8], tu[8], trow[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) { sc[m] = scs[m]; tu[m] = taus[m]; }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) trow[m] = (m == r) ? tu[m] : 0.0;
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < j; ++m) acc = fma(trow[m], (U[m * 8 + j] * sc[m]) * sc[j], acc);
+      if (j > r) trow[j] = -tu[j] * acc;
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
+  }
+}
+
 // ------------------------------------------------------------------ the kernel
 // Each CTA: R (init zero, or R_init[cta]) absorbs its rows [row_begin, row_end)
 // of `src`, then writes R (NP x NP, row-major, zeros below the diagonal) to
@@ -487,13 +595,15 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   double* Ws = smem_dyn + C::OFF_WS;
   double* S = smem_dyn + C::OFF_S;
   double* scratch = smem_dyn + C::OFF_LD;
+  double* Mg = smem_dyn + C::OFF_M;
+  double* Rst = smem_dyn + C::OFF_RST;
+  volatile double* flag = smem_dyn + C::OFF_FLAG;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int64_t cta = blockIdx.x;
   double* Ytw = smem_dyn + C::OFF_YT + warp * C::SZ_YT;
-  double* Xw = smem_dyn + C::OFF_X + warp * C::KW;
 
   double* R;
   if constexpr (C::R_SMEM) R = smem_dyn + C::OFF_R;
@@ -538,7 +648,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
     const uint32_t bytes = uint32_t(nr) * uint32_t(rcol) * 8u;
     bulk_fetch(bar, raw, s.ptr(v0), bytes & ~15u);
   };
-  if (use_tma && tid == 0 && row_begin < row_end) issue(row_begin, row_begin);
+  if ((use_tma & 1) && tid == 0 && row_begin < row_end) issue(row_begin, row_begin);
 
   double c[C::NLT][C::KWT][2];  // this warp's rows of every column tile (C^T accumulator layout)
   uint32_t phase = 0;
@@ -556,7 +666,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
       const int64_t pv0 = row0 + (int64_t)h * rb;
       const int nr = pass_nrows(pv0, rb, row0);
       const int nel = nr * rcol;
-      if (use_tma) {
+      if (use_tma & 1) {
         mbar_wait(bar, phase);
         phase ^= 1;
         if ((nel & 1) && tid == 0) raw[nel - 1] = __ldg(s.ptr(pv0) + nel - 1);  // 8-byte tail
@@ -579,7 +689,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
           }
       }
       __syncthreads();  // raw consumed: prefetch the next pass / chunk behind the panel loop
-      if (use_tma && tid == 0) {
+      if ((use_tma & 1) && tid == 0) {
         const bool same = h + 1 < npass && pv0 + rb < row_end;
         const int64_t nv0 = same ? pv0 + rb : row0 + C::K;
         if (nv0 < row_end) issue(nv0, same ? row0 : nv0);
@@ -590,19 +700,70 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
 #pragma unroll 1
     for (int p = 0; p < C::NLT; ++p) {
       const int j0 = 8 * p;
-      // ---------------- panel factorisation by all warps (panel tile copied out of c[])
-      double cp[C::KWT][2];
+      double cp[C::KWT][2];  // panel tile X (this warp's rows)
 #pragma unroll
       for (int q = 0; q < C::NLT; ++q)
         if (q == p)
 #pragma unroll
           for (int it = 0; it < C::KWT; ++it) { cp[it][0] = c[q][it][0]; cp[it][1] = c[q][it][1]; }
-      if (JQ_PROBE != 2 && JQ_PROBE != 3)
-        factor_panel_all<C>(cp, R, j0, Ytw, T, U, taus, scs, Xw, P, warp, lane);
+      // ---------------- (1) partial Gram X^T X (slot p) and partial (X^T C_q)^T of the
+      // trailing tiles, X^T rows of this warp for the apply step
+      {
+        double z[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0};
+#pragma unroll
+        for (int it = 0; it < C::KWT; ++it) {
+          dmma(z, cp[it][0], cp[it][0]);
+          dmma(z2, cp[it][1], cp[it][1]);
+        }
+        *reinterpret_cast<double2*>(Zp + (warp * C::NLT + p) * 64 + 2 * lane) = make_double2(z[0] + z2[0], z[1] + z2[1]);
+      }
+#pragma unroll
+      for (int q = 0; q < C::NLT; ++q) {
+        if (q > p) {
+          double z[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0};
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it) {
+            dmma(z, c[q][it][0], cp[it][0]);
+            dmma(z2, c[q][it][1], cp[it][1]);
+          }
+          *reinterpret_cast<double2*>(Zp + (warp * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0] + z2[0], z[1] + z2[1]);
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < C::KWT; ++it)
+        *reinterpret_cast<double2*>(Ytw + g * C::LDYT + 8 * it + 2 * t) = make_double2(cp[it][0], cp[it][1]);
+      __syncthreads();
       KT_MARK(1);
-      // ---------------- trailing update:  Z = R_rows + Y^T C,  W = T^T Z,  R_rows -= W,  C -= Y W
-      // (1) partial Z^T over this warp's rows, B operand = Y straight from registers
-      if (JQ_PROBE != 1 && JQ_PROBE != 3) {
+      // ---------------- (2) the 8-column Householder chain on the summed Gram (warp 0)
+      if (warp == 0) {
+        double G[2] = {0.0, 0.0};
+#pragma unroll
+        for (int w = 0; w < C::WARPS; ++w) {  // fixed order
+          const double2 gg = *reinterpret_cast<const double2*>(Zp + (w * C::NLT + p) * 64 + 2 * lane);
+          G[0] += gg.x;
+          G[1] += gg.y;
+        }
+        const bool ok = factor_panel_gram<C>(G, R, j0, T, Mg, Rst, lane) && !(use_tma & 2);
+        __syncwarp();
+        if (ok) {  // commit the panel's R rows
+          for (int k = lane; k < 64; k += 32) {
+            const int r = k >> 3, cc = k & 7;
+            if (cc >= r) R[rix<C>(j0 + r, j0 + cc)] = Rst[k];
+          }
+        }
+        if (lane == 0) flag[0] = ok ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      if (flag[0] == 0.0) {
+        // cancellation: explicit factorisation from the row data (rare; CTA-uniform)
+        factor_panel_all<C>(cp, R, j0, Ytw, T, U, taus, scs, P, warp, lane);  // cp <- Y, Ytw <- Y^T
+        if (warp == 0) {
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int e = 2 * lane + k, r = e >> 3, cc = e & 7;
+            Mg[r * C::LDT + cc] = r == cc ? 1.0 : 0.0;
+          }
+        }
 #pragma unroll
         for (int q = 0; q < C::NLT; ++q) {
           if (q > p) {
@@ -615,31 +776,38 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
             *reinterpret_cast<double2*>(Zp + (warp * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0], z[1]);
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
       KT_MARK(2);
-      // (2) tile q is reduced by warp q % WARPS: fixed-order sum + R rows, W = T^T Z, R -= W
+      // ---------------- (3) tile q by warp q % WARPS:  Z^T = R_rows^T + S M',  W^T = Z^T T,
+      // R_rows -= W,  V^T = W^T M'^T  (S = sum of the partials, fixed order)
       if (JQ_PROBE != 1 && JQ_PROBE != 3) {
         for (int q = p + 1 + ((warp - (p + 1)) % C::WARPS + C::WARPS) % C::WARPS; q < C::NLT; q += C::WARPS) {
           const int l0 = q * 8;
           const int r0i = rix<C>(j0 + 2 * t, l0 + g), r1i = rix<C>(j0 + 2 * t + 1, l0 + g);
-          double z0 = R[r0i], z1 = R[r1i];
+          double s0 = 0.0, s1 = 0.0;
 #pragma unroll
           for (int w = 0; w < C::WARPS; ++w) {
             const double2 zz = *reinterpret_cast<const double2*>(Zp + (w * C::NLT + q) * 64 + 2 * lane);
-            z0 += zz.x;
-            z1 += zz.y;
+            s0 += zz.x;
+            s1 += zz.y;
           }
+          double zt[2] = {R[r0i], R[r1i]};
+          dmma(zt, s0, Mg[(2 * t) * C::LDT + g]);
+          dmma(zt, s1, Mg[(2 * t + 1) * C::LDT + g]);
           double wv[2] = {0.0, 0.0};
-          dmma(wv, z0, T[(2 * t) * C::LDT + g]);
-          dmma(wv, z1, T[(2 * t + 1) * C::LDT + g]);
+          dmma(wv, zt[0], T[(2 * t) * C::LDT + g]);
+          dmma(wv, zt[1], T[(2 * t + 1) * C::LDT + g]);
           R[r0i] -= wv[0];
           R[r1i] -= wv[1];
-          *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-wv[0], -wv[1]);
+          double vv[2] = {0.0, 0.0};
+          dmma(vv, wv[0], Mg[g * C::LDT + 2 * t]);
+          dmma(vv, wv[1], Mg[g * C::LDT + 2 * t + 1]);
+          *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-vv[0], -vv[1]);
         }
       }
       __syncthreads();
-      // (3) C -= Y W on this warp's rows (A = -W^T from smem, B = Y^T rows of this warp)
+      // ---------------- (4) C_q -= X V on this warp's rows (A = -V^T from smem, B = X^T rows)
       if (JQ_PROBE != 1 && JQ_PROBE != 3) {
 #pragma unroll
         for (int q = 0; q < C::NLT; ++q) {
@@ -653,6 +821,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
           }
         }
       }
+      __syncwarp();  // Ytw read by the whole warp before the next panel rewrites it
       KT_MARK(3);
     }
     __syncthreads();
@@ -672,6 +841,286 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
       const int r = idx / C::NP, c2 = idx - r * C::NP;
       if (c2 < r) out[idx] = 0.0;
     }
+  }
+}
+
+// ------------------------------------------------------------------ warp-independent TSQR
+// v5 layout for NP <= 64: every WARP is an independent streaming-TSQR leaf with its
+// own packed R in shared memory.  A CTA round loads K = WARPS * KW rows (the
+// TMA + prep loader of tsqr_kernel, CTA barriers only at pass boundaries); warp w
+// then absorbs rows [w*KW, (w+1)*KW) of the round into its R.  The Householder
+// column chain needs only warp shuffles (no CTA barrier per column), and the eight
+// warps' chains and DMMA updates interleave freely on the SM.  Each CTA writes
+// WARPS leaf factors, combined by the same fixed binary tree.
+template <int NP_>
+struct CfgW {
+  static constexpr int NP = NP_;
+  static constexpr int NLT = NP / 8;
+  static constexpr int WARPS = 4;           // small CTAs: two or more per SM overlap one's load phase with another's panels
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int KW = 32;             // rows per warp per round (registers: NP*KW/32 doubles)
+  static constexpr int KWT = KW / 8;
+  static constexpr int K = WARPS * KW;      // rows per CTA round
+  static constexpr bool R_SMEM = true;
+  static constexpr int MIN_CTAS = NP <= 32 ? 4 : 2;
+  __host__ __device__ static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
+  static constexpr int LDT = 10;
+  static constexpr int LDYT = KW + 2;
+  static constexpr int RAW = NP * 32;
+  static constexpr int SZ_R = rp_off(NLT);  // per warp
+  static constexpr int OFF_R = 0;
+  static constexpr int OFF_YT = OFF_R + WARPS * SZ_R;      // [WARPS][8][LDYT]
+  static constexpr int SZ_YT = 8 * LDYT;
+  static constexpr int OFF_T = OFF_YT + WARPS * SZ_YT;     // [WARPS][8][LDT]
+  static constexpr int OFF_U = OFF_T + WARPS * 8 * LDT;    // [WARPS][64]
+  static constexpr int OFF_TAU = OFF_U + WARPS * 64;       // [WARPS][8]
+  static constexpr int OFF_SC = OFF_TAU + WARPS * 8;       // [WARPS][8]
+  static constexpr int OFF_RAW = OFF_SC + WARPS * 8;
+  static constexpr int OFF_S = OFF_RAW + RAW;
+  static constexpr int OFF_BAR = OFF_S + NP;
+  static constexpr int TOTAL = OFF_BAR + 2;
+  // loader scratch (3 per-row coefficients + 2 per thread) lives only during the
+  // load phase: it aliases the Y^T / T / U area of the panel loop
+  static constexpr int OFF_LD = OFF_YT;
+  static constexpr int SZ_LD = 3 * K + 2 * THREADS;
+  static_assert(SZ_LD <= OFF_RAW - OFF_YT, "loader scratch alias");
+  static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+// Householder factorisation of one 8-column panel by ONE warp over its KW rows
+// stacked under its own R (same dlarfg convention and reflector algebra as
+// factor_panel_all; the column sums need only the quad butterflies).
+template <class C>
+__device__ __forceinline__ void factor_panel_warp(double (&cp)[C::KWT][2], double* R, const int j0, double* Ytw,
+                                                  double* T, double* U, double* taus, double* scs, const int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  double alpha_n = R[rix<C>(j0, j0)], rg_n = R[rix<C>(j0, j0 + g)];
+  double scale_g = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const double alpha = alpha_n, rgj = rg_n;
+    if (jj < 7) {
+      alpha_n = R[rix<C>(j0 + jj + 1, j0 + jj + 1)];
+      rg_n = R[rix<C>(j0 + jj + 1, j0 + g)];
+    }
+    double xv[C::KWT][2];
+#pragma unroll
+    for (int it = 0; it < C::KWT; ++it) {
+      xv[it][0] = __shfl_sync(FULL, cp[it][0], jj * 4 + t);
+      xv[it][1] = __shfl_sync(FULL, cp[it][1], jj * 4 + t);
+    }
+    double dp0 = 0.0, dp1 = 0.0, sp0 = 0.0, sp1 = 0.0;
+#pragma unroll
+    for (int it = 0; it < C::KWT; ++it) {
+      dp0 = fma(xv[it][0], cp[it][0], dp0);
+      dp1 = fma(xv[it][1], cp[it][1], dp1);
+      sp0 = fma(xv[it][0], xv[it][0], sp0);
+      sp1 = fma(xv[it][1], xv[it][1], sp1);
+    }
+    double d = dp0 + dp1, sj = sp0 + sp1;
+    d += __shfl_xor_sync(FULL, d, 1);
+    sj += __shfl_xor_sync(FULL, sj, 1);
+    d += __shfl_xor_sync(FULL, d, 2);
+    sj += __shfl_xor_sync(FULL, sj, 2);
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (sj != 0.0) {  // warp-uniform: every quad holds the same |x|^2
+      const double s2 = fma(alpha, alpha, sj);
+      if (s2 > 1e-280 && s2 < 1e280) {
+        const double rn = rsqrt_nr(s2);
+        const double nrm = s2 * rn;
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = fma(fabs(alpha), rn, 1.0);
+        scale = rcp_nr(alpha - beta);
+      } else {
+        const double nrm = sqrt(alpha * alpha + sj);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+    }
+    const double tw = tau * fma(scale, d, rgj);
+    const double a = g > jj ? -tw * scale : 0.0;
+#pragma unroll
+    for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) cp[it][b] = fma(a, xv[it][b], cp[it][b]);
+    if (g == jj) scale_g = scale;
+    if (t == 0) {
+      if (g >= jj) R[rix<C>(j0 + jj, j0 + g)] = g > jj ? rgj - tw : beta;
+      else U[g * 8 + jj] = d;
+      if (g == jj) { taus[jj] = tau; scs[jj] = scale; }
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < C::KWT; ++it) {
+    cp[it][0] *= scale_g;
+    cp[it][1] *= scale_g;
+    *reinterpret_cast<double2*>(Ytw + g * C::LDYT + 8 * it + 2 * t) = make_double2(cp[it][0], cp[it][1]);
+  }
+  __syncwarp();
+  {
+    // T row r = lane & 7 (computed branch-free by every lane, stored by lanes < 8)
+    const int r = lane & 7;
+    double sc[8], tu[8], trow[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) { sc[m] = scs[m]; tu[m] = taus[m]; }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) trow[m] = (m == r) ? tu[m] : 0.0;
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int m = 0; m < j; ++m) {
+        const double v = trow[m] * ((U[m * 8 + j] * sc[m]) * sc[j]);
+        if (m & 1) acc1 += v; else acc0 += v;
+      }
+      if (j > r) trow[j] = -tu[j] * (acc0 + acc1);
+    }
+    if (lane < 8) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
+    }
+  }
+  __syncwarp();
+}
+
+template <class C, class Src>
+__global__ void __launch_bounds__(C::THREADS, C::MIN_CTAS)
+tsqr_wkernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __restrict__ r_out, int use_tma) {
+  extern __shared__ __align__(16) double smem_dyn[];
+  double* raw = smem_dyn + C::OFF_RAW;
+  double* S = smem_dyn + C::OFF_S;
+  double* scratch = smem_dyn + C::OFF_LD;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t cta = blockIdx.x;
+  double* R = smem_dyn + C::OFF_R + warp * C::SZ_R;
+  double* Ytw = smem_dyn + C::OFF_YT + warp * C::SZ_YT;
+  double* T = smem_dyn + C::OFF_T + warp * 8 * C::LDT;
+  double* U = smem_dyn + C::OFF_U + warp * 64;
+  double* taus = smem_dyn + C::OFF_TAU + warp * 8;
+  double* scs = smem_dyn + C::OFF_SC + warp * 8;
+
+  Src s = src;
+  const int64_t row_begin = cta * rows_per_cta;
+  const int64_t row_end = min(total_rows, row_begin + rows_per_cta);
+  for (int idx = lane; idx < C::SZ_R; idx += 32) R[idx] = 0.0;
+  s.template begin<C>(S, row_begin);
+  if (tid == 0) mbar_init(bar);
+  __syncthreads();
+
+  auto pass_nrows = [&](int64_t v0, int rb, int64_t chunk0) -> int {
+    int64_t lim = chunk0 + C::K < row_end ? chunk0 + C::K : row_end;
+    int64_t nr = lim - v0 < (int64_t)rb ? lim - v0 : (int64_t)rb;
+    const int64_t av = s.avail(v0);
+    nr = av < nr ? av : nr;
+    return nr > 0 ? (int)nr : 0;
+  };
+  auto issue = [&](int64_t v0, int64_t chunk0) {
+    const int rcol = s.rc(v0);
+    const int nr = pass_nrows(v0, pass_rows<C>(rcol), chunk0);
+    const uint32_t bytes = uint32_t(nr) * uint32_t(rcol) * 8u;
+    bulk_fetch(bar, raw, s.ptr(v0), bytes & ~15u);
+  };
+  if (use_tma && tid == 0 && row_begin < row_end) issue(row_begin, row_begin);
+
+  double c[C::NLT][C::KWT][2];
+  uint32_t phase = 0;
+  KT_DECL
+
+  for (int64_t row0 = row_begin; row0 < row_end; row0 += C::K) {
+    const int rcol = s.rc(row0);
+    const int rb = pass_rows<C>(rcol);
+    const int npass = (C::K + rb - 1) / rb;
+#pragma unroll
+    for (int q = 0; q < C::NLT; ++q)
+#pragma unroll
+      for (int it = 0; it < C::KWT; ++it) c[q][it][0] = c[q][it][1] = 0.0;
+    __syncthreads();  // every warp left the previous round's panel loop (scratch aliases Y^T/T/U)
+    for (int h = 0; h < npass && row0 + (int64_t)h * rb < row_end; ++h) {
+      const int64_t pv0 = row0 + (int64_t)h * rb;
+      const int nr = pass_nrows(pv0, rb, row0);
+      const int nel = nr * rcol;
+      if (use_tma) {
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        if ((nel & 1) && tid == 0) raw[nel - 1] = __ldg(s.ptr(pv0) + nel - 1);
+      } else {
+        const double* src_rows = s.ptr(pv0);
+        for (int e = tid; e < nel; e += C::THREADS) raw[e] = __ldg(src_rows + e);
+      }
+      __syncthreads();
+      s.template prep<C>(raw, S, scratch, pv0, nr);
+      __syncthreads();
+      // this warp's rows of the pass (skipped when the pass holds none of them)
+      const int lo = warp * C::KW - h * rb;
+      if (lo < rb && lo + C::KW > 0) {
+#pragma unroll
+        for (int q = 0; q < C::NLT; ++q) {
+          const int l = q * 8 + g;
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              const int li = lo + 8 * it + 2 * t + b;
+              if (li >= 0 && li < rb) c[q][it][b] = s.template value<C>(raw, scratch, pv0, li, l, nr, rcol);
+            }
+        }
+      }
+      __syncthreads();
+      if (use_tma && tid == 0) {
+        const bool same = h + 1 < npass && pv0 + rb < row_end;
+        const int64_t nv0 = same ? pv0 + rb : row0 + C::K;
+        if (nv0 < row_end) issue(nv0, same ? row0 : nv0);
+      }
+    }
+    KT_MARK(0);
+#pragma unroll 1
+    for (int p = 0; p < C::NLT; ++p) {
+      const int j0 = 8 * p;
+      double cp[C::KWT][2];
+#pragma unroll
+      for (int q = 0; q < C::NLT; ++q)
+        if (q == p)
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it) { cp[it][0] = c[q][it][0]; cp[it][1] = c[q][it][1]; }
+      factor_panel_warp<C>(cp, R, j0, Ytw, T, U, taus, scs, lane);
+      KT_MARK(1);
+      // trailing tiles q > p:  Z^T = R_rows^T + C^T Y,  W^T = Z^T T,  R_rows -= W,  C -= Y W
+#pragma unroll
+      for (int q = 0; q < C::NLT; ++q) {
+        if (q > p) {
+          const int r0i = rix<C>(j0 + 2 * t, 8 * q + g), r1i = rix<C>(j0 + 2 * t + 1, 8 * q + g);
+          double z[2] = {R[r0i], R[r1i]}, z2[2] = {0.0, 0.0};
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it) {
+            dmma(z, c[q][it][0], cp[it][0]);
+            dmma(z2, c[q][it][1], cp[it][1]);
+          }
+          double wv[2] = {0.0, 0.0};
+          dmma(wv, z[0] + z2[0], T[(2 * t) * C::LDT + g]);
+          dmma(wv, z[1] + z2[1], T[(2 * t + 1) * C::LDT + g]);
+          R[r0i] -= wv[0];
+          R[r1i] -= wv[1];
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it) {
+            dmma(c[q][it], -wv[0], Ytw[(2 * t) * C::LDYT + 8 * it + g]);
+            dmma(c[q][it], -wv[1], Ytw[(2 * t + 1) * C::LDYT + 8 * it + g]);
+          }
+        }
+      }
+      __syncwarp();  // R rows / Y^T / T of this panel consumed before the next panel rewrites them
+      KT_MARK(3);
+    }
+    KT_MARK(4);
+  }
+  KT_FLUSH();
+  double* out = r_out + (cta * C::WARPS + warp) * C::NP * C::NP;
+  for (int idx = lane; idx < C::NP * C::NP; idx += 32) {
+    const int r = idx / C::NP, c2 = idx - r * C::NP;
+    out[idx] = c2 >= r ? R[rix<C>(r, c2)] : 0.0;
   }
 }
 
@@ -713,6 +1162,7 @@ static int ctas_per_sm() {
     cudaGetLastError();
     n = 1;
   }
+  if (const char* e = getenv("JQ_TSQR_CTAS_PER_SM")) n = std::min(n, atoi(e));  // experiments
   return std::max(1, n);
 }
 
@@ -722,6 +1172,12 @@ static int launch_tsqr(jq_ctx* ctx, int grid, const Src& src, int64_t rows_per_c
                        int use_tma) {
   auto kern = tsqr_kernel<C, Src, COMBINE>;
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  // JQ_TSQR_EXPLICIT=1: every panel takes the explicit (row data) path (tests / A-B timing)
+  static const bool explicit_panels = [] {
+    const char* e = getenv("JQ_TSQR_EXPLICIT");
+    return e && e[0] == '1';
+  }();
+  if (explicit_panels) use_tma |= 2;
   kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, rows_per_cta, total_rows, r_init,
                                                    init_count, r_out, use_tma);
   JQ_CHECK_LAUNCH(ctx);
@@ -746,7 +1202,7 @@ static int tree_combine(jq_ctx* ctx, double* a, double* b, int64_t count, double
 size_t tsqr_ws_bytes(int64_t rows, int64_t n, int sms) {
   int np = np_for(n);
   if (np < 0) return 0;
-  int64_t leaves = std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 32, cdiv(rows, 64)));
+  int64_t leaves = std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 32, cdiv(rows, 32) + 16));
   return 2 * ws_bytes(size_t(leaves) * np * np, sizeof(double)) + ws_bytes(size_t(np) * np, 8);
 }
 
@@ -780,13 +1236,71 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   return JQ_OK;
 }
 
+// warp-independent leaves (tsqr_wkernel, experimental: JQ_TSQR_IMPL=warp) for NP <= 64;
+// the default is the CTA-wide kernel
+static bool warp_impl() {
+  static const bool w = [] {
+    const char* e = getenv("JQ_TSQR_IMPL");
+    return e && e[0] == 'w';
+  }();
+  return w;
+}
+
+template <class CW, class Src>
+static int run_stream_w(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
+                        bool canonical, double* r_out, int use_tma) {
+  using C = Cfg<CW::NP>;  // tree combine
+  align = std::max<int64_t>(align, CW::K);
+  if (align % CW::K) return fail(JQ_E_INVALID, "row alignment must be a multiple of the TSQR round");
+  static int occ = [] {
+    int o = 0;
+    cudaFuncSetAttribute(tsqr_wkernel<CW, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CW::SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tsqr_wkernel<CW, Src>, CW::THREADS, CW::SMEM) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      o = 1;
+    }
+    if (const char* e = getenv("JQ_TSQR_CTAS_PER_SM")) o = std::min(o, atoi(e));
+    return std::max(1, o);
+  }();
+  int64_t max_ctas = int64_t(ctx->sms) * occ;
+  int64_t units = std::max<int64_t>(1, cdiv(vrows, align));
+  int64_t ctas = std::min(max_ctas, units);
+  int64_t rows_per_cta = cdiv(units, ctas) * align;
+  ctas = std::max<int64_t>(1, cdiv(vrows, rows_per_cta));
+  const int64_t leaves = ctas * CW::WARPS;
+  double* a = ws_alloc<double>(ctx, size_t(leaves) * C::NP * C::NP);
+  double* b = ws_alloc<double>(ctx, size_t((leaves + 1) / 2) * C::NP * C::NP + 1);
+  if (!a || !b) return fail(JQ_E_OOM, "workspace exhausted (TSQR leaves)");
+  ctx->timing.tsqr_ctas += ctas;
+  ctx->timing.reduced_rows += vrows;
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
+  auto kern = tsqr_wkernel<CW, Src>;
+  JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CW::SMEM));
+  kern<<<(int)ctas, CW::THREADS, CW::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a, use_tma);
+  JQ_CHECK_LAUNCH(ctx);
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
+  double* fin = nullptr;
+  JQ_TRY(tree_combine<C>(ctx, a, b, leaves, &fin));
+  finalize_r_kernel<<<(int)cdiv(int64_t(n) * n, 256), 256, 0, ctx->stream>>>(fin, C::NP, n, canonical, r_out);
+  JQ_CHECK_LAUNCH(ctx);
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[5], ctx->stream);
+  return JQ_OK;
+}
+
 template <class Src>
 static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
                            bool canonical, double* r_out, int use_tma) {
   switch (np_for(n)) {
-    case 16: return run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-    case 32: return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-    case 64: return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+    case 16:
+      return warp_impl() ? run_stream_w<CfgW<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
+                         : run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+    case 32:
+      return warp_impl() ? run_stream_w<CfgW<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
+                         : run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+    case 64:
+      return warp_impl() ? run_stream_w<CfgW<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
+                         : run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 128: return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
   }

@@ -30,4 +30,4 @@ names = ["load", "factor/arrive", "barrier wait", "update", "chunk-end barrier"]
 tot = sum(buf[i] for i in range(5))
 print(f"variant={a.variant} ctas(launches incl. tree)={ctas} tsqr_ms={t['tsqr_ms']:.2f}")
 for i, nm in enumerate(names):
-    print(f"  {nm:20s} {buf[i] / tot:6.1%}")
+    print(f"  {nm:20s} {buf[i] / tot:6.1%}  {buf[i] / 1e6:12.1f} Mcycles (sum over warps)")
