@@ -194,8 +194,9 @@ struct FigaroSrc {
           g = fa.gid_a ? fa.gid_a[r] : 0;
           if (g >= 0) m2g = fa.gid_a ? (double)fa.b_count[g] : (double)fa.m2_global;
         }
-        c1[i] = sqrt(m2g);
-        c2[i] = g >= 0 ? rsqrt(m2g) : 0.0;
+        const double rs2 = g >= 0 && m2g > 0.0 ? rsqrt_nr(m2g) : 0.0;
+        c1[i] = m2g * rs2;  // sqrt(m2g)
+        c2[i] = rs2;
         mode[i] = (double)g;
       }
       return;
@@ -222,10 +223,11 @@ struct FigaroSrc {
           if (rr == 0) {
             md = 1.0;
           } else {
-            const double si = sqrt((double)rr), si1 = sqrt((double)rr + 1.0), sm = sqrt(m1g);
+            // sqrt(r)/sqrt(r+1) sqrt(m1g) = r a2,  a2 = sqrt(m1g) / sqrt(r (r+1))  (MUFU + Newton)
+            const double rd = (double)rr;
             md = 2.0;
-            a1 = si / si1 * sm;
-            a2 = sm / (si * si1);
+            a2 = (m1g * rsqrt_nr(m1g)) * rsqrt_nr(rd * (rd + 1.0));
+            a1 = rd * a2;
           }
         }
       }
@@ -238,15 +240,24 @@ struct FigaroSrc {
     const int rps = (nrows + nseg - 1) / nseg;
     const int c = threadIdx.x % n2, seg = threadIdx.x / n2;
     const bool active = threadIdx.x < nseg * n2;
+    // rows are processed in batches of 4 (loads issued together, then the short
+    // sequential recurrence in registers)
     double loc = 0.0, reset = 0.0;
+    const int i0 = seg * rps, i1 = min(nrows, i0 + rps);
     if (active) {
-      for (int k = 0; k < rps; ++k) {
-        const int i = seg * rps + k;
-        if (i >= nrows) break;
-        const double xv = raw[i * n2 + c];
-        const int md = (int)mode[i];
-        if (md == 1) { loc = xv; reset = 1.0; }
-        else if (md == 2) loc += xv;
+      for (int ib = i0; ib < i1; ib += 4) {
+        double xv[4], md[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool in = ib + k < i1;
+          xv[k] = in ? raw[(ib + k) * n2 + c] : 0.0;
+          md[k] = in ? mode[ib + k] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (md[k] == 1.0) { loc = xv[k]; reset = 1.0; }
+          else if (md[k] == 2.0) loc += xv[k];
+        }
       }
       ls[seg * n2 + c] = loc;
       rs[seg * n2 + c] = reset;
@@ -259,15 +270,25 @@ struct FigaroSrc {
     }
     __syncthreads();  // every thread of a column has read S before the last segment rewrites it
     if (active) {
-      for (int k = 0; k < rps; ++k) {
-        const int i = seg * rps + k;
-        if (i >= nrows) break;
-        const double xv = raw[i * n2 + c];
-        const int md = (int)mode[i];
-        double out = 0.0;
-        if (md == 1) sv = xv;
-        else if (md == 2) { out = fma(c1[i], xv, -c2[i] * sv); sv += xv; }
-        raw[i * n2 + c] = out;
+      for (int ib = i0; ib < i1; ib += 4) {
+        double xv[4], md[4], a1[4], a2[4], out[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool in = ib + k < i1;
+          xv[k] = in ? raw[(ib + k) * n2 + c] : 0.0;
+          md[k] = in ? mode[ib + k] : 0.0;
+          a1[k] = in ? c1[ib + k] : 0.0;
+          a2[k] = in ? c2[ib + k] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          out[k] = 0.0;
+          if (md[k] == 1.0) sv = xv[k];
+          else if (md[k] == 2.0) { out[k] = fma(a1[k], xv[k], -a2[k] * sv); sv += xv[k]; }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (ib + k < i1) raw[(ib + k) * n2 + c] = out[k];
       }
       if (seg == nseg - 1) S[c] = sv;
     }
