@@ -148,6 +148,10 @@ struct DenseSrc {
   __device__ double value(const double* raw, const double*, int64_t, int i, int l, int nrows, int rcols) const {
     return (i < nrows && l < rcols) ? raw[i * rcols + l] : 0.0;
   }
+  // warp-specialised loader (tsqr_ws_kernel): chunk rows never cross limit(v0)
+  __device__ int64_t limit(int64_t) const { return INT64_MAX; }
+  template <class C>
+  __device__ void prep_warp(double*, double*, double*, int64_t, int, int) const {}
 };
 
 struct FigaroSrc {
@@ -294,6 +298,91 @@ struct FigaroSrc {
     }
   }
 
+  __device__ int64_t limit(int64_t v0) const { return v0 < m1pad ? m1pad : INT64_MAX; }
+
+  // prep by ONE warp (the loader warp of tsqr_ws_kernel): per-row scalars, then the
+  // B-part tail transform in place, lane = column (sequential over the chunk rows,
+  // loads batched by 4); S is the running prefix of the loader.
+  template <class C>
+  __device__ void prep_warp(double* raw, double* S, double* scratch, int64_t v0, int nrows, int lane) const {
+    double* c1 = scratch;
+    double* c2 = scratch + C::K;
+    double* mode = scratch + 2 * C::K;
+    if (v0 < m1pad) {
+      for (int i = lane; i < C::K; i += 32) {
+        int g = -1;
+        double m2g = 0.0;
+        if (i < nrows) {
+          const int64_t r = v0 + i;
+          g = fa.gid_a ? fa.gid_a[r] : 0;
+          if (g >= 0) m2g = fa.gid_a ? (double)fa.b_count[g] : (double)fa.m2_global;
+        }
+        const double rs2 = g >= 0 && m2g > 0.0 ? rsqrt_nr(m2g) : 0.0;
+        c1[i] = m2g * rs2;
+        c2[i] = rs2;
+        mode[i] = (double)g;
+      }
+      __syncwarp();
+      return;
+    }
+    const int64_t b0 = v0 - m1pad;
+    for (int i = lane; i < C::K; i += 32) {
+      double md = 0.0, a1 = 0.0, a2 = 0.0;
+      if (i < nrows) {
+        const int64_t br = b0 + i;
+        int64_t rr = 0;
+        double m1g = 0.0;
+        bool valid = true;
+        if (fa.gid_b) {
+          const int g = fa.gid_b[br];
+          valid = g >= 0;
+          if (valid) { rr = br - fa.b_start[g]; m1g = (double)fa.a_count[g]; }
+        } else {
+          rr = fa.b_row0 + br;
+          m1g = (double)fa.m1_global;
+        }
+        if (valid) {
+          if (rr == 0) {
+            md = 1.0;
+          } else {
+            const double rd = (double)rr;
+            md = 2.0;
+            a2 = (m1g * rsqrt_nr(m1g)) * rsqrt_nr(rd * (rd + 1.0));
+            a1 = rd * a2;
+          }
+        }
+      }
+      c1[i] = a1; c2[i] = a2; mode[i] = md;
+    }
+    __syncwarp();
+    const int n2 = (int)fa.n2;
+    for (int c = lane; c < n2; c += 32) {
+      double sv = S[c];
+      for (int ib = 0; ib < nrows; ib += 4) {
+        double xv[4], md[4], a1[4], a2[4], out[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool in = ib + k < nrows;
+          xv[k] = in ? raw[(ib + k) * n2 + c] : 0.0;
+          md[k] = in ? mode[ib + k] : 0.0;
+          a1[k] = in ? c1[ib + k] : 0.0;
+          a2[k] = in ? c2[ib + k] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          out[k] = 0.0;
+          if (md[k] == 1.0) sv = xv[k];
+          else if (md[k] == 2.0) { out[k] = fma(a1[k], xv[k], -a2[k] * sv); sv += xv[k]; }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (ib + k < nrows) raw[(ib + k) * n2 + c] = out[k];
+      }
+      S[c] = sv;
+    }
+    __syncwarp();
+  }
+
   template <class C>
   __device__ double value(const double* raw, const double* scratch, int64_t v0, int i, int l, int nrows,
                           int rcols) const {
@@ -368,7 +457,14 @@ __device__ long long g_ptime[16];
 // x . c_g, one quad reduction, and a CTA-wide fixed-order sum of the WARPS partials
 // gives d_g (g = j: |x|^2; g > j: reflector dot product; g < j: T entries).
 // On return cp holds Y (scaled) and Yt (this warp's rows) / T / R rows are written.
-template <class C>
+// bar.sync id, n: a barrier among the n threads (whole warps) that execute it
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// NW = warps holding rows (partials summed in warp order), BAR = 0: __syncthreads,
+// else named barrier BAR over those NW warps; `warp` = the caller's row-warp index.
+template <class C, int NW = C::WARPS, int BAR = 0>
 __device__ __forceinline__ void factor_panel_all(double (&cp)[C::KWT][2], double* R, const int j0, double* Ytw,
                                                  double* T, double* U, double* taus, double* scs,
                                                  double* P, const int warp, const int lane) {
@@ -400,13 +496,14 @@ __device__ __forceinline__ void factor_panel_all(double (&cp)[C::KWT][2], double
     double d = dp0 + dp1;
     d += __shfl_xor_sync(FULL, d, 1);
     d += __shfl_xor_sync(FULL, d, 2);
-    double* Pj = P + (jj & 1) * (C::WARPS * 8);
+    double* Pj = P + (jj & 1) * (NW * 8);
     if (t == 0) Pj[warp * 8 + g] = d;
-    __syncthreads();
+    if (BAR == 0) __syncthreads();
+    else named_bar(BAR, NW * 32);
     d = 0.0;
     double sj = 0.0;
 #pragma unroll
-    for (int w = 0; w < C::WARPS; ++w) {  // fixed order: bit-identical in every warp
+    for (int w = 0; w < NW; ++w) {  // fixed order: bit-identical in every warp
       d += Pj[w * 8 + g];
       sj += Pj[w * 8 + jj];
     }
@@ -471,87 +568,6 @@ __device__ __forceinline__ void factor_panel_all(double (&cp)[C::KWT][2], double
   }
 }
 
-// ------------------------------------------------------------------ Gram panel
-// Householder factorisation of the stacked panel [R_p; X] (R_p: the panel's 8 R rows,
-// X: the chunk's K rows of the panel columns, CTA-wide) computed from the 8 x 8 Gram
-// G = X^T X alone.  Reflector i (alpha = R[i][i], |x_i'|^2 = G[i][i]) only needs inner
-// products of the current columns, and applying it is the rank-2 update
-//   x_c <- x_c + a_c x_i  =>  G[g][c] += a_g G[i][c] + a_c G[g][i] + a_g a_c G[i][i],
-// so the 8-step chain runs on registers (two Gram entries per lane, accumulator
-// layout) with no row data, no CTA barrier and a latency independent of K.  The
-// columns are tracked as x' = X M; the trailing update uses Y = X M' (M' = M diag(scale))
-// through 8 x 8 products.  Cancellation guard: step i is accepted only if
-//   alpha^2 + G[i][i] >= 1e-2 (alpha^2 + P_i),   P_i = G0[i][i] + sum a_i^2 |x_k'|^2,
-// which bounds the relative rounding error of |[alpha; x_i']|^2 by ~1e-13; otherwise the
-// panel is redone by factor_panel_all (explicit row data).  Run by warp 0 only.
-template <class C>
-__device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double* R, const int j0, double* T,
-                                                  double* Mg, double* Rst, const int lane) {
-  const int g = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
-  double M0 = (g == c0) ? 1.0 : 0.0, M1 = (g == c1) ? 1.0 : 0.0;
-  double T0 = 0.0, T1 = 0.0;  // T[g][c0], T[g][c1], built one column per step
-  double P = __shfl_sync(FULL, (g & 1) ? G[1] : G[0], 4 * g + (g >> 1));  // G0[g][g]
-  double sc0 = 0.0, sc1 = 0.0;
-  bool ok = true;
-  double alpha_n = R[rix<C>(j0, j0)], rg_n = R[rix<C>(j0, j0 + g)];
-  double r0_n = R[rix<C>(j0, j0 + c0)], r1_n = R[rix<C>(j0, j0 + c1)];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const double alpha = alpha_n, rg = rg_n, r0 = r0_n, r1 = r1_n;
-    if (i < 7) {
-      alpha_n = R[rix<C>(j0 + i + 1, j0 + i + 1)];
-      rg_n = R[rix<C>(j0 + i + 1, j0 + g)];
-      r0_n = R[rix<C>(j0 + i + 1, j0 + c0)];
-      r1_n = R[rix<C>(j0 + i + 1, j0 + c1)];
-    }
-    const double e = (i & 1) ? G[1] : G[0];
-    const double d0 = __shfl_sync(FULL, G[0], 4 * i + t);        // G[i][c0]
-    const double d1 = __shfl_sync(FULL, G[1], 4 * i + t);        // G[i][c1]
-    const double dg = __shfl_sync(FULL, e, 4 * g + (i >> 1));    // G[g][i]
-    const double sj = __shfl_sync(FULL, e, 4 * i + (i >> 1));    // G[i][i]
-    const double Pi = __shfl_sync(FULL, P, 4 * i);
-    const double mgi = __shfl_sync(FULL, (i & 1) ? M1 : M0, 4 * g + (i >> 1));  // M[g][i]
-    const double s2 = fma(alpha, alpha, sj);
-    ok = ok && (s2 >= 1e-2 * fma(alpha, alpha, Pi));
-    double tau = 0.0, beta = alpha, scale = 0.0;
-    if (sj > 0.0) {
-      if (s2 > 1e-280 && s2 < 1e280) {
-        const double rn = rsqrt_nr(s2);
-        const double nrm = s2 * rn;
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = fma(fabs(alpha), rn, 1.0);
-        scale = rcp_nr(alpha - beta);
-      } else {
-        const double nrm = sqrt(s2);
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-    }
-    const double twg = tau * fma(scale, dg, rg), tw0 = tau * fma(scale, d0, r0), tw1 = tau * fma(scale, d1, r1);
-    const double ag = g > i ? -twg * scale : 0.0;
-    const double a0 = c0 > i ? -tw0 * scale : 0.0;
-    const double a1 = c1 > i ? -tw1 * scale : 0.0;
-    if (t == 0 && g >= i) Rst[i * 8 + g] = g > i ? rg - twg : beta;
-    // T column i: T[g][i] = -tau_i sum_m T[g][m] (y_m . y_i),  y_m . y_i = sc_m sc_i G[m][i]
-    // (entries of T for columns >= i and scales of columns > i are still zero)
-    double tp = fma(T1 * sc1, d1, T0 * sc0 * d0);
-    tp += __shfl_xor_sync(FULL, tp, 1);
-    tp += __shfl_xor_sync(FULL, tp, 2);
-    const double tgi = g < i ? -tau * scale * tp : (g == i ? tau : 0.0);
-    if (c0 == i) { sc0 = scale; T0 = tgi; }
-    if (c1 == i) { sc1 = scale; T1 = tgi; }
-    G[0] = fma(ag * a0, sj, fma(a0, dg, fma(ag, d0, G[0])));
-    G[1] = fma(ag * a1, sj, fma(a1, dg, fma(ag, d1, G[1])));
-    M0 = fma(a0, mgi, M0);
-    M1 = fma(a1, mgi, M1);
-    P = fma(ag * ag, sj, P);
-  }
-  *reinterpret_cast<double2*>(Mg + g * C::LDT + c0) = make_double2(M0 * sc0, M1 * sc1);
-  *reinterpret_cast<double2*>(T + g * C::LDT + c0) = make_double2(T0, T1);
-  return ok;
-}
-
 // T (8 x 8 upper triangular) of the compact WY form from U[m][j] = x_m . x_j (m < j),
 // taus and scales: T[r][r] = tau_r, T[r][j] = -tau_j sum_{m=r}^{j-1} T[r][m] (y_m . y_j).
 // Lanes 0..7 of the calling warp (U / taus / scs visible to them).
@@ -575,6 +591,109 @@ __device__ __forceinline__ void compute_T(double* T, const double* U, const doub
 #pragma unroll
     for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
   }
+}
+
+// ------------------------------------------------------------------ Gram panel
+#ifdef JQ_KTIME
+__device__ unsigned long long g_gram_fail[16];
+#endif
+// Householder factorisation of the stacked panel [R_p; X] (R_p: the panel's 8 R rows,
+// X: the chunk's K rows of the panel columns, CTA-wide) computed from the 8 x 8 Gram
+// G = X^T X alone.  Reflector i (alpha = R[i][i], |x_i'|^2 = G[i][i]) only needs inner
+// products of the current columns, and applying it is the rank-2 update
+//   x_c <- x_c + a_c x_i  =>  G[g][c] += a_g G[i][c] + a_c G[g][i] + a_g a_c G[i][i],
+// so the 8-step chain runs on registers (two Gram entries per lane, accumulator
+// layout) with no row data, no CTA barrier and a latency independent of K.  The
+// columns are tracked as x' = X M; the trailing update uses Y = X M' (M' = M diag(scale))
+// through 8 x 8 products.  Cancellation guard: step i is accepted only if
+//   alpha^2 + G[i][i] >= 1e-2 (alpha^2 + P_i),   P_i = G0[i][i] + sum a_i^2 |x_k'|^2,
+// which bounds the relative rounding error of |[alpha; x_i']|^2 by ~1e-13; otherwise the
+// panel is redone by factor_panel_all (explicit row data).  Run by warp 0 only.
+template <class C>
+__device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2], const double* Rs,
+                                                  const int j0, double* T, double* Mg, double* Us, double* taus,
+                                                  double* scs, const int lane) {
+  // Rs/j0: R in shared memory (read only); Rb: on return the panel's new 8 x 8 R block
+  // in accumulator layout (lane (g,t): R[g][c0], R[g][c1]), committed by the caller.
+  const int g = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
+  double M0 = (g == c0) ? 1.0 : 0.0, M1 = (g == c1) ? 1.0 : 0.0;
+  double P = __shfl_sync(FULL, (g & 1) ? G[1] : G[0], 4 * g + (g >> 1));  // G0[g][g]
+  double T0 = 0.0, T1 = 0.0;  // T[g][c0], T[g][c1], built one column per step
+  double sc0 = 0.0, sc1 = 0.0;
+  bool ok = true;
+  (void)Us; (void)taus; (void)scs;
+  // row i of the R block (alpha = R[i][i], rg = R[i][g], r0/r1 = R[i][c0/c1]) from shared
+  // memory, one step ahead (row i is only rewritten at step i, in registers)
+  auto rrow = [&](int i, double& al, double& rg_, double& r0_, double& r1_) {
+    al = Rs[rix<C>(j0 + i, j0 + i)];
+    rg_ = Rs[rix<C>(j0 + i, j0 + g)];
+    r0_ = Rs[rix<C>(j0 + i, j0 + c0)];
+    r1_ = Rs[rix<C>(j0 + i, j0 + c1)];
+  };
+  double alpha_n, rg_n, r0_n, r1_n;
+  rrow(0, alpha_n, rg_n, r0_n, r1_n);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double alpha = alpha_n, rg = rg_n, r0 = r0_n, r1 = r1_n;
+    if (i < 7) rrow(i + 1, alpha_n, rg_n, r0_n, r1_n);
+    const double e = (i & 1) ? G[1] : G[0];
+    const double d0 = __shfl_sync(FULL, G[0], 4 * i + t);        // G[i][c0]
+    const double d1 = __shfl_sync(FULL, G[1], 4 * i + t);        // G[i][c1]
+    const double dg = __shfl_sync(FULL, e, 4 * g + (i >> 1));    // G[g][i]
+    const double sj = __shfl_sync(FULL, e, 4 * i + (i >> 1));    // G[i][i]
+    const double Pi = __shfl_sync(FULL, P, 4 * i);
+    const double mgi = __shfl_sync(FULL, (i & 1) ? M1 : M0, 4 * g + (i >> 1));  // M[g][i]
+    const double s2 = fma(alpha, alpha, sj);
+#ifdef JQ_KTIME
+    if (ok && !(s2 >= 1e-2 * fma(alpha, alpha, Pi)) && lane == 0) {
+      atomicAdd(&g_gram_fail[i], 1ull);
+      if (g_gram_fail[8] < 8) {
+        const unsigned long long k = atomicAdd(&g_gram_fail[8], 1ull);
+        if (k < 8) printf("gram fail step %d: alpha %.3e sj %.3e Pi %.3e s2 %.3e\n", i, alpha, sj, Pi, s2);
+      }
+    }
+#endif
+    ok = ok && (s2 >= 1e-2 * fma(alpha, alpha, Pi));
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (sj > 0.0) {
+      if (s2 > 1e-280 && s2 < 1e280) {
+        const double rn = rsqrt_nr(s2);
+        const double nrm = s2 * rn;
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = fma(fabs(alpha), rn, 1.0);
+        scale = rcp_nr(alpha - beta);
+      } else {
+        const double nrm = sqrt(s2);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+    }
+    const double twg = tau * fma(scale, dg, rg), tw0 = tau * fma(scale, d0, r0), tw1 = tau * fma(scale, d1, r1);
+    const double ag = g > i ? -twg * scale : 0.0;
+    const double a0 = c0 > i ? -tw0 * scale : 0.0;
+    const double a1 = c1 > i ? -tw1 * scale : 0.0;
+    if (g == i) {  // new row i of R
+      Rb[0] = c0 > i ? r0 - tw0 : (c0 == i ? beta : 0.0);
+      Rb[1] = c1 > i ? r1 - tw1 : (c1 == i ? beta : 0.0);
+    }
+    // T column i: T[g][i] = -tau_i sum_m T[g][m] (y_m . y_i),  y_m . y_i = sc_m sc_i G[m][i]
+    // (entries of T for columns >= i and scales of columns > i are still zero)
+    double tp = fma(T1 * sc1, d1, T0 * sc0 * d0);
+    tp += __shfl_xor_sync(FULL, tp, 1);
+    tp += __shfl_xor_sync(FULL, tp, 2);
+    const double tgi = g < i ? -tau * scale * tp : (g == i ? tau : 0.0);
+    if (c0 == i) { sc0 = scale; T0 = tgi; }
+    if (c1 == i) { sc1 = scale; T1 = tgi; }
+    G[0] = fma(ag * a0, sj, fma(a0, dg, fma(ag, d0, G[0])));
+    G[1] = fma(ag * a1, sj, fma(a1, dg, fma(ag, d1, G[1])));
+    M0 = fma(a0, mgi, M0);
+    M1 = fma(a1, mgi, M1);
+    P = fma(ag * ag, sj, P);
+  }
+  *reinterpret_cast<double2*>(Mg + g * C::LDT + c0) = make_double2(M0 * sc0, M1 * sc1);
+  *reinterpret_cast<double2*>(T + g * C::LDT + c0) = make_double2(T0, T1);
+  return ok;
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -617,7 +736,6 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   double* S = smem_dyn + C::OFF_S;
   double* scratch = smem_dyn + C::OFF_LD;
   double* Mg = smem_dyn + C::OFF_M;
-  double* Rst = smem_dyn + C::OFF_RST;
   volatile double* flag = smem_dyn + C::OFF_FLAG;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
 
@@ -764,13 +882,11 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
           G[0] += gg.x;
           G[1] += gg.y;
         }
-        const bool ok = factor_panel_gram<C>(G, R, j0, T, Mg, Rst, lane) && !(use_tma & 2);
-        __syncwarp();
+        double Rb[2];
+        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, T, Mg, U, taus, scs, lane) && !(use_tma & 2);
         if (ok) {  // commit the panel's R rows
-          for (int k = lane; k < 64; k += 32) {
-            const int r = k >> 3, cc = k & 7;
-            if (cc >= r) R[rix<C>(j0 + r, j0 + cc)] = Rst[k];
-          }
+          if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
+          if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];
         }
         if (lane == 0) flag[0] = ok ? 1.0 : 0.0;
       }
@@ -1145,6 +1261,8 @@ tsqr_wkernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __restri
   }
 }
 
+#include "jq_tsqr_ws.cuh"
+
 // crop NP x NP -> n x n, optional canonical signs
 __global__ void finalize_r_kernel(const double* __restrict__ rnp, int np, int n, bool canonical,
                                   double* __restrict__ out) {
@@ -1257,14 +1375,67 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   return JQ_OK;
 }
 
-// warp-independent leaves (tsqr_wkernel, experimental: JQ_TSQR_IMPL=warp) for NP <= 64;
-// the default is the CTA-wide kernel
-static bool warp_impl() {
-  static const bool w = [] {
+// Leaf kernel for NP <= 64: warp-specialised tsqr_ws_kernel (default), CTA-wide
+// tsqr_kernel (JQ_TSQR_IMPL=cta) or warp-independent tsqr_wkernel (JQ_TSQR_IMPL=warp,
+// experimental); the env switch exists for A/B timing and tests.
+static int leaf_impl() {
+  static const int w = [] {
     const char* e = getenv("JQ_TSQR_IMPL");
-    return e && e[0] == 'w';
+    if (e && e[0] == 'w') return 1;
+    if (e && e[0] == 'c') return 2;
+    return 0;
   }();
   return w;
+}
+static bool warp_impl() { return leaf_impl() == 1; }
+
+template <class CS, class Src>
+static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
+                         bool canonical, double* r_out, int use_tma) {
+  using C = Cfg<CS::NP>;  // tree combine
+  static int occ = [] {
+    int o = 0;
+    cudaFuncSetAttribute(tsqr_ws_kernel<CS, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tsqr_ws_kernel<CS, Src>, CS::THREADS, CS::SMEM) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      o = 1;
+    }
+    if (const char* e = getenv("JQ_TSQR_CTAS_PER_SM")) o = std::min(o, atoi(e));
+    return std::max(1, o);
+  }();
+  static const bool explicit_panels = [] {
+    const char* e = getenv("JQ_TSQR_EXPLICIT");
+    return e && e[0] == '1';
+  }();
+  static const int debug_flags = [] {  // JQ_TSQR_DEBUG=4: loader skips the transform (timing only)
+    const char* e = getenv("JQ_TSQR_DEBUG");
+    return e ? atoi(e) & 4 : 0;
+  }();
+  align = std::max<int64_t>(align, 8);
+  int64_t max_ctas = int64_t(ctx->sms) * occ;
+  int64_t units = std::max<int64_t>(1, cdiv(vrows, align));
+  int64_t ctas = std::min(max_ctas, units);
+  int64_t rows_per_cta = cdiv(units, ctas) * align;
+  ctas = std::max<int64_t>(1, cdiv(vrows, rows_per_cta));
+  double* a = ws_alloc<double>(ctx, size_t(ctas) * C::NP * C::NP);
+  double* b = ws_alloc<double>(ctx, size_t((ctas + 1) / 2) * C::NP * C::NP + 1);
+  if (!a || !b) return fail(JQ_E_OOM, "workspace exhausted (TSQR leaves)");
+  ctx->timing.tsqr_ctas += ctas;
+  ctx->timing.reduced_rows += vrows;
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
+  auto kern = tsqr_ws_kernel<CS, Src>;
+  JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM));
+  kern<<<(int)ctas, CS::THREADS, CS::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a,
+                                                          (use_tma ? 1 : 0) | (explicit_panels ? 2 : 0) | debug_flags);
+  JQ_CHECK_LAUNCH(ctx);
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
+  double* fin = nullptr;
+  JQ_TRY(tree_combine<C>(ctx, a, b, ctas, &fin));
+  finalize_r_kernel<<<(int)cdiv(int64_t(n) * n, 256), 256, 0, ctx->stream>>>(fin, C::NP, n, canonical, r_out);
+  JQ_CHECK_LAUNCH(ctx);
+  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[5], ctx->stream);
+  return JQ_OK;
 }
 
 template <class CW, class Src>
@@ -1314,12 +1485,15 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
                            bool canonical, double* r_out, int use_tma) {
   switch (np_for(n)) {
     case 16:
+      if (leaf_impl() == 0) return run_stream_ws<CfgS<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 32:
+      if (leaf_impl() == 0) return run_stream_ws<CfgS<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 64:
+      if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 128: return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
@@ -1394,6 +1568,24 @@ int canonicalize_dev(jq_ctx* ctx, const double* r, int64_t n, double* out) {
 }  // namespace jq
 
 #ifdef JQ_KTIME
+extern "C" JQ_API int jq_debug_gram_fail(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, jq::g_gram_fail, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(jq::g_gram_fail, z, sizeof(z));
+  }
+  return 0;
+}
+extern "C" JQ_API int jq_debug_ktime_ws(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, jq::g_kt_ws, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(jq::g_kt_ws, z, sizeof(z));
+  }
+  return 0;
+}
 extern "C" JQ_API int jq_debug_ktime(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, jq::g_ktime, sizeof(unsigned long long) * 8);

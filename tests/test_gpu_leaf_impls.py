@@ -1,0 +1,23 @@
+"""The TSQR leaf kernel has three implementations (warp-specialised default, CTA-wide,
+explicit-panel fallback forced) selected by environment variables that the library
+reads once per process; each is checked in a subprocess against the same parity tests."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"JQ_TSQR_IMPL": "cta"}, {"JQ_TSQR_EXPLICIT": "1"},
+                                 {"JQ_TSQR_IMPL": "cta", "JQ_TSQR_EXPLICIT": "1"}],
+                         ids=["cta", "ws-explicit", "cta-explicit"])
+def test_leaf_impl_parity(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "figaro or householder or shard"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
