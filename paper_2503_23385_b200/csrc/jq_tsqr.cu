@@ -1383,6 +1383,7 @@ static int leaf_impl() {
     const char* e = getenv("JQ_TSQR_IMPL");
     if (e && e[0] == 'w') return 1;
     if (e && e[0] == 'c') return 2;
+    if (e && e[0] == '2') return 3;  // warp-specialised, two CTAs of 8 warps per SM
     return 0;
   }();
   return w;
@@ -1486,14 +1487,20 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
   switch (np_for(n)) {
     case 16:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 3)
+        return run_stream_ws<CfgS<16, 8, 6, 2>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 32:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 3)
+        return run_stream_ws<CfgS<32, 8, 6, 2>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 64:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 3)
+        return run_stream_ws<CfgS<64, 8, 6, 2>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 128: return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);

@@ -19,18 +19,21 @@
 // barrier BAR_DATA (data warps) inside the update, mbarriers READY (loader -> data)
 // and FREE (data -> loader) once per chunk, TMA mbarrier inside the loader.
 
-template <int NP_>
+// WARPS_ warps per CTA, DW_ of them data warps (the warps off SM sub-partition 0),
+// MINB_ CTAs per SM.  <NP, 16, 12, 1>: one CTA per SM, 12 data warps (K = 192 rows
+// per chain), two spare SMSP-0 warps; <NP, 8, 6, 2>: two CTAs of 6 data warps.
+template <int NP_, int WARPS_ = 16, int DW_ = 12, int MINB_ = 1>
 struct CfgS {
   static constexpr int NP = NP_;
   static constexpr int NLT = NP / 8;
-  static constexpr int WARPS = 8;
+  static constexpr int WARPS = WARPS_;
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int DW = 6;               // data warps
+  static constexpr int DW = DW_;             // data warps
   static constexpr int KW = 16;              // rows per data warp
   static constexpr int KWT = KW / 8;
   static constexpr int K = DW * KW;          // chunk rows
   static constexpr bool R_SMEM = true;
-  static constexpr int MIN_CTAS = 2;
+  static constexpr int MIN_CTAS = MINB_;
   __host__ __device__ static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
   static constexpr int LDT = 10;
   static constexpr int LDYT = KW + 2;
@@ -52,11 +55,11 @@ struct CfgS {
   static constexpr int OFF_LD = OFF_P + 2 * DW * 8;       // loader per-row scalars [3][K]
   static constexpr int OFF_S = OFF_LD + 3 * K;            // loader running prefix
   static constexpr int OFF_FLAG = OFF_S + NP;             // [2] chain accepted, by parity
-  static constexpr int OFF_ROLE = OFF_FLAG + 2;           // 8 ints: SMSP of each warp
-  static constexpr int OFF_BAR = OFF_ROLE + 4;            // 4 mbarriers: TMA, READY, FREE
+  static constexpr int OFF_ROLE = OFF_FLAG + 2;           // WARPS ints: SMSP of each warp
+  static constexpr int OFF_BAR = OFF_ROLE + WARPS / 2;    // 4 mbarriers: TMA, READY, FREE
   static constexpr int TOTAL = OFF_BAR + 4;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
-  static_assert(SMEM <= 113 * 1024, "two CTAs per SM");
+  static_assert(SMEM <= (MIN_CTAS == 1 ? 227 : 113) * 1024, "shared memory per CTA");
   static_assert(NP <= 64, "loader transform assumes <= 64 columns per side");
 };
 
@@ -120,23 +123,30 @@ tsqr_ws_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __rest
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  int chain_w = -1, loader_w = -1;
+  // chain / loader: the first two warps on SMSP 0; data warps: the DW warps elsewhere
+  // (any other layout falls back to chain 0, loader 1, data 2..DW+1: only slower)
+  int chain_w = -1, loader_w = -1, ndata = 0;
   for (int w = 0; w < C::WARPS; ++w) {
     if (role[w] == 0) {
       if (chain_w < 0) chain_w = w;
       else if (loader_w < 0) loader_w = w;
+    } else {
+      ++ndata;
     }
   }
-  if (chain_w < 0 || loader_w < 0) { chain_w = 0; loader_w = 4; }  // unexpected layout: any split works
+  const bool mapped = chain_w >= 0 && loader_w >= 0 && ndata == C::DW;
+  if (!mapped) { chain_w = 0; loader_w = 1; }
   int d = -1;  // data-warp index
   {
     int k = 0;
     for (int w = 0; w < C::WARPS; ++w) {
-      if (w == chain_w || w == loader_w) continue;
+      const bool data = mapped ? role[w] != 0 : (w >= 2 && w < 2 + C::DW);
+      if (!data) continue;
       if (w == warp) d = k;
       ++k;
     }
   }
+  if (warp != chain_w && warp != loader_w && d < 0) return;  // spare warp
 
   // chunk sequence (identical in every warp): K rows, clipped at the CTA end and at
   // the source's part boundary
