@@ -308,8 +308,11 @@ struct FigaroSrc {
     double* c1 = scratch;
     double* c2 = scratch + C::K;
     double* mode = scratch + 2 * C::K;
+    static_assert(C::K % 32 == 0, "loader rows per lane");
     if (v0 < m1pad) {
-      for (int i = lane; i < C::K; i += 32) {
+#pragma unroll
+      for (int ii = 0; ii < C::K / 32; ++ii) {  // independent rows: all in flight
+        const int i = lane + 32 * ii;
         int g = -1;
         double m2g = 0.0;
         if (i < nrows) {
@@ -326,8 +329,12 @@ struct FigaroSrc {
       return;
     }
     const int64_t b0 = v0 - m1pad;
-    for (int i = lane; i < C::K; i += 32) {
-      double md = 0.0, a1 = 0.0, a2 = 0.0;
+    int* imode = reinterpret_cast<int*>(mode);  // B part: 0 no row / 1 group start / 2 tail row
+#pragma unroll
+    for (int ii = 0; ii < C::K / 32; ++ii) {
+      const int i = lane + 32 * ii;
+      int md = 0;
+      double a1 = 0.0, a2 = 0.0;
       if (i < nrows) {
         const int64_t br = b0 + i;
         int64_t rr = 0;
@@ -343,43 +350,83 @@ struct FigaroSrc {
         }
         if (valid) {
           if (rr == 0) {
-            md = 1.0;
+            md = 1;
           } else {
             const double rd = (double)rr;
-            md = 2.0;
+            md = 2;
             a2 = (m1g * rsqrt_nr(m1g)) * rsqrt_nr(rd * (rd + 1.0));
             a1 = rd * a2;
           }
         }
       }
-      c1[i] = a1; c2[i] = a2; mode[i] = md;
+      c1[i] = a1; c2[i] = a2; imode[i] = md;
     }
     __syncwarp();
+    // lane = columns lane and lane + 32 (n2 <= 64), one pass over the rows in batches of
+    // 4 (vector loads of the row scalars; a select-free path when the 4 rows are all
+    // tail rows, the Cartesian case), the next batch's loads issued first
     const int n2 = (int)fa.n2;
-    for (int c = lane; c < n2; c += 32) {
-      double sv = S[c];
-      for (int ib = 0; ib < nrows; ib += 4) {
-        double xv[4], md[4], a1[4], a2[4], out[4];
+    const int ca = lane, cb = lane + 32;
+    const bool ha = ca < n2, hb = cb < n2;
+    double sa = ha ? S[ca] : 0.0, sb = hb ? S[cb] : 0.0;
+    const int nfull = nrows & ~3;
+    double xa[4], xb[4];
+    double2 q1[2], q2[2];
+    int4 qm;
+    auto load = [&](int ib) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool in = ib + k < nrows;
-          xv[k] = in ? raw[(ib + k) * n2 + c] : 0.0;
-          md[k] = in ? mode[ib + k] : 0.0;
-          a1[k] = in ? c1[ib + k] : 0.0;
-          a2[k] = in ? c2[ib + k] : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          out[k] = 0.0;
-          if (md[k] == 1.0) sv = xv[k];
-          else if (md[k] == 2.0) { out[k] = fma(a1[k], xv[k], -a2[k] * sv); sv += xv[k]; }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (ib + k < nrows) raw[(ib + k) * n2 + c] = out[k];
+      for (int k = 0; k < 4; ++k) {
+        xa[k] = ha ? raw[(ib + k) * n2 + ca] : 0.0;
+        xb[k] = hb ? raw[(ib + k) * n2 + cb] : 0.0;
       }
-      S[c] = sv;
+      q1[0] = *reinterpret_cast<const double2*>(c1 + ib);
+      q1[1] = *reinterpret_cast<const double2*>(c1 + ib + 2);
+      q2[0] = *reinterpret_cast<const double2*>(c2 + ib);
+      q2[1] = *reinterpret_cast<const double2*>(c2 + ib + 2);
+      qm = *reinterpret_cast<const int4*>(imode + ib);
+    };
+    if (nfull > 0) load(0);
+    for (int ib = 0; ib < nfull; ib += 4) {
+      const double ya[4] = {xa[0], xa[1], xa[2], xa[3]}, yb[4] = {xb[0], xb[1], xb[2], xb[3]};
+      const double b1[4] = {q1[0].x, q1[0].y, q1[1].x, q1[1].y}, b2[4] = {q2[0].x, q2[0].y, q2[1].x, q2[1].y};
+      const int mk[4] = {qm.x, qm.y, qm.z, qm.w};
+      if (ib + 4 < nfull) load(ib + 4);
+      double oa[4], ob[4];
+      if ((mk[0] & mk[1] & mk[2] & mk[3]) == 2) {  // all tail rows
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          oa[k] = fma(b1[k], ya[k], -b2[k] * sa);
+          ob[k] = fma(b1[k], yb[k], -b2[k] * sb);
+          sa += ya[k];
+          sb += yb[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          oa[k] = mk[k] == 2 ? fma(b1[k], ya[k], -b2[k] * sa) : 0.0;
+          ob[k] = mk[k] == 2 ? fma(b1[k], yb[k], -b2[k] * sb) : 0.0;
+          sa = mk[k] == 1 ? ya[k] : (mk[k] == 2 ? sa + ya[k] : sa);
+          sb = mk[k] == 1 ? yb[k] : (mk[k] == 2 ? sb + yb[k] : sb);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (ha) raw[(ib + k) * n2 + ca] = oa[k];
+        if (hb) raw[(ib + k) * n2 + cb] = ob[k];
+      }
     }
+    for (int i = nfull; i < nrows; ++i) {  // tail of a partial chunk
+      const double x0 = ha ? raw[i * n2 + ca] : 0.0, x1 = hb ? raw[i * n2 + cb] : 0.0;
+      const int mk = imode[i];
+      const double o0 = mk == 2 ? fma(c1[i], x0, -c2[i] * sa) : 0.0;
+      const double o1 = mk == 2 ? fma(c1[i], x1, -c2[i] * sb) : 0.0;
+      sa = mk == 1 ? x0 : (mk == 2 ? sa + x0 : sa);
+      sb = mk == 1 ? x1 : (mk == 2 ? sb + x1 : sb);
+      if (ha) raw[i * n2 + ca] = o0;
+      if (hb) raw[i * n2 + cb] = o1;
+    }
+    if (ha) S[ca] = sa;
+    if (hb) S[cb] = sb;
     __syncwarp();
   }
 
@@ -417,6 +464,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
     if (ok) return;
     if (spin > (1u << 26)) __trap();
+  }
+}
+// Wait for a long phase (a whole chunk) without spinning: the waiting warp shares its
+// SM sub-partition with the latency-bound chain warp, so it backs off with nanosleep.
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t phase) {
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    __nanosleep(256);
+    if (spin > (1u << 24)) __trap();
   }
 }
 // thread 0: fetch `bytes16` (multiple of 16) bytes, or just complete the phase
@@ -594,6 +658,11 @@ __device__ __forceinline__ void compute_T(double* T, const double* U, const doub
 }
 
 // ------------------------------------------------------------------ Gram panel
+// X[g][g] of an 8 x 8 matrix held in accumulator layout, in every lane of quad g
+__device__ __forceinline__ double diag_of(const double (&X)[2], const int lane) {
+  const int g = lane >> 2;
+  return __shfl_sync(FULL, (g & 1) ? X[1] : X[0], 4 * g + (g >> 1));
+}
 #ifdef JQ_KTIME
 __device__ unsigned long long g_gram_fail[16];
 #endif
@@ -612,12 +681,12 @@ __device__ unsigned long long g_gram_fail[16];
 template <class C>
 __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2], const double* Rs,
                                                   const int j0, double* T, double* Mg, double* Us, double* taus,
-                                                  double* scs, const int lane) {
+                                                  double* scs, const int lane, const double Pg) {
   // Rs/j0: R in shared memory (read only); Rb: on return the panel's new 8 x 8 R block
   // in accumulator layout (lane (g,t): R[g][c0], R[g][c1]), committed by the caller.
   const int g = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
   double M0 = (g == c0) ? 1.0 : 0.0, M1 = (g == c1) ? 1.0 : 0.0;
-  double P = __shfl_sync(FULL, (g & 1) ? G[1] : G[0], 4 * g + (g >> 1));  // G0[g][g]
+  double P = Pg;  // error scale of column g: G0[g][g] (or a larger bound for a derived Gram)
   double T0 = 0.0, T1 = 0.0;  // T[g][c0], T[g][c1], built one column per step
   double sc0 = 0.0, sc1 = 0.0;
   bool ok = true;
@@ -883,7 +952,8 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
           G[1] += gg.y;
         }
         double Rb[2];
-        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, T, Mg, U, taus, scs, lane) && !(use_tma & 2);
+        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, T, Mg, U, taus, scs, lane, diag_of(G, lane)) &&
+                        !(use_tma & 2);
         if (ok) {  // commit the panel's R rows
           if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
           if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];
@@ -1383,22 +1453,22 @@ static int leaf_impl() {
     const char* e = getenv("JQ_TSQR_IMPL");
     if (e && e[0] == 'w') return 1;
     if (e && e[0] == 'c') return 2;
-    if (e && e[0] == '2') return 3;  // warp-specialised, two CTAs of 8 warps per SM
+    if (e && e[0] == 's') return 4;  // warp-specialised v1 (data warps on the lookahead path)
     return 0;
   }();
   return w;
 }
 static bool warp_impl() { return leaf_impl() == 1; }
 
-template <class CS, class Src>
+template <class CS, class Src, bool V2 = true>
 static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
                          bool canonical, double* r_out, int use_tma) {
   using C = Cfg<CS::NP>;  // tree combine
   static int occ = [] {
     int o = 0;
-    cudaFuncSetAttribute(tsqr_ws_kernel<CS, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tsqr_ws_kernel<CS, Src>, CS::THREADS, CS::SMEM) !=
-        cudaSuccess) {
+    auto k = V2 ? tsqr_ws2_kernel<CS, Src> : tsqr_ws_kernel<CS, Src>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, CS::THREADS, CS::SMEM) != cudaSuccess) {
       cudaGetLastError();
       o = 1;
     }
@@ -1425,7 +1495,7 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
   ctx->timing.tsqr_ctas += ctas;
   ctx->timing.reduced_rows += vrows;
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
-  auto kern = tsqr_ws_kernel<CS, Src>;
+  auto kern = V2 ? tsqr_ws2_kernel<CS, Src> : tsqr_ws_kernel<CS, Src>;
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM));
   kern<<<(int)ctas, CS::THREADS, CS::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a,
                                                           (use_tma ? 1 : 0) | (explicit_panels ? 2 : 0) | debug_flags);
@@ -1487,20 +1557,20 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
   switch (np_for(n)) {
     case 16:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      if (leaf_impl() == 3)
-        return run_stream_ws<CfgS<16, 8, 6, 2>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 4)
+        return run_stream_ws<CfgS<16>, Src, false>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 32:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      if (leaf_impl() == 3)
-        return run_stream_ws<CfgS<32, 8, 6, 2>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 4)
+        return run_stream_ws<CfgS<32>, Src, false>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 64:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      if (leaf_impl() == 3)
-        return run_stream_ws<CfgS<64, 8, 6, 2>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 4)
+        return run_stream_ws<CfgS<64>, Src, false>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return warp_impl() ? run_stream_w<CfgW<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
                          : run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 128: return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
@@ -1575,6 +1645,15 @@ int canonicalize_dev(jq_ctx* ctx, const double* r, int64_t n, double* out) {
 }  // namespace jq
 
 #ifdef JQ_KTIME
+extern "C" JQ_API int jq_debug_trace(long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, jq::g_trace, sizeof(long long) * 4096);
+  if (reset) {
+    static long long z[4096];
+    cudaMemcpyToSymbol(jq::g_trace, z, sizeof(z));
+  }
+  return 0;
+}
 extern "C" JQ_API int jq_debug_gram_fail(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, jq::g_gram_fail, sizeof(unsigned long long) * 16);

@@ -21,7 +21,9 @@
 
 // WARPS_ warps per CTA, DW_ of them data warps (the warps off SM sub-partition 0),
 // MINB_ CTAs per SM.  <NP, 16, 12, 1>: one CTA per SM, 12 data warps (K = 192 rows
-// per chain), two spare SMSP-0 warps; <NP, 8, 6, 2>: two CTAs of 6 data warps.
+// per chain), two spare SMSP-0 warps.  (Two CTAs of 8 warps, 6 data warps each, were
+// measured 5% slower: their chains share SMSP 0 and the lookahead DMMAs of one CTA
+// queue behind the other's bulk update.)
 template <int NP_, int WARPS_ = 16, int DW_ = 12, int MINB_ = 1>
 struct CfgS {
   static constexpr int NP = NP_;
@@ -55,8 +57,10 @@ struct CfgS {
   static constexpr int OFF_LD = OFF_P + 2 * DW * 8;       // loader per-row scalars [3][K]
   static constexpr int OFF_S = OFF_LD + 3 * K;            // loader running prefix
   static constexpr int OFF_FLAG = OFF_S + NP;             // [2] chain accepted, by parity
-  static constexpr int OFF_ROLE = OFF_FLAG + 2;           // WARPS ints: SMSP of each warp
-  static constexpr int OFF_BAR = OFF_ROLE + WARPS / 2;    // 4 mbarriers: TMA, READY, FREE
+  static constexpr int OFF_GP = OFF_FLAG + 2;             // [DW][64] C^T C partials of the next tile (ws2)
+  static constexpr int OFF_GD = OFF_GP + DW * 64;         // [DW][64] direct Gram partials (ws2)
+  static constexpr int OFF_ROLE = OFF_GD + DW * 64;       // WARPS ints: SMSP of each warp
+  static constexpr int OFF_BAR = OFF_ROLE + WARPS / 2;    // mbarriers: TMA, READY, FREE, VREADY
   static constexpr int TOTAL = OFF_BAR + 4;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
   static_assert(SMEM <= (MIN_CTAS == 1 ? 227 : 113) * 1024, "shared memory per CTA");
@@ -80,6 +84,15 @@ __device__ unsigned long long g_kt_ws[16];
 #define WS_DECL
 #define WS_MARK(i) do {} while (0)
 #define WS_FLUSH(base) do {} while (0)
+#endif
+
+#ifdef JQ_KTIME
+__device__ long long g_trace[4096];
+// (who, event) timestamps of CTA 0, lane 0, per-warp slots (no atomics on the path)
+#define TR(who, ev) do { if (blockIdx.x == 0 && lane == 0 && tr_k < 600) { \
+                           g_trace[(who) * 1365 + 2 * tr_k] = (ev); g_trace[(who) * 1365 + 2 * tr_k + 1] = clock64(); ++tr_k; } } while (0)
+#else
+#define TR(who, ev) do {} while (0)
 #endif
 
 constexpr int BAR_ALL = 1;   // chain + data warps
@@ -213,7 +226,7 @@ tsqr_ws_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __rest
         WS_MARK(3);
         double Rb[2];
         const bool ok = factor_panel_gram<C>(G, Rb, R, j0, Tc, Mc, smem_dyn + C::OFF_U, smem_dyn + C::OFF_TAU,
-                                             smem_dyn + C::OFF_SC, lane) && !(flags & 2);
+                                             smem_dyn + C::OFF_SC, lane, diag_of(G, lane)) && !(flags & 2);
         WS_MARK(1);
         if (ok) {
           if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
@@ -395,6 +408,394 @@ tsqr_ws_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __rest
   }
 
   // ---- write R (chain + data warps; zeros strictly below the diagonal)
+  double* out = r_out + cta * C::NP * C::NP;
+  for (int idx = (warp == chain_w ? 0 : (d + 1) * 32) + lane; idx < C::NP * C::NP; idx += (C::DW + 1) * 32) {
+    const int r = idx / C::NP, c2 = idx - r * C::NP;
+    out[idx] = c2 >= r ? R[rix<C>(r, c2)] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ ws2: chain-only critical path
+// Same roles as tsqr_ws_kernel, but the chain warp also performs, right after B_p,
+// the update of tile p+1 by panel p (S = sum of the (X^T C)^T partials, Z, W = T^T Z,
+// R rows, V = M' W) and derives the Gram of the updated tile without touching its
+// rows:  (C - X V)^T (C - X V) = C^T C - V^T S - S^T V + V^T (X^T X) V,  from the
+// data warps' C^T C partials (computed one panel ahead), S, V and the panel's own
+// Gram X^T X -- eight 8 x 8 DMMA products on SM sub-partition 0.  The data warps
+// are then off the critical path: they apply V to tile p+1 when the chain signals it
+// (mbarrier VREADY) and finish panel p's other tiles while the chain runs panel p+1.
+// The cancellation guard starts from P = diag(C^T C) + diag(V^T X^T X V) (the scale of
+// the rounding error of the derived Gram).  After an explicit-fallback panel the next
+// Gram is taken directly from the updated rows (barrier D).
+template <class C, class Src>
+__global__ void __launch_bounds__(C::THREADS, C::MIN_CTAS)
+tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __restrict__ r_out, int flags) {
+  extern __shared__ __align__(16) double smem_dyn[];
+  double* R = smem_dyn + C::OFF_R;
+  double* raw = smem_dyn + C::OFF_RAW;
+  double* Zp = smem_dyn + C::OFF_ZP;
+  double* Ws = smem_dyn + C::OFF_WS;
+  double* Gp = smem_dyn + C::OFF_GP;
+  double* Gd = smem_dyn + C::OFF_GD;
+  double* S = smem_dyn + C::OFF_S;
+  double* scratch = smem_dyn + C::OFF_LD;
+  volatile double* flag = smem_dyn + C::OFF_FLAG;
+  int* role = reinterpret_cast<int*>(smem_dyn + C::OFF_ROLE);
+  uint64_t* bar_tma = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
+  uint64_t* bar_ready = bar_tma + 1;
+  uint64_t* bar_free = bar_tma + 2;
+  uint64_t* bar_v = bar_tma + 3;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t cta = blockIdx.x;
+  const int64_t row_begin = cta * rows_per_cta;
+  const int64_t row_end = min(total_rows, row_begin + rows_per_cta);
+  constexpr int NALL = (C::DW + 1) * 32;
+  int tr_k = 0;
+  (void)tr_k;
+
+  if (lane == 0) {
+    unsigned wid;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    role[warp] = (int)(wid & 3);
+  }
+  for (int idx = tid; idx < C::SZ_R; idx += C::THREADS) R[idx] = 0.0;
+  src.template begin<C>(S, row_begin);
+  if (tid == 0) {
+    mbar_init_n(bar_tma, 1);
+    mbar_init_n(bar_ready, 1);
+    mbar_init_n(bar_free, C::DW);
+    mbar_init_n(bar_v, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  int chain_w = -1, loader_w = -1, ndata = 0;
+  for (int w = 0; w < C::WARPS; ++w) {
+    if (role[w] == 0) {
+      if (chain_w < 0) chain_w = w;
+      else if (loader_w < 0) loader_w = w;
+    } else {
+      ++ndata;
+    }
+  }
+  const bool mapped = chain_w >= 0 && loader_w >= 0 && ndata == C::DW;
+  if (!mapped) { chain_w = 0; loader_w = 1; }
+  int d = -1;
+  {
+    int k = 0;
+    for (int w = 0; w < C::WARPS; ++w) {
+      const bool data = mapped ? role[w] != 0 : (w >= 2 && w < 2 + C::DW);
+      if (!data) continue;
+      if (w == warp) d = k;
+      ++k;
+    }
+  }
+  if (warp != chain_w && warp != loader_w && d < 0) return;
+
+  auto chunk_end = [&](int64_t r0) -> int64_t {
+    int64_t e = r0 + C::K < row_end ? r0 + C::K : row_end;
+    const int64_t lim = src.limit(r0);
+    return e < lim ? e : lim;
+  };
+  auto chunk_rows = [&](int64_t r0, int64_t r1) -> int {
+    const int64_t av = src.avail(r0);
+    const int64_t nr = r1 - r0 < av ? r1 - r0 : av;
+    return nr > 0 ? (int)nr : 0;
+  };
+  // sum of the DW partials of an 8 x 8 accumulator-layout matrix (fixed order)
+  auto sum_partials = [&](const double* base, int stride, double (&out)[2]) {
+    out[0] = 0.0;
+    out[1] = 0.0;
+#pragma unroll
+    for (int w = 0; w < C::DW; ++w) {
+      const double2 v = *reinterpret_cast<const double2*>(base + w * stride + 2 * lane);
+      out[0] += v.x;
+      out[1] += v.y;
+    }
+  };
+
+  if (warp == loader_w) {
+    uint32_t ph_tma = 0, ph_free = 0;
+    int64_t nchunk = 0;
+    for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0), ++nchunk) {
+      const int64_t r1 = chunk_end(r0);
+      const int nr = chunk_rows(r0, r1);
+      const int rcol = src.rc(r0);
+      const int nel = nr * rcol;
+      if (nchunk > 0) {
+        mbar_wait_idle(bar_free, ph_free);  // the loader sits next to the chain warp on SMSP 0
+        ph_free ^= 1;
+      }
+      TR(2, 1);
+      if (flags & 1) {
+        if (lane == 0) bulk_fetch(bar_tma, raw, src.ptr(r0), uint32_t(nel) * 8u & ~15u);
+        mbar_wait(bar_tma, ph_tma);
+        ph_tma ^= 1;
+        if ((nel & 1) && lane == 0) raw[nel - 1] = __ldg(src.ptr(r0) + nel - 1);
+      } else {
+        const double* p = src.ptr(r0);
+        for (int e = lane; e < nel; e += 32) raw[e] = __ldg(p + e);
+      }
+      __syncwarp();
+      TR(2, 2);
+      src.template prep_warp<C>(raw, S, scratch, r0, nr, lane);
+      TR(2, 3);
+      if (lane == 0) mbar_arrive(bar_ready);
+    }
+    return;
+  }
+
+  if (warp == chain_w) {
+    // ================= chain warp: the whole critical path
+    for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0)) {
+      named_bar(BAR_ALL, NALL);  // direct Gram partials of tile 0
+      double G[2];
+      sum_partials(Gd, 64, G);
+      double Pg = diag_of(G, lane);
+#pragma unroll 1
+      for (int p = 0; p < C::NLT; ++p) {
+        const int par = p & 1, j0 = 8 * p;
+        double* Tc = smem_dyn + C::OFF_T + par * 8 * C::LDT;
+        double* Mc = smem_dyn + C::OFF_M + par * 8 * C::LDT;
+        const double G0[2] = {G[0], G[1]};  // X^T X of panel p (before the chain)
+        TR(0, 1);
+        double Rb[2];
+        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, Tc, Mc, smem_dyn + C::OFF_U, smem_dyn + C::OFF_TAU,
+                                             smem_dyn + C::OFF_SC, lane, Pg) && !(flags & 2);
+        if (ok) {
+          if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
+          if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];
+        }
+        if (lane == 0) flag[par] = ok ? 1.0 : 0.0;
+        TR(0, 2);
+        named_bar(BAR_ALL, NALL);  // B_p: chain results out, data partials in
+        TR(0, 3);
+        if (!ok) named_bar(BAR_ALL, NALL);  // F_p: explicit panel done by the data warps
+        if (p + 1 < C::NLT) {
+          const int q = p + 1, l0 = 8 * q;
+          double cc[2] = {0.0, 0.0};
+          if (ok) sum_partials(Gp, 64, cc);  // C^T C of tile q (read before VREADY frees Gp)
+          double st[2];
+          sum_partials(Zp + q * 64, C::NLT * 64, st);  // (X^T C_q)^T
+          const int r0i = rix<C>(j0 + 2 * t, l0 + g), r1i = rix<C>(j0 + 2 * t + 1, l0 + g);
+          double zt[2] = {R[r0i], R[r1i]};
+          dmma(zt, st[0], Mc[(2 * t) * C::LDT + g]);
+          dmma(zt, st[1], Mc[(2 * t + 1) * C::LDT + g]);
+          double wv[2] = {0.0, 0.0};
+          dmma(wv, zt[0], Tc[(2 * t) * C::LDT + g]);
+          dmma(wv, zt[1], Tc[(2 * t + 1) * C::LDT + g]);
+          R[r0i] -= wv[0];
+          R[r1i] -= wv[1];
+          double vt[2] = {0.0, 0.0};  // V^T = W^T M'^T
+          dmma(vt, wv[0], Mc[g * C::LDT + 2 * t]);
+          dmma(vt, wv[1], Mc[g * C::LDT + 2 * t + 1]);
+          *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-vt[0], -vt[1]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_v);  // tile q may be updated
+          TR(0, 4);
+          if (ok) {
+            // Gram of the updated tile: C^T C - V^T S - S^T V + (V^T G0) V   (all ^T as stored)
+            double gn[2] = {cc[0], cc[1]};
+            dmma(gn, -vt[0], st[0]);  // - V^T S   : A = V^T (k-perm), B = S^T rows
+            dmma(gn, -vt[1], st[1]);
+            dmma(gn, -st[0], vt[0]);  // - S^T V
+            dmma(gn, -st[1], vt[1]);
+            double e2[2] = {0.0, 0.0};  // V^T G0
+            dmma(e2, vt[0], G0[0]);
+            dmma(e2, vt[1], G0[1]);
+            double e3[2] = {0.0, 0.0};  // (V^T G0) V
+            dmma(e3, e2[0], vt[0]);
+            dmma(e3, e2[1], vt[1]);
+            G[0] = gn[0] + e3[0];
+            G[1] = gn[1] + e3[1];
+            const double dcc = diag_of(cc, lane), de3 = diag_of(e3, lane);
+            Pg = dcc + de3;
+            TR(0, 5);
+          } else {
+            named_bar(BAR_ALL, NALL);  // D_q: direct Gram partials of the updated tile
+            sum_partials(Gd, 64, G);
+            Pg = diag_of(G, lane);
+          }
+        }
+      }
+    }
+    named_bar(BAR_ALL, NALL);  // R final
+  } else {
+    // ================= data warps
+    double* Ytw = smem_dyn + C::OFF_YT + d * C::SZ_YT;
+    double* U = smem_dyn + C::OFF_U;
+    double* taus = smem_dyn + C::OFF_TAU;
+    double* scs = smem_dyn + C::OFF_SC;
+    double* P = smem_dyn + C::OFF_P;
+    double c[C::NLT][C::KWT][2];
+    uint32_t ph_ready = 0, ph_v = 0;
+
+    auto gram_partial = [&](int q, double* dst) {  // (C_q^T C_q) partial of this warp's rows
+#pragma unroll
+      for (int qq = 0; qq < C::NLT; ++qq) {
+        if (qq == q) {
+          double z[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0};
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it) {
+            dmma(z, c[qq][it][0], c[qq][it][0]);
+            dmma(z2, c[qq][it][1], c[qq][it][1]);
+          }
+          *reinterpret_cast<double2*>(dst + d * 64 + 2 * lane) = make_double2(z[0] + z2[0], z[1] + z2[1]);
+        }
+      }
+    };
+
+    for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0)) {
+      const int64_t r1 = chunk_end(r0);
+      const int nr = chunk_rows(r0, r1);
+      const int rcol = src.rc(r0);
+      if (d == 0) TR(1, 7);
+      mbar_wait(bar_ready, ph_ready);
+      ph_ready ^= 1;
+      if (d == 0) TR(1, 8);
+#pragma unroll
+      for (int q = 0; q < C::NLT; ++q) {
+        const int l = q * 8 + g;
+#pragma unroll
+        for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            c[q][it][b] = src.template value<C>(raw, scratch, r0, d * C::KW + 8 * it + 2 * t + b, l, nr, rcol);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_free);
+      gram_partial(0, Gd);
+      named_bar(BAR_ALL, NALL);
+
+#pragma unroll 1
+      for (int p = 0; p < C::NLT; ++p) {
+        const int j0 = 8 * p, par = p & 1;
+        const double* Tp = smem_dyn + C::OFF_T + (par ^ 1) * 8 * C::LDT;
+        const double* Mp = smem_dyn + C::OFF_M + (par ^ 1) * 8 * C::LDT;
+        if (p > 0) {
+          // (1) tile p with panel p-1, V from the chain
+          // B operands of the panel p-1 update (X^T or Y^T rows of this warp), loaded once
+          // for every tile: keeps the data warps' shared-memory traffic (which slows the
+          // chain warp's shuffles) low
+          double yb[C::KWT][2];
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it) {
+            yb[it][0] = Ytw[(2 * t) * C::LDYT + 8 * it + g];
+            yb[it][1] = Ytw[(2 * t + 1) * C::LDYT + 8 * it + g];
+          }
+          mbar_wait(bar_v, ph_v);
+          ph_v ^= 1;
+          if (d == 0) TR(1, 1);
+#pragma unroll
+          for (int q = 0; q < C::NLT; ++q) {
+            if (q == p) {
+              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+#pragma unroll
+              for (int it = 0; it < C::KWT; ++it) {
+                dmma(c[q][it], nw.x, yb[it][0]);
+                dmma(c[q][it], nw.y, yb[it][1]);
+              }
+            }
+          }
+          if (flag[par ^ 1] == 0.0) {  // panel p-1 was explicit: the chain needs the direct Gram
+            gram_partial(p, Gd);
+            named_bar(BAR_ALL, NALL);  // D_p
+          }
+          // (3) tiles q > p with panel p-1
+          for (int q = p + 1 + ((d - (p + 1)) % C::DW + C::DW) % C::DW; q < C::NLT; q += C::DW) {
+            const int l0 = 8 * q;
+            const int r0i = rix<C>(j0 - 8 + 2 * t, l0 + g), r1i = rix<C>(j0 - 8 + 2 * t + 1, l0 + g);
+            double st[2];
+            sum_partials(Zp + q * 64, C::NLT * 64, st);
+            double zt[2] = {R[r0i], R[r1i]};
+            dmma(zt, st[0], Mp[(2 * t) * C::LDT + g]);
+            dmma(zt, st[1], Mp[(2 * t + 1) * C::LDT + g]);
+            double wv[2] = {0.0, 0.0};
+            dmma(wv, zt[0], Tp[(2 * t) * C::LDT + g]);
+            dmma(wv, zt[1], Tp[(2 * t + 1) * C::LDT + g]);
+            R[r0i] -= wv[0];
+            R[r1i] -= wv[1];
+            double vt[2] = {0.0, 0.0};
+            dmma(vt, wv[0], Mp[g * C::LDT + 2 * t]);
+            dmma(vt, wv[1], Mp[g * C::LDT + 2 * t + 1]);
+            *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-vt[0], -vt[1]);
+          }
+          if (d == 0) TR(1, 2);
+          named_bar(BAR_DATA, C::DW * 32);
+          if (d == 0) TR(1, 3);
+#pragma unroll
+          for (int q = 0; q < C::NLT; ++q) {
+            if (q > p) {
+              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+#pragma unroll
+              for (int it = 0; it < C::KWT; ++it) {
+                dmma(c[q][it], nw.x, yb[it][0]);
+                dmma(c[q][it], nw.y, yb[it][1]);
+              }
+            }
+          }
+        }
+        double cp[C::KWT][2];
+#pragma unroll
+        for (int q = 0; q < C::NLT; ++q)
+          if (q == p)
+#pragma unroll
+            for (int it = 0; it < C::KWT; ++it) { cp[it][0] = c[q][it][0]; cp[it][1] = c[q][it][1]; }
+        __syncwarp();
+        if (d == 0) TR(1, 4);
+        // (4) X^T of panel p, partial (X^T C_q)^T of the tiles q > p, C^T C of tile p+1
+#pragma unroll
+        for (int it = 0; it < C::KWT; ++it)
+          *reinterpret_cast<double2*>(Ytw + g * C::LDYT + 8 * it + 2 * t) = make_double2(cp[it][0], cp[it][1]);
+#pragma unroll
+        for (int q = 0; q < C::NLT; ++q) {
+          if (q > p) {
+            double z[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0};
+#pragma unroll
+            for (int it = 0; it < C::KWT; ++it) {
+              dmma(z, c[q][it][0], cp[it][0]);
+              dmma(z2, c[q][it][1], cp[it][1]);
+            }
+            *reinterpret_cast<double2*>(Zp + (d * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0] + z2[0], z[1] + z2[1]);
+          }
+        }
+        if (p + 1 < C::NLT) gram_partial(p + 1, Gp);
+        if (d == 0) TR(1, 5);
+        named_bar(BAR_ALL, NALL);  // B_p
+        if (d == 0) TR(1, 6);
+        if (flag[par] == 0.0) {
+          double* Tc = smem_dyn + C::OFF_T + par * 8 * C::LDT;
+          double* Mc = smem_dyn + C::OFF_M + par * 8 * C::LDT;
+          factor_panel_all<C, C::DW, BAR_DATA>(cp, R, j0, Ytw, Tc, U, taus, scs, P, d, lane);
+          if (d == 0) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int e = 2 * lane + k, r = e >> 3, cc = e & 7;
+              Mc[r * C::LDT + cc] = r == cc ? 1.0 : 0.0;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < C::NLT; ++q) {
+            if (q > p) {
+              double z[2] = {0.0, 0.0};
+#pragma unroll
+              for (int it = 0; it < C::KWT; ++it) {
+                dmma(z, c[q][it][0], cp[it][0]);
+                dmma(z, c[q][it][1], cp[it][1]);
+              }
+              *reinterpret_cast<double2*>(Zp + (d * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0], z[1]);
+            }
+          }
+          named_bar(BAR_DATA, C::DW * 32);
+          named_bar(BAR_ALL, NALL);  // F_p
+        }
+      }
+    }
+    named_bar(BAR_ALL, NALL);  // R final
+  }
+
   double* out = r_out + cta * C::NP * C::NP;
   for (int idx = (warp == chain_w ? 0 : (d + 1) * 32) + lane; idx < C::NP * C::NP; idx += (C::DW + 1) * 32) {
     const int r = idx / C::NP, c2 = idx - r * C::NP;

@@ -38,3 +38,20 @@ ff = N.lib().jq_debug_gram_fail; ff.argtypes = [ctypes.c_void_p, ctypes.c_int]
 fb = (ctypes.c_ulonglong * 16)()
 ff(fb, 1)
 print("gram chain rejections by step:", list(fb[:8]))
+tf = N.lib().jq_debug_trace; tf.argtypes = [ctypes.c_void_p, ctypes.c_int]; tf.restype = ctypes.c_int
+tb = (ctypes.c_longlong * 4096)()
+tf(tb, 1)
+P.figaro_r(P.Table(A), P.Table(B))
+torch.cuda.synchronize()
+tf(tb, 1)
+ev = sorted([(tb[w * 1365 + 2 * k + 1], w, tb[w * 1365 + 2 * k]) for w in (0, 1, 2) for k in range(600)
+             if tb[w * 1365 + 2 * k + 1] != 0])
+evnames = {(0, 1): "chain start", (0, 2): "chain done", (0, 3): "chain B pass", (0, 4): "chain VREADY",
+           (0, 5): "chain Gnext", (1, 1): "d0 V ok", (1, 2): "d0 reduce done", (1, 3): "d0 BAR_DATA pass",
+           (1, 4): "d0 applies done", (1, 5): "d0 step4 done", (1, 6): "d0 B pass", (1, 7): "d0 wait READY",
+           (1, 8): "d0 READY ok", (2, 1): "loader FREE ok", (2, 2): "loader TMA done", (2, 3): "loader prep done"}
+t0 = ev[0][0] if ev else 0
+prev = t0
+for ts, who, e in ev[:160]:
+    print(f"{ts - t0:9d} +{ts - prev:6d}  {evnames.get((who, e), (who, e))}")
+    prev = ts
