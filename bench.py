@@ -43,6 +43,10 @@ CONFIGS = {
     5: dict(m=1_000_000, n=128, keys=None, want_v=True, name="C5 full SVD cartesian 1e6 x 128 |x| 1e6 x 128"),
 }
 METRIC = "join rows/sec (m1*m2/t), time-to-R"
+# dram__bytes_read.sum + dram__bytes_write.sum per leaf-kernel launch (ncu --set full)
+NCU_TRAFFIC = {(4, "footnote"): {"bytes": 51.224204e9 + 14.270464e6,
+                                 "note": "per tsqr_ws2_kernel launch (one side, 1e8 x 64 f64 = 51.2e9 algorithmic "
+                                         "bytes): no re-reads; profiles/r01_ncu_ws2_c4.md"}}
 
 
 def peaks():
@@ -296,9 +300,17 @@ def main():
         stage_avg = {k: float(np.mean([s[k] for s in stage])) for k in ("group_ms", "scan_ms", "tsqr_ms", "tree_ms", "svd_ms", "total_ms")}
         flops, alg = tsqr_flops(args.variant, cfg, m, n, stage[0])
         achieved = flops / (stage_avg["tsqr_ms"] / 1e3) / 1e12
-        roof = {"kernel": "tsqr_kernel (Claim-1 rows generated in the loader + Householder TSQR on DMMA)",
+        # DRAM traffic of one leaf launch from the ncu --set full capture of this config
+        # (profiles/r01_ncu_ws2_c4.md): footnote C4, one side = 1e8 x 64 f64 rows
+        traffic = NCU_TRAFFIC.get((args.config, args.variant))
+        roof = {"kernel": ("tsqr_ws2_kernel (warp-specialised TSQR leaf: loader warp builds the Claim-1 / tail rows, "
+                           "chain warp runs the Gram-panel Householder chain, 12 data warps do the DMMA updates)"
+                           if args.variant == "footnote" and n <= 64 else
+                           "tsqr_kernel (CTA-wide TSQR leaf, Gram-panel chain + explicit fallback, DMMA updates)"),
                 "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "frac": achieved / FP64_PEAK_TFLOPS,
+                "traffic": traffic["bytes"] if traffic else None,
+                "traffic_note": traffic["note"] if traffic else "no ncu capture for this config",
                 "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 figure",
                 "algorithmic": alg, "share_of_step": stage_avg["tsqr_ms"] / ms}
         pk = peaks()

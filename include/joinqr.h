@@ -74,7 +74,9 @@ JQ_API int jq_ctx_destroy(jq_ctx* ctx);
 JQ_API int jq_ctx_set_stream(jq_ctx* ctx, void* cuda_stream);
 JQ_API int jq_ctx_sync(jq_ctx* ctx);
 /* Internal variant switch: 0 = dense Claim-1 reduced matrix (north star),
- * 1 = footnote variant (head/tail of both sides, PAPER.md:59 footnote). */
+ * 1 = footnote variant (head/tail of both sides, PAPER.md:59 footnote),
+ * 2 = auto (default): footnote from (m1 + m2) * (n1 + n2) > 1e8, else dense.
+ * All variants return the same canonical R within the parity tolerance. */
 JQ_API int jq_ctx_set_variant(jq_ctx* ctx, int variant);
 JQ_API int jq_last_timing(jq_ctx* ctx, jq_timing* out);
 /* Number of launches of this library's kernels since context creation. */

@@ -104,14 +104,15 @@ def set_device(device: int) -> None:
         _tls.ctx = None
 
 
-VARIANTS = {"dense": 0, "footnote": 1}
-_variant = VARIANTS[os.environ.get("JOINQR_VARIANT", "dense")]
+VARIANTS = {"dense": 0, "footnote": 1, "auto": 2}
+_variant = VARIANTS[os.environ.get("JOINQR_VARIANT", "auto")]
 
 
 def set_variant(name: str) -> None:
     """figaro_r / figaro_svd internal reduction: "dense" = the Claim-1 reduced matrix
     (north star), "footnote" = head/tail of BOTH sides (PAPER.md:59
-    footnote, 4x fewer TSQR flops at n1 = n2).  Same R (Gram-identical), parity-tested."""
+    footnote, 4x fewer TSQR flops at n1 = n2), "auto" (default) = footnote from
+    (m1 + m2)(n1 + n2) > 1e8 reduced elements.  Same R (Gram-identical), parity-tested."""
     global _variant
     _variant = VARIANTS[name]
     c = getattr(_tls, "ctx", None)

@@ -279,10 +279,17 @@ static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int6
   return rc;
 }
 
+// Variant 2 (auto, the default): the footnote variant from 1e8 reduced elements up
+// (measured crossover: C2 2e6 x 32 is faster dense, C3 2e7 x 64 and C5 2e6 x 256 footnote).
+static bool use_footnote(const jq_ctx* ctx, int64_t rows, int64_t n) {
+  if (ctx->variant == 2) return double(rows) * double(n) > 1e8;
+  return ctx->variant == 1;
+}
+
 // Device-resident figaro_r: R (n x n, canonical) into r_out (device).
 static int figaro_r_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
                         const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
-  if (ctx->variant == 1) return figaro_r_footnote_dev(ctx, a, m1, n1, ka, b, m2, n2, kb, r_out);
+  if (use_footnote(ctx, m1 + m2, n1 + n2)) return figaro_r_footnote_dev(ctx, a, m1, n1, ka, b, m2, n2, kb, r_out);
   const bool keyed = ka != nullptr;
   ctx->timing.tsqr_ctas = 0;
   ctx->timing.reduced_rows = 0;
@@ -340,7 +347,7 @@ static bool use_streamed(const double* a, int64_t m1, int64_t n1, const double* 
 static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const double* b, int64_t m2,
                              int64_t n2, double* dr /* device, n x n canonical */) {
   const int64_t n = n1 + n2;
-  const bool foot = ctx->variant == 1;
+  const bool foot = use_footnote(ctx, m1 + m2, n);
   const int64_t piece_bytes = int64_t(512) << 20;
   auto prows = [&](int64_t cols) {
     int64_t pr = piece_bytes / (8 * std::max<int64_t>(cols, 1));
@@ -534,7 +541,7 @@ int jq_ctx_sync(jq_ctx* ctx) {
 
 int jq_ctx_set_variant(jq_ctx* ctx, int variant) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
-  if (variant != 0 && variant != 1) return fail(JQ_E_INVALID, "variant must be 0 (dense) or 1 (footnote)");
+  if (variant < 0 || variant > 2) return fail(JQ_E_INVALID, "variant must be 0 (dense), 1 (footnote) or 2 (auto)");
   ctx->variant = variant;
   return JQ_OK;
 }
@@ -657,7 +664,7 @@ int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, 
     return fail(JQ_E_INVALID, "bad shard geometry");
   if (m1 <= 0 || m2 <= 0 || b_row0 < 0 || b_row0 + b_rows > m2 || a_row0 < 0 || a_row0 + a_rows > m1)
     return fail(JQ_E_INVALID, "bad global sizes for the shard");
-  const bool foot = ctx->variant == 1;
+  const bool foot = use_footnote(ctx, m1 + m2, n1 + n2);
   if (foot && (!a_prefix || !a_total)) return fail(JQ_E_INVALID, "footnote shards need a_prefix and a_total");
   JQ_TRY(begin_call(ctx));
   const int64_t n = n1 + n2;

@@ -60,7 +60,7 @@ struct jq_ctx {
   jq::Workspace ws;
   int* d_flags = nullptr;    // device error flags
   int* h_flags = nullptr;    // pinned mirror
-  int variant = 0;              // 0 dense Claim-1, 1 footnote (head/tail of both sides)
+  int variant = 2;              // 0 dense Claim-1, 1 footnote (head/tail of both sides), 2 auto
   bool record_tsqr_events = true;
   int64_t launches = 0;
   jq_timing timing{};

@@ -164,7 +164,7 @@ def test_householder_r(P, rows, cols):
 def variant(request, P):
     P.set_variant(request.param)
     yield request.param
-    P.set_variant("dense")
+    P.set_variant("auto")
 
 
 @pytest.mark.parametrize("m1,n1,m2,n2,groups", [
@@ -327,3 +327,18 @@ def test_streamed_host_path_matches_device_path(P, variant):
     finally:
         P.set_variant("dense")
     check_r(r_host, r_dev, 1e-12)
+
+
+@pytest.mark.gpu
+def test_auto_variant_large_join_matches_oracle_gram(P):
+    """Default variant ("auto") above its 1e8-element threshold takes the footnote
+    path; R must still match the factorised Gram of the join."""
+    import oracle as O
+    rng = np.random.default_rng(7)
+    m, n = 450_000, 120
+    a, b = rng.random((m, n // 2)), rng.random((m, n // 2))
+    P.set_variant("auto")
+    r = np.asarray(P.figaro_r(P.Table(a), P.Table(b)))
+    g = O.factorised_gram(O.Table(a), O.Table(b))
+    err = np.linalg.norm(r.T @ r - g) / np.linalg.norm(g)
+    assert err < 1e-10, err
