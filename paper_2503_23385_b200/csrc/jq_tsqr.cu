@@ -53,22 +53,21 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// 1/x and 1/sqrt(x) from the MUFU approximations plus two Newton steps (<= 1 ulp;
-// the CUDA IEEE division/sqrt sequences cost ~180 cycles on the panel's critical path).
+// 1/x and 1/sqrt(x) from the MUFU approximations (~1e-6 relative) plus ONE cubically
+// convergent correction each: r (1 + e + e^2) and y (1 + e/2 + 3e^2/8), measured at
+// <= 2.2e-16 relative (tools/microbench/approx_acc.cu) -- the accuracy of two Newton
+// steps with a shorter dependent chain (3 and 4 fp64 ops) on the panel's critical path.
 __device__ __forceinline__ double rcp_nr(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  return y * fma(-h * y, y, 1.5);
+  const double e = fma(-x * y, y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -722,22 +721,15 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
       }
     }
 #endif
-    ok = ok && (s2 >= 1e-2 * fma(alpha, alpha, Pi));
-    double tau = 0.0, beta = alpha, scale = 0.0;
-    if (sj > 0.0) {
-      if (s2 > 1e-280 && s2 < 1e280) {
-        const double rn = rsqrt_nr(s2);
-        const double nrm = s2 * rn;
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = fma(fabs(alpha), rn, 1.0);
-        scale = rcp_nr(alpha - beta);
-      } else {
-        const double nrm = sqrt(s2);
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-    }
+    // branch-free scalars; |[alpha; x]|^2 outside the safe range of the MUFU
+    // approximations rejects the panel (the explicit path has an IEEE branch)
+    const bool refl = sj > 0.0;
+    ok = ok && (s2 >= 1e-2 * fma(alpha, alpha, Pi)) && (!refl || (s2 > 1e-280 && s2 < 1e280));
+    const double rn = rsqrt_nr(refl ? s2 : 1.0);
+    const double nrm = s2 * rn;
+    const double beta = refl ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
+    const double tau = refl ? fma(fabs(alpha), rn, 1.0) : 0.0;
+    const double scale = refl ? rcp_nr(alpha - beta) : 0.0;
     const double twg = tau * fma(scale, dg, rg), tw0 = tau * fma(scale, d0, r0), tw1 = tau * fma(scale, d1, r1);
     const double ag = g > i ? -twg * scale : 0.0;
     const double a0 = c0 > i ? -tw0 * scale : 0.0;
