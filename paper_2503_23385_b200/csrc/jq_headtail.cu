@@ -36,6 +36,43 @@ __global__ void __launch_bounds__(256) segscan_tile_kernel(
   double s[MAXC];
 #pragma unroll
   for (int k = 0; k < MAXC; ++k) s[k] = 0.0;
+  if (!gid && cols <= 64) {
+    // one segment (Cartesian): plain column sums, 4 rows in flight per lane and
+    // a fixed-order combine (deterministic); the segment starts at global row 0
+    double a[2][4];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[k][u] = 0.0;
+    const bool h0 = lane < cols, h1 = lane + 32 < cols;
+    int64_t r = r0;
+    for (; r + 4 <= r1; r += 4) {
+      double v[2][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* row = x + (r + u) * cols;
+        v[0][u] = h0 ? __ldg(row + lane) : 0.0;
+        v[1][u] = h1 ? __ldg(row + lane + 32) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { a[0][u] += v[0][u]; a[1][u] += v[1][u]; }
+    }
+    for (; r < r1; ++r) {
+      const double* row = x + r * cols;
+      if (h0) a[0][0] += __ldg(row + lane);
+      if (h1) a[1][0] += __ldg(row + lane + 32);
+    }
+    s[0] = (a[0][0] + a[0][1]) + (a[0][2] + a[0][3]);
+    s[1] = (a[1][0] + a[1][1]) + (a[1][2] + a[1][3]);
+    if (r1 == rows) {
+      if (h0) totals[lane] = s[0];
+      if (h1) totals[lane + 32] = s[1];
+    }
+    if (h0) agg[t * cols + lane] = s[0];
+    if (h1) agg[t * cols + lane + 32] = s[1];
+    if (lane == 0) flag[t] = r0 == 0;
+    return;
+  }
   int seg = gid ? gid[r0] : 0;
   int any_start = (r0 == 0) || (gid && gid[r0 - 1] != seg);
   for (int64_t r = r0; r < r1; ++r) {
