@@ -673,10 +673,11 @@ __device__ unsigned long long g_gram_fail[16];
 // so the 8-step chain runs on registers (two Gram entries per lane, accumulator
 // layout) with no row data, no CTA barrier and a latency independent of K.  The
 // columns are tracked as x' = X M; the trailing update uses Y = X M' (M' = M diag(scale))
-// through 8 x 8 products.  Cancellation guard: step i is accepted only if
-//   alpha^2 + G[i][i] >= 1e-2 (alpha^2 + P_i),   P_i = G0[i][i] + sum a_i^2 |x_k'|^2,
-// which bounds the relative rounding error of |[alpha; x_i']|^2 by ~1e-13; otherwise the
-// panel is redone by factor_panel_all (explicit row data).  Run by warp 0 only.
+// through 8 x 8 products.  Cancellation guard (checked once, after the 8 steps): every
+// step i must have  alpha_i^2 + G[i][i] >= 1e-2 (alpha_i^2 + P_i)  with
+// P_i = sum_k M[k][i]^2 G0[k][k] (x_i' = X M[:, i]: the scale of the rounding error of
+// |x_i'|^2), which bounds the relative error of |[alpha; x_i']|^2 by ~1e-13; otherwise
+// the panel is redone by factor_panel_all (explicit row data).
 template <class C>
 __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2], const double* Rs,
                                                   const int j0, double* T, double* Mg, double* Us, double* taus,
@@ -685,7 +686,11 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
   // in accumulator layout (lane (g,t): R[g][c0], R[g][c1]), committed by the caller.
   const int g = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
   double M0 = (g == c0) ? 1.0 : 0.0, M1 = (g == c1) ? 1.0 : 0.0;
-  double P = Pg;  // error scale of column g: G0[g][g] (or a larger bound for a derived Gram)
+  // cancellation guard, evaluated after the 8 steps: per step s2_i = alpha_i^2 + |x_i'|^2
+  // and alpha_i are kept; P_i = sum_k M[k][i]^2 Pg_k bounds the scale of the rounding
+  // error of |x_i'|^2 (x_i' = X M[:, i], Pg_k = G0[k][k] or a larger bound)
+  double s2r[8], alr[8];
+  unsigned reflm = 0;
   double T0 = 0.0, T1 = 0.0;  // T[g][c0], T[g][c1], built one column per step
   double sc0 = 0.0, sc1 = 0.0;
   bool ok = true;
@@ -709,22 +714,14 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
     const double d1 = __shfl_sync(FULL, G[1], 4 * i + t);        // G[i][c1]
     const double dg = __shfl_sync(FULL, e, 4 * g + (i >> 1));    // G[g][i]
     const double sj = __shfl_sync(FULL, e, 4 * i + (i >> 1));    // G[i][i]
-    const double Pi = __shfl_sync(FULL, P, 4 * i);
     const double mgi = __shfl_sync(FULL, (i & 1) ? M1 : M0, 4 * g + (i >> 1));  // M[g][i]
     const double s2 = fma(alpha, alpha, sj);
-#ifdef JQ_KTIME
-    if (ok && !(s2 >= 1e-2 * fma(alpha, alpha, Pi)) && lane == 0) {
-      atomicAdd(&g_gram_fail[i], 1ull);
-      if (g_gram_fail[8] < 8) {
-        const unsigned long long k = atomicAdd(&g_gram_fail[8], 1ull);
-        if (k < 8) printf("gram fail step %d: alpha %.3e sj %.3e Pi %.3e s2 %.3e\n", i, alpha, sj, Pi, s2);
-      }
-    }
-#endif
     // branch-free scalars; |[alpha; x]|^2 outside the safe range of the MUFU
     // approximations rejects the panel (the explicit path has an IEEE branch)
     const bool refl = sj > 0.0;
-    ok = ok && (s2 >= 1e-2 * fma(alpha, alpha, Pi)) && (!refl || (s2 > 1e-280 && s2 < 1e280));
+    s2r[i] = s2;
+    alr[i] = alpha;
+    reflm |= refl ? (1u << i) : 0u;
     const double rn = rsqrt_nr(refl ? s2 : 1.0);
     const double nrm = s2 * rn;
     const double beta = refl ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
@@ -740,9 +737,13 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
     }
     // T column i: T[g][i] = -tau_i sum_m T[g][m] (y_m . y_i),  y_m . y_i = sc_m sc_i G[m][i]
     // (entries of T for columns >= i and scales of columns > i are still zero)
+#if defined(JQ_CHAIN_EXP) && (JQ_CHAIN_EXP & 1)  // timing experiment: no T
+    const double tp = 0.0;
+#else
     double tp = fma(T1 * sc1, d1, T0 * sc0 * d0);
     tp += __shfl_xor_sync(FULL, tp, 1);
     tp += __shfl_xor_sync(FULL, tp, 2);
+#endif
     const double tgi = g < i ? -tau * scale * tp : (g == i ? tau : 0.0);
     if (c0 == i) { sc0 = scale; T0 = tgi; }
     if (c1 == i) { sc1 = scale; T1 = tgi; }
@@ -750,8 +751,27 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
     G[1] = fma(ag * a1, sj, fma(a1, dg, fma(ag, d1, G[1])));
     M0 = fma(a0, mgi, M0);
     M1 = fma(a1, mgi, M1);
-    P = fma(ag * ag, sj, P);
   }
+  // guard: P_c for this lane's columns c0, c1 (sum over the 8 rows g of the quad column)
+  double p0 = M0 * M0 * Pg, p1 = M1 * M1 * Pg;
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    p0 += __shfl_xor_sync(FULL, p0, off);
+    p1 += __shfl_xor_sync(FULL, p1, off);
+  }
+  double s2a = 0.0, ala = 0.0, s2b = 0.0, alb = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (c0 == i) { s2a = s2r[i]; ala = alr[i]; }
+    if (c1 == i) { s2b = s2r[i]; alb = alr[i]; }
+  }
+  const bool ra = (reflm >> c0) & 1u, rb = (reflm >> c1) & 1u;
+  const bool good = (s2a >= 1e-2 * fma(ala, ala, p0)) && (!ra || (s2a > 1e-280 && s2a < 1e280)) &&
+                    (s2b >= 1e-2 * fma(alb, alb, p1)) && (!rb || (s2b > 1e-280 && s2b < 1e280));
+  ok = __all_sync(FULL, good);
+#ifdef JQ_KTIME
+  if (!ok && lane == 0) atomicAdd(&g_gram_fail[0], 1ull);
+#endif
   *reinterpret_cast<double2*>(Mg + g * C::LDT + c0) = make_double2(M0 * sc0, M1 * sc1);
   *reinterpret_cast<double2*>(T + g * C::LDT + c0) = make_double2(T0, T1);
   return ok;

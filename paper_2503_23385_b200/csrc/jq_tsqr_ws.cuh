@@ -675,35 +675,8 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
         const double* Tp = smem_dyn + C::OFF_T + (par ^ 1) * 8 * C::LDT;
         const double* Mp = smem_dyn + C::OFF_M + (par ^ 1) * 8 * C::LDT;
         if (p > 0) {
-          // (1) tile p with panel p-1, V from the chain
-          // B operands of the panel p-1 update (X^T or Y^T rows of this warp), loaded once
-          // for every tile: keeps the data warps' shared-memory traffic (which slows the
-          // chain warp's shuffles) low
-          double yb[C::KWT][2];
-#pragma unroll
-          for (int it = 0; it < C::KWT; ++it) {
-            yb[it][0] = Ytw[(2 * t) * C::LDYT + 8 * it + g];
-            yb[it][1] = Ytw[(2 * t + 1) * C::LDYT + 8 * it + g];
-          }
-          mbar_wait(bar_v, ph_v);
-          ph_v ^= 1;
-          if (d == 0) TR(1, 1);
-#pragma unroll
-          for (int q = 0; q < C::NLT; ++q) {
-            if (q == p) {
-              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
-#pragma unroll
-              for (int it = 0; it < C::KWT; ++it) {
-                dmma(c[q][it], nw.x, yb[it][0]);
-                dmma(c[q][it], nw.y, yb[it][1]);
-              }
-            }
-          }
-          if (flag[par ^ 1] == 0.0) {  // panel p-1 was explicit: the chain needs the direct Gram
-            gram_partial(p, Gd);
-            named_bar(BAR_ALL, NALL);  // D_p
-          }
-          // (3) tiles q > p with panel p-1
+          // (3a) reduces of the tiles q > p with panel p-1 first: their inputs (partials,
+          // T, M') are ready since B_{p-1}, so they overlap the chain warp's update of tile p
           for (int q = p + 1 + ((d - (p + 1)) % C::DW + C::DW) % C::DW; q < C::NLT; q += C::DW) {
             const int l0 = 8 * q;
             const int r0i = rix<C>(j0 - 8 + 2 * t, l0 + g), r1i = rix<C>(j0 - 8 + 2 * t + 1, l0 + g);
@@ -725,6 +698,34 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
           if (d == 0) TR(1, 2);
           named_bar(BAR_DATA, C::DW * 32);
           if (d == 0) TR(1, 3);
+          // B operands of the panel p-1 update (X^T or Y^T rows of this warp), loaded once
+          // for every tile: keeps the data warps' shared-memory traffic low
+          double yb[C::KWT][2];
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it) {
+            yb[it][0] = Ytw[(2 * t) * C::LDYT + 8 * it + g];
+            yb[it][1] = Ytw[(2 * t + 1) * C::LDYT + 8 * it + g];
+          }
+          // (1) tile p with panel p-1, V from the chain
+          mbar_wait(bar_v, ph_v);
+          ph_v ^= 1;
+          if (d == 0) TR(1, 1);
+#pragma unroll
+          for (int q = 0; q < C::NLT; ++q) {
+            if (q == p) {
+              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+#pragma unroll
+              for (int it = 0; it < C::KWT; ++it) {
+                dmma(c[q][it], nw.x, yb[it][0]);
+                dmma(c[q][it], nw.y, yb[it][1]);
+              }
+            }
+          }
+          if (flag[par ^ 1] == 0.0) {  // panel p-1 was explicit: the chain needs the direct Gram
+            gram_partial(p, Gd);
+            named_bar(BAR_ALL, NALL);  // D_p
+          }
+          // (3b) applies of the tiles q > p
 #pragma unroll
           for (int q = 0; q < C::NLT; ++q) {
             if (q > p) {

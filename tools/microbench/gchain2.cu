@@ -13,9 +13,11 @@ __global__ void __launch_bounds__(256, 2) gchain2(long long* cyc, double* sink, 
   asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
   if (lane == 0) role[warp] = wid;
   __syncthreads();
-  int chain_w = -1;
-  for (int w = 0; w < 8; ++w) if ((role[w] & 3) == 0 && chain_w < 0) chain_w = (mode == 0) ? 0 : w;
-  if (warp != chain_w) {
+  int chain_w = -1, chain_w2 = -1;
+  for (int w = 0; w < 8; ++w) if ((role[w] & 3) == 0) { if (chain_w < 0) chain_w = (mode == 0) ? 0 : w; else if (chain_w2 < 0) chain_w2 = w; }
+  if (mode != 3) chain_w2 = -1;
+  const bool second = warp == chain_w2;
+  if (warp != chain_w && !second) {
     const bool dm = mode == 2 ? true : (role[warp] & 3) != 0;  // mode 2: DMMA on every other warp
     if (!dm) return;
     double acc[8][2] = {};
@@ -28,10 +30,11 @@ __global__ void __launch_bounds__(256, 2) gchain2(long long* cyc, double* sink, 
     sink[blockIdx.x * 256 + threadIdx.x] = s2;
     return;
   }
-  double* R = smem_dyn + C::OFF_R;
-  double* T = smem_dyn + C::OFF_T; double* U = smem_dyn + C::OFF_U;
-  double* taus = smem_dyn + C::OFF_TAU; double* scs = smem_dyn + C::OFF_SC;
-  double* Mg = smem_dyn + C::OFF_M;
+  const int off = second ? 6000 : 0;  // private R / T / M' for the second chain (RAW area)
+  double* R = smem_dyn + C::OFF_R + (second ? C::OFF_RAW : 0);
+  double* T = smem_dyn + C::OFF_RAW + 3000 + off / 6; double* U = smem_dyn + C::OFF_RAW + 3200 + off / 6;
+  double* taus = smem_dyn + C::OFF_RAW + 3400 + off / 6; double* scs = smem_dyn + C::OFF_RAW + 3500 + off / 6;
+  double* Mg = smem_dyn + C::OFF_RAW + 3600 + off / 6;
   for (int i = lane; i < C::SZ_R; i += 32) R[i] = 0.0;
   __syncwarp();
   for (int i = lane; i < 8; i += 32) R[rix<C>(i, i)] = 3.0 + i;
@@ -50,7 +53,7 @@ __global__ void __launch_bounds__(256, 2) gchain2(long long* cyc, double* sink, 
   }
   long long t1 = clock64();
   sink[blockIdx.x * 256 + threadIdx.x] = G[0] + okall;
-  if (lane == 0) { cyc[2 * blockIdx.x] = (t1 - t0) / reps; cyc[2 * blockIdx.x + 1] = wid; }
+  if (lane == 0 && !second) { cyc[2 * blockIdx.x] = (t1 - t0) / reps; cyc[2 * blockIdx.x + 1] = wid; }
 }
 }
 int main() {
@@ -59,9 +62,9 @@ int main() {
   const int n = 296;
   cudaMallocManaged(&cyc, 16 * n); cudaMalloc(&sink, 8 * 256 * n);
   cudaFuncSetAttribute(jq::gchain2<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-  const char* names[3] = {"chain=warp 0, DMMA on %warpid%4!=0", "chain by %warpid, DMMA on %warpid%4!=0",
-                          "chain by %warpid, DMMA on all other warps"};
-  for (int mode = 0; mode < 3; ++mode) {
+  const char* names[4] = {"chain=warp 0, DMMA on %warpid%4!=0", "chain by %warpid, DMMA on %warpid%4!=0",
+                          "chain by %warpid, DMMA on all other warps", "TWO chains on SMSP 0, DMMA elsewhere"};
+  for (int mode = 0; mode < 4; ++mode) {
     for (int w = 0; w < 2; ++w) jq::gchain2<C><<<n, 256, (int)C::SMEM>>>(cyc, sink, 100, mode);
     cudaDeviceSynchronize();
     double lo[2] = {0, 0}; int cnt[2] = {0, 0};
