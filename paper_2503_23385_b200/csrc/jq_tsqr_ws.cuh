@@ -439,7 +439,8 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
   double* Gd = smem_dyn + C::OFF_GD;
   double* S = smem_dyn + C::OFF_S;
   double* scratch = smem_dyn + C::OFF_LD;
-  volatile double* flag = smem_dyn + C::OFF_FLAG;
+  volatile int* flag = reinterpret_cast<volatile int*>(smem_dyn + C::OFF_FLAG);  // integer compares: the
+  // data warps' FP64 datapath is busy with DMMA
   int* role = reinterpret_cast<int*>(smem_dyn + C::OFF_ROLE);
   uint64_t* bar_tma = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
   uint64_t* bar_ready = bar_tma + 1;
@@ -568,7 +569,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
           if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
           if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];
         }
-        if (lane == 0) flag[par] = ok ? 1.0 : 0.0;
+        if (lane == 0) flag[par] = ok ? 1 : 0;
         TR(0, 2);
         named_bar(BAR_ALL, NALL);  // B_p: chain results out, data partials in
         TR(0, 3);
@@ -632,17 +633,19 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     double c[C::NLT][C::KWT][2];
     uint32_t ph_ready = 0, ph_v = 0;
 
+    // (single DMMA accumulation chains: a final DADD would queue behind the other warps'
+    // DMMAs in this SM sub-partition's FP64 datapath)
     auto gram_partial = [&](int q, double* dst) {  // (C_q^T C_q) partial of this warp's rows
 #pragma unroll
       for (int qq = 0; qq < C::NLT; ++qq) {
         if (qq == q) {
-          double z[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0};
+          double z[2] = {0.0, 0.0};
 #pragma unroll
           for (int it = 0; it < C::KWT; ++it) {
             dmma(z, c[qq][it][0], c[qq][it][0]);
-            dmma(z2, c[qq][it][1], c[qq][it][1]);
+            dmma(z, c[qq][it][1], c[qq][it][1]);
           }
-          *reinterpret_cast<double2*>(dst + d * 64 + 2 * lane) = make_double2(z[0] + z2[0], z[1] + z2[1]);
+          *reinterpret_cast<double2*>(dst + d * 64 + 2 * lane) = make_double2(z[0], z[1]);
         }
       }
     };
@@ -706,6 +709,18 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
             yb[it][0] = Ytw[(2 * t) * C::LDYT + 8 * it + g];
             yb[it][1] = Ytw[(2 * t + 1) * C::LDYT + 8 * it + g];
           }
+          // (3b) applies of the tiles q > p (independent of the chain's V of tile p)
+#pragma unroll
+          for (int q = 0; q < C::NLT; ++q) {
+            if (q > p) {
+              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+#pragma unroll
+              for (int it = 0; it < C::KWT; ++it) {
+                dmma(c[q][it], nw.x, yb[it][0]);
+                dmma(c[q][it], nw.y, yb[it][1]);
+              }
+            }
+          }
           // (1) tile p with panel p-1, V from the chain
           mbar_wait(bar_v, ph_v);
           ph_v ^= 1;
@@ -721,21 +736,9 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
               }
             }
           }
-          if (flag[par ^ 1] == 0.0) {  // panel p-1 was explicit: the chain needs the direct Gram
+          if (flag[par ^ 1] == 0) {  // panel p-1 was explicit: the chain needs the direct Gram
             gram_partial(p, Gd);
             named_bar(BAR_ALL, NALL);  // D_p
-          }
-          // (3b) applies of the tiles q > p
-#pragma unroll
-          for (int q = 0; q < C::NLT; ++q) {
-            if (q > p) {
-              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
-#pragma unroll
-              for (int it = 0; it < C::KWT; ++it) {
-                dmma(c[q][it], nw.x, yb[it][0]);
-                dmma(c[q][it], nw.y, yb[it][1]);
-              }
-            }
           }
         }
         double cp[C::KWT][2];
@@ -753,20 +756,20 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
 #pragma unroll
         for (int q = 0; q < C::NLT; ++q) {
           if (q > p) {
-            double z[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0};
+            double z[2] = {0.0, 0.0};
 #pragma unroll
             for (int it = 0; it < C::KWT; ++it) {
               dmma(z, c[q][it][0], cp[it][0]);
-              dmma(z2, c[q][it][1], cp[it][1]);
+              dmma(z, c[q][it][1], cp[it][1]);
             }
-            *reinterpret_cast<double2*>(Zp + (d * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0] + z2[0], z[1] + z2[1]);
+            *reinterpret_cast<double2*>(Zp + (d * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0], z[1]);
           }
         }
         if (p + 1 < C::NLT) gram_partial(p + 1, Gp);
         if (d == 0) TR(1, 5);
         named_bar(BAR_ALL, NALL);  // B_p
         if (d == 0) TR(1, 6);
-        if (flag[par] == 0.0) {
+        if (flag[par] == 0) {
           double* Tc = smem_dyn + C::OFF_T + par * 8 * C::LDT;
           double* Mc = smem_dyn + C::OFF_M + par * 8 * C::LDT;
           factor_panel_all<C, C::DW, BAR_DATA>(cp, R, j0, Ytw, Tc, U, taus, scs, P, d, lane);
