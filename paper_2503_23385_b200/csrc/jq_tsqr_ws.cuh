@@ -505,16 +505,21 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     const int64_t nr = r1 - r0 < av ? r1 - r0 : av;
     return nr > 0 ? (int)nr : 0;
   };
-  // sum of the DW partials of an 8 x 8 accumulator-layout matrix (fixed order)
+  // sum of the DW partials of an 8 x 8 accumulator-layout matrix: all loads first, then a
+  // fixed pairwise tree (deterministic, dependent depth log2(DW) instead of DW)
   auto sum_partials = [&](const double* base, int stride, double (&out)[2]) {
-    out[0] = 0.0;
-    out[1] = 0.0;
+    double2 v[C::DW];
 #pragma unroll
-    for (int w = 0; w < C::DW; ++w) {
-      const double2 v = *reinterpret_cast<const double2*>(base + w * stride + 2 * lane);
-      out[0] += v.x;
-      out[1] += v.y;
-    }
+    for (int w = 0; w < C::DW; ++w) v[w] = *reinterpret_cast<const double2*>(base + w * stride + 2 * lane);
+#pragma unroll
+    for (int h = 1; h < C::DW; h <<= 1)
+#pragma unroll
+      for (int w = 0; w + h < C::DW; w += 2 * h) {
+        v[w].x += v[w + h].x;
+        v[w].y += v[w + h].y;
+      }
+    out[0] = v[0].x;
+    out[1] = v[0].y;
   };
 
   if (warp == loader_w) {
