@@ -1063,286 +1063,6 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   }
 }
 
-// ------------------------------------------------------------------ warp-independent TSQR
-// v5 layout for NP <= 64: every WARP is an independent streaming-TSQR leaf with its
-// own packed R in shared memory.  A CTA round loads K = WARPS * KW rows (the
-// TMA + prep loader of tsqr_kernel, CTA barriers only at pass boundaries); warp w
-// then absorbs rows [w*KW, (w+1)*KW) of the round into its R.  The Householder
-// column chain needs only warp shuffles (no CTA barrier per column), and the eight
-// warps' chains and DMMA updates interleave freely on the SM.  Each CTA writes
-// WARPS leaf factors, combined by the same fixed binary tree.
-template <int NP_>
-struct CfgW {
-  static constexpr int NP = NP_;
-  static constexpr int NLT = NP / 8;
-  static constexpr int WARPS = 4;           // small CTAs: two or more per SM overlap one's load phase with another's panels
-  static constexpr int THREADS = WARPS * 32;
-  static constexpr int KW = 32;             // rows per warp per round (registers: NP*KW/32 doubles)
-  static constexpr int KWT = KW / 8;
-  static constexpr int K = WARPS * KW;      // rows per CTA round
-  static constexpr bool R_SMEM = true;
-  static constexpr int MIN_CTAS = NP <= 32 ? 4 : 2;
-  __host__ __device__ static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
-  static constexpr int LDT = 10;
-  static constexpr int LDYT = KW + 2;
-  static constexpr int RAW = NP * 32;
-  static constexpr int SZ_R = rp_off(NLT);  // per warp
-  static constexpr int OFF_R = 0;
-  static constexpr int OFF_YT = OFF_R + WARPS * SZ_R;      // [WARPS][8][LDYT]
-  static constexpr int SZ_YT = 8 * LDYT;
-  static constexpr int OFF_T = OFF_YT + WARPS * SZ_YT;     // [WARPS][8][LDT]
-  static constexpr int OFF_U = OFF_T + WARPS * 8 * LDT;    // [WARPS][64]
-  static constexpr int OFF_TAU = OFF_U + WARPS * 64;       // [WARPS][8]
-  static constexpr int OFF_SC = OFF_TAU + WARPS * 8;       // [WARPS][8]
-  static constexpr int OFF_RAW = OFF_SC + WARPS * 8;
-  static constexpr int OFF_S = OFF_RAW + RAW;
-  static constexpr int OFF_BAR = OFF_S + NP;
-  static constexpr int TOTAL = OFF_BAR + 2;
-  // loader scratch (3 per-row coefficients + 2 per thread) lives only during the
-  // load phase: it aliases the Y^T / T / U area of the panel loop
-  static constexpr int OFF_LD = OFF_YT;
-  static constexpr int SZ_LD = 3 * K + 2 * THREADS;
-  static_assert(SZ_LD <= OFF_RAW - OFF_YT, "loader scratch alias");
-  static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
-  static_assert(SMEM <= 227 * 1024, "shared memory budget");
-};
-
-// Householder factorisation of one 8-column panel by ONE warp over its KW rows
-// stacked under its own R (same dlarfg convention and reflector algebra as
-// factor_panel_all; the column sums need only the quad butterflies).
-template <class C>
-__device__ __forceinline__ void factor_panel_warp(double (&cp)[C::KWT][2], double* R, const int j0, double* Ytw,
-                                                  double* T, double* U, double* taus, double* scs, const int lane) {
-  const int g = lane >> 2, t = lane & 3;
-  double alpha_n = R[rix<C>(j0, j0)], rg_n = R[rix<C>(j0, j0 + g)];
-  double scale_g = 0.0;
-#pragma unroll
-  for (int jj = 0; jj < 8; ++jj) {
-    const double alpha = alpha_n, rgj = rg_n;
-    if (jj < 7) {
-      alpha_n = R[rix<C>(j0 + jj + 1, j0 + jj + 1)];
-      rg_n = R[rix<C>(j0 + jj + 1, j0 + g)];
-    }
-    double xv[C::KWT][2];
-#pragma unroll
-    for (int it = 0; it < C::KWT; ++it) {
-      xv[it][0] = __shfl_sync(FULL, cp[it][0], jj * 4 + t);
-      xv[it][1] = __shfl_sync(FULL, cp[it][1], jj * 4 + t);
-    }
-    double dp0 = 0.0, dp1 = 0.0, sp0 = 0.0, sp1 = 0.0;
-#pragma unroll
-    for (int it = 0; it < C::KWT; ++it) {
-      dp0 = fma(xv[it][0], cp[it][0], dp0);
-      dp1 = fma(xv[it][1], cp[it][1], dp1);
-      sp0 = fma(xv[it][0], xv[it][0], sp0);
-      sp1 = fma(xv[it][1], xv[it][1], sp1);
-    }
-    double d = dp0 + dp1, sj = sp0 + sp1;
-    d += __shfl_xor_sync(FULL, d, 1);
-    sj += __shfl_xor_sync(FULL, sj, 1);
-    d += __shfl_xor_sync(FULL, d, 2);
-    sj += __shfl_xor_sync(FULL, sj, 2);
-    double tau = 0.0, beta = alpha, scale = 0.0;
-    if (sj != 0.0) {  // warp-uniform: every quad holds the same |x|^2
-      const double s2 = fma(alpha, alpha, sj);
-      if (s2 > 1e-280 && s2 < 1e280) {
-        const double rn = rsqrt_nr(s2);
-        const double nrm = s2 * rn;
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = fma(fabs(alpha), rn, 1.0);
-        scale = rcp_nr(alpha - beta);
-      } else {
-        const double nrm = sqrt(alpha * alpha + sj);
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-    }
-    const double tw = tau * fma(scale, d, rgj);
-    const double a = g > jj ? -tw * scale : 0.0;
-#pragma unroll
-    for (int it = 0; it < C::KWT; ++it)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) cp[it][b] = fma(a, xv[it][b], cp[it][b]);
-    if (g == jj) scale_g = scale;
-    if (t == 0) {
-      if (g >= jj) R[rix<C>(j0 + jj, j0 + g)] = g > jj ? rgj - tw : beta;
-      else U[g * 8 + jj] = d;
-      if (g == jj) { taus[jj] = tau; scs[jj] = scale; }
-    }
-  }
-#pragma unroll
-  for (int it = 0; it < C::KWT; ++it) {
-    cp[it][0] *= scale_g;
-    cp[it][1] *= scale_g;
-    *reinterpret_cast<double2*>(Ytw + g * C::LDYT + 8 * it + 2 * t) = make_double2(cp[it][0], cp[it][1]);
-  }
-  __syncwarp();
-  {
-    // T row r = lane & 7 (computed branch-free by every lane, stored by lanes < 8)
-    const int r = lane & 7;
-    double sc[8], tu[8], trow[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) { sc[m] = scs[m]; tu[m] = taus[m]; }
-#pragma unroll
-    for (int m = 0; m < 8; ++m) trow[m] = (m == r) ? tu[m] : 0.0;
-#pragma unroll
-    for (int j = 1; j < 8; ++j) {
-      double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-      for (int m = 0; m < j; ++m) {
-        const double v = trow[m] * ((U[m * 8 + j] * sc[m]) * sc[j]);
-        if (m & 1) acc1 += v; else acc0 += v;
-      }
-      if (j > r) trow[j] = -tu[j] * (acc0 + acc1);
-    }
-    if (lane < 8) {
-#pragma unroll
-      for (int m = 0; m < 8; ++m) T[r * C::LDT + m] = trow[m];
-    }
-  }
-  __syncwarp();
-}
-
-template <class C, class Src>
-__global__ void __launch_bounds__(C::THREADS, C::MIN_CTAS)
-tsqr_wkernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __restrict__ r_out, int use_tma) {
-  extern __shared__ __align__(16) double smem_dyn[];
-  double* raw = smem_dyn + C::OFF_RAW;
-  double* S = smem_dyn + C::OFF_S;
-  double* scratch = smem_dyn + C::OFF_LD;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int64_t cta = blockIdx.x;
-  double* R = smem_dyn + C::OFF_R + warp * C::SZ_R;
-  double* Ytw = smem_dyn + C::OFF_YT + warp * C::SZ_YT;
-  double* T = smem_dyn + C::OFF_T + warp * 8 * C::LDT;
-  double* U = smem_dyn + C::OFF_U + warp * 64;
-  double* taus = smem_dyn + C::OFF_TAU + warp * 8;
-  double* scs = smem_dyn + C::OFF_SC + warp * 8;
-
-  Src s = src;
-  const int64_t row_begin = cta * rows_per_cta;
-  const int64_t row_end = min(total_rows, row_begin + rows_per_cta);
-  for (int idx = lane; idx < C::SZ_R; idx += 32) R[idx] = 0.0;
-  s.template begin<C>(S, row_begin);
-  if (tid == 0) mbar_init(bar);
-  __syncthreads();
-
-  auto pass_nrows = [&](int64_t v0, int rb, int64_t chunk0) -> int {
-    int64_t lim = chunk0 + C::K < row_end ? chunk0 + C::K : row_end;
-    int64_t nr = lim - v0 < (int64_t)rb ? lim - v0 : (int64_t)rb;
-    const int64_t av = s.avail(v0);
-    nr = av < nr ? av : nr;
-    return nr > 0 ? (int)nr : 0;
-  };
-  auto issue = [&](int64_t v0, int64_t chunk0) {
-    const int rcol = s.rc(v0);
-    const int nr = pass_nrows(v0, pass_rows<C>(rcol), chunk0);
-    const uint32_t bytes = uint32_t(nr) * uint32_t(rcol) * 8u;
-    bulk_fetch(bar, raw, s.ptr(v0), bytes & ~15u);
-  };
-  if (use_tma && tid == 0 && row_begin < row_end) issue(row_begin, row_begin);
-
-  double c[C::NLT][C::KWT][2];
-  uint32_t phase = 0;
-  KT_DECL
-
-  for (int64_t row0 = row_begin; row0 < row_end; row0 += C::K) {
-    const int rcol = s.rc(row0);
-    const int rb = pass_rows<C>(rcol);
-    const int npass = (C::K + rb - 1) / rb;
-#pragma unroll
-    for (int q = 0; q < C::NLT; ++q)
-#pragma unroll
-      for (int it = 0; it < C::KWT; ++it) c[q][it][0] = c[q][it][1] = 0.0;
-    __syncthreads();  // every warp left the previous round's panel loop (scratch aliases Y^T/T/U)
-    for (int h = 0; h < npass && row0 + (int64_t)h * rb < row_end; ++h) {
-      const int64_t pv0 = row0 + (int64_t)h * rb;
-      const int nr = pass_nrows(pv0, rb, row0);
-      const int nel = nr * rcol;
-      if (use_tma) {
-        mbar_wait(bar, phase);
-        phase ^= 1;
-        if ((nel & 1) && tid == 0) raw[nel - 1] = __ldg(s.ptr(pv0) + nel - 1);
-      } else {
-        const double* src_rows = s.ptr(pv0);
-        for (int e = tid; e < nel; e += C::THREADS) raw[e] = __ldg(src_rows + e);
-      }
-      __syncthreads();
-      s.template prep<C>(raw, S, scratch, pv0, nr);
-      __syncthreads();
-      // this warp's rows of the pass (skipped when the pass holds none of them)
-      const int lo = warp * C::KW - h * rb;
-      if (lo < rb && lo + C::KW > 0) {
-#pragma unroll
-        for (int q = 0; q < C::NLT; ++q) {
-          const int l = q * 8 + g;
-#pragma unroll
-          for (int it = 0; it < C::KWT; ++it)
-#pragma unroll
-            for (int b = 0; b < 2; ++b) {
-              const int li = lo + 8 * it + 2 * t + b;
-              if (li >= 0 && li < rb) c[q][it][b] = s.template value<C>(raw, scratch, pv0, li, l, nr, rcol);
-            }
-        }
-      }
-      __syncthreads();
-      if (use_tma && tid == 0) {
-        const bool same = h + 1 < npass && pv0 + rb < row_end;
-        const int64_t nv0 = same ? pv0 + rb : row0 + C::K;
-        if (nv0 < row_end) issue(nv0, same ? row0 : nv0);
-      }
-    }
-    KT_MARK(0);
-#pragma unroll 1
-    for (int p = 0; p < C::NLT; ++p) {
-      const int j0 = 8 * p;
-      double cp[C::KWT][2];
-#pragma unroll
-      for (int q = 0; q < C::NLT; ++q)
-        if (q == p)
-#pragma unroll
-          for (int it = 0; it < C::KWT; ++it) { cp[it][0] = c[q][it][0]; cp[it][1] = c[q][it][1]; }
-      factor_panel_warp<C>(cp, R, j0, Ytw, T, U, taus, scs, lane);
-      KT_MARK(1);
-      // trailing tiles q > p:  Z^T = R_rows^T + C^T Y,  W^T = Z^T T,  R_rows -= W,  C -= Y W
-#pragma unroll
-      for (int q = 0; q < C::NLT; ++q) {
-        if (q > p) {
-          const int r0i = rix<C>(j0 + 2 * t, 8 * q + g), r1i = rix<C>(j0 + 2 * t + 1, 8 * q + g);
-          double z[2] = {R[r0i], R[r1i]}, z2[2] = {0.0, 0.0};
-#pragma unroll
-          for (int it = 0; it < C::KWT; ++it) {
-            dmma(z, c[q][it][0], cp[it][0]);
-            dmma(z2, c[q][it][1], cp[it][1]);
-          }
-          double wv[2] = {0.0, 0.0};
-          dmma(wv, z[0] + z2[0], T[(2 * t) * C::LDT + g]);
-          dmma(wv, z[1] + z2[1], T[(2 * t + 1) * C::LDT + g]);
-          R[r0i] -= wv[0];
-          R[r1i] -= wv[1];
-#pragma unroll
-          for (int it = 0; it < C::KWT; ++it) {
-            dmma(c[q][it], -wv[0], Ytw[(2 * t) * C::LDYT + 8 * it + g]);
-            dmma(c[q][it], -wv[1], Ytw[(2 * t + 1) * C::LDYT + 8 * it + g]);
-          }
-        }
-      }
-      __syncwarp();  // R rows / Y^T / T of this panel consumed before the next panel rewrites them
-      KT_MARK(3);
-    }
-    KT_MARK(4);
-  }
-  KT_FLUSH();
-  double* out = r_out + (cta * C::WARPS + warp) * C::NP * C::NP;
-  for (int idx = lane; idx < C::NP * C::NP; idx += 32) {
-    const int r = idx / C::NP, c2 = idx - r * C::NP;
-    out[idx] = c2 >= r ? R[rix<C>(r, c2)] : 0.0;
-  }
-}
-
 #include "jq_tsqr_ws.cuh"
 
 // crop NP x NP -> n x n, optional canonical signs
@@ -1457,28 +1177,23 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   return JQ_OK;
 }
 
-// Leaf kernel for NP <= 64: warp-specialised tsqr_ws_kernel (default), CTA-wide
-// tsqr_kernel (JQ_TSQR_IMPL=cta) or warp-independent tsqr_wkernel (JQ_TSQR_IMPL=warp,
-// experimental); the env switch exists for A/B timing and tests.
+// Leaf kernel for NP <= 64: warp-specialised tsqr_ws2_kernel (default) or the CTA-wide
+// tsqr_kernel (JQ_TSQR_IMPL=cta, for A/B timing and tests); NP >= 128 always CTA-wide.
 static int leaf_impl() {
   static const int w = [] {
     const char* e = getenv("JQ_TSQR_IMPL");
-    if (e && e[0] == 'w') return 1;
-    if (e && e[0] == 'c') return 2;
-    if (e && e[0] == 's') return 4;  // warp-specialised v1 (data warps on the lookahead path)
-    return 0;
+    return (e && e[0] == 'c') ? 2 : 0;
   }();
   return w;
 }
-static bool warp_impl() { return leaf_impl() == 1; }
 
-template <class CS, class Src, bool V2 = true>
+template <class CS, class Src>
 static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
                          bool canonical, double* r_out, int use_tma) {
   using C = Cfg<CS::NP>;  // tree combine
   static int occ = [] {
     int o = 0;
-    auto k = V2 ? tsqr_ws2_kernel<CS, Src> : tsqr_ws_kernel<CS, Src>;
+    auto k = tsqr_ws2_kernel<CS, Src>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, CS::THREADS, CS::SMEM) != cudaSuccess) {
       cudaGetLastError();
@@ -1507,7 +1222,7 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
   ctx->timing.tsqr_ctas += ctas;
   ctx->timing.reduced_rows += vrows;
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
-  auto kern = V2 ? tsqr_ws2_kernel<CS, Src> : tsqr_ws_kernel<CS, Src>;
+  auto kern = tsqr_ws2_kernel<CS, Src>;
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM));
   kern<<<(int)ctas, CS::THREADS, CS::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a,
                                                           (use_tma ? 1 : 0) | (explicit_panels ? 2 : 0) | debug_flags);
@@ -1521,70 +1236,19 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
   return JQ_OK;
 }
 
-template <class CW, class Src>
-static int run_stream_w(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
-                        bool canonical, double* r_out, int use_tma) {
-  using C = Cfg<CW::NP>;  // tree combine
-  align = std::max<int64_t>(align, CW::K);
-  if (align % CW::K) return fail(JQ_E_INVALID, "row alignment must be a multiple of the TSQR round");
-  static int occ = [] {
-    int o = 0;
-    cudaFuncSetAttribute(tsqr_wkernel<CW, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CW::SMEM);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tsqr_wkernel<CW, Src>, CW::THREADS, CW::SMEM) !=
-        cudaSuccess) {
-      cudaGetLastError();
-      o = 1;
-    }
-    if (const char* e = getenv("JQ_TSQR_CTAS_PER_SM")) o = std::min(o, atoi(e));
-    return std::max(1, o);
-  }();
-  int64_t max_ctas = int64_t(ctx->sms) * occ;
-  int64_t units = std::max<int64_t>(1, cdiv(vrows, align));
-  int64_t ctas = std::min(max_ctas, units);
-  int64_t rows_per_cta = cdiv(units, ctas) * align;
-  ctas = std::max<int64_t>(1, cdiv(vrows, rows_per_cta));
-  const int64_t leaves = ctas * CW::WARPS;
-  double* a = ws_alloc<double>(ctx, size_t(leaves) * C::NP * C::NP);
-  double* b = ws_alloc<double>(ctx, size_t((leaves + 1) / 2) * C::NP * C::NP + 1);
-  if (!a || !b) return fail(JQ_E_OOM, "workspace exhausted (TSQR leaves)");
-  ctx->timing.tsqr_ctas += ctas;
-  ctx->timing.reduced_rows += vrows;
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
-  auto kern = tsqr_wkernel<CW, Src>;
-  JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CW::SMEM));
-  kern<<<(int)ctas, CW::THREADS, CW::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a, use_tma);
-  JQ_CHECK_LAUNCH(ctx);
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
-  double* fin = nullptr;
-  JQ_TRY(tree_combine<C>(ctx, a, b, leaves, &fin));
-  finalize_r_kernel<<<(int)cdiv(int64_t(n) * n, 256), 256, 0, ctx->stream>>>(fin, C::NP, n, canonical, r_out);
-  JQ_CHECK_LAUNCH(ctx);
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[5], ctx->stream);
-  return JQ_OK;
-}
-
 template <class Src>
 static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
                            bool canonical, double* r_out, int use_tma) {
   switch (np_for(n)) {
     case 16:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      if (leaf_impl() == 4)
-        return run_stream_ws<CfgS<16>, Src, false>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      return warp_impl() ? run_stream_w<CfgW<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
-                         : run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      return run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 32:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      if (leaf_impl() == 4)
-        return run_stream_ws<CfgS<32>, Src, false>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      return warp_impl() ? run_stream_w<CfgW<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
-                         : run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 64:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      if (leaf_impl() == 4)
-        return run_stream_ws<CfgS<64>, Src, false>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      return warp_impl() ? run_stream_w<CfgW<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma)
-                         : run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 128: return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
   }
@@ -1672,15 +1336,6 @@ extern "C" JQ_API int jq_debug_gram_fail(unsigned long long* out, int reset) {
   if (reset) {
     unsigned long long z[16] = {};
     cudaMemcpyToSymbol(jq::g_gram_fail, z, sizeof(z));
-  }
-  return 0;
-}
-extern "C" JQ_API int jq_debug_ktime_ws(unsigned long long* out, int reset) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, jq::g_kt_ws, sizeof(unsigned long long) * 16);
-  if (reset) {
-    unsigned long long z[16] = {};
-    cudaMemcpyToSymbol(jq::g_kt_ws, z, sizeof(z));
   }
   return 0;
 }

@@ -4,20 +4,22 @@
 // panel takes ~3.5k cycles alone but ~8.6k when other warps issue DMMA on the SAME
 // SM sub-partition (the FP64 datapath is shared per SMSP), and is unaffected by DMMA
 // on the other three.  A co-resident second CTA has its warps rotated by one SMSP
-// (tools/microbench/warpid.cu).  So each CTA reads %warpid and gives its two warps on
-// SMSP 0 the latency-bound roles:
-//   * the CHAIN warp: Gram panel chain (factor_panel_gram), T, M', R rows;
-//   * the LOADER warp: TMA of the next chunk's raw rows + the Claim-1 / tail
+// (tools/microbench/warpid.cu).  So the CTA (16 warps, one per SM) reads %warpid and
+// gives two of its warps on SMSP 0 the latency-bound roles:
+//   * the CHAIN warp: the Gram-panel chain (factor_panel_gram: T, M', R rows), then
+//     the update of the next tile (the lookahead tile) and its Gram, derived from
+//     partials -- the whole critical path;
+//   * the LOADER warp: TMA of the next chunk's raw rows and the Claim-1 / tail
 //     transform in place (prep_warp), one chunk ahead of the data warps;
-// and the six warps on SMSPs 1-3 hold the chunk (DW x KW rows in registers) and do
-// all DMMA work.  Panel p's chain overlaps the data warps finishing panel p-1's
-// trailing update (lookahead: tile p first, then the Gram of panel p, then the other
-// tiles).  The role assignment only moves work between warps: results do not depend
-// on it (row ownership and every reduction order follow the data-warp index).
+// and the twelve warps on SMSPs 1-3 hold the chunk (DW x KW rows in registers) and
+// do all bulk DMMA work: partials, the reduces of the other tiles and the applies.
+// The role assignment only moves work between warps: results do not depend on it
+// (row ownership and every reduction order follow the data-warp index).
 //
-// Synchronisation: named barrier BAR_ALL (chain + data warps) twice per panel, named
-// barrier BAR_DATA (data warps) inside the update, mbarriers READY (loader -> data)
-// and FREE (data -> loader) once per chunk, TMA mbarrier inside the loader.
+// Synchronisation: named barrier BAR_ALL (chain + data warps) once per panel (plus F / D
+// after an explicit-fallback panel), BAR_DATA (data warps) inside the update, mbarriers
+// READY (loader -> data) and FREE (data -> loader) once per chunk, VREADY
+// (chain -> data) once per panel, and the loader's TMA mbarrier.
 
 // WARPS_ warps per CTA, DW_ of them data warps (the warps off SM sub-partition 0),
 // MINB_ CTAs per SM.  <NP, 16, 12, 1>: one CTA per SM, 12 data warps (K = 192 rows
@@ -74,17 +76,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-#ifdef JQ_KTIME
-__device__ unsigned long long g_kt_ws[16];
-#define WS_DECL long long ws_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long ws_t = clock64();
-#define WS_MARK(i) do { long long n_ = clock64(); ws_acc[i] += n_ - ws_t; ws_t = n_; } while (0)
-#define WS_FLUSH(base) do { if (lane == 0) for (int i_ = 0; i_ < 8; ++i_) \
-                              atomicAdd(&g_kt_ws[(base) + i_], (unsigned long long)ws_acc[i_]); } while (0)
-#else
-#define WS_DECL
-#define WS_MARK(i) do {} while (0)
-#define WS_FLUSH(base) do {} while (0)
-#endif
 
 #ifdef JQ_KTIME
 __device__ long long g_trace[4096];
@@ -98,325 +89,8 @@ __device__ long long g_trace[4096];
 constexpr int BAR_ALL = 1;   // chain + data warps
 constexpr int BAR_DATA = 2;  // data warps
 
-template <class C, class Src>
-__global__ void __launch_bounds__(C::THREADS, C::MIN_CTAS)
-tsqr_ws_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __restrict__ r_out, int flags) {
-  extern __shared__ __align__(16) double smem_dyn[];
-  double* R = smem_dyn + C::OFF_R;
-  double* raw = smem_dyn + C::OFF_RAW;
-  double* Zp = smem_dyn + C::OFF_ZP;
-  double* Ws = smem_dyn + C::OFF_WS;
-  double* S = smem_dyn + C::OFF_S;
-  double* scratch = smem_dyn + C::OFF_LD;
-  volatile double* flag = smem_dyn + C::OFF_FLAG;
-  int* role = reinterpret_cast<int*>(smem_dyn + C::OFF_ROLE);
-  uint64_t* bar_tma = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
-  uint64_t* bar_ready = bar_tma + 1;
-  uint64_t* bar_free = bar_tma + 2;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int64_t cta = blockIdx.x;
-  const int64_t row_begin = cta * rows_per_cta;
-  const int64_t row_end = min(total_rows, row_begin + rows_per_cta);
-
-  // ---- roles from the SM sub-partition of each warp
-  if (lane == 0) {
-    unsigned wid;
-    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-    role[warp] = (int)(wid & 3);
-  }
-  for (int idx = tid; idx < C::SZ_R; idx += C::THREADS) R[idx] = 0.0;
-  src.template begin<C>(S, row_begin);
-  if (tid == 0) {
-    mbar_init_n(bar_tma, 1);
-    mbar_init_n(bar_ready, 1);
-    mbar_init_n(bar_free, C::DW);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  // chain / loader: the first two warps on SMSP 0; data warps: the DW warps elsewhere
-  // (any other layout falls back to chain 0, loader 1, data 2..DW+1: only slower)
-  int chain_w = -1, loader_w = -1, ndata = 0;
-  for (int w = 0; w < C::WARPS; ++w) {
-    if (role[w] == 0) {
-      if (chain_w < 0) chain_w = w;
-      else if (loader_w < 0) loader_w = w;
-    } else {
-      ++ndata;
-    }
-  }
-  const bool mapped = chain_w >= 0 && loader_w >= 0 && ndata == C::DW;
-  if (!mapped) { chain_w = 0; loader_w = 1; }
-  int d = -1;  // data-warp index
-  {
-    int k = 0;
-    for (int w = 0; w < C::WARPS; ++w) {
-      const bool data = mapped ? role[w] != 0 : (w >= 2 && w < 2 + C::DW);
-      if (!data) continue;
-      if (w == warp) d = k;
-      ++k;
-    }
-  }
-  if (warp != chain_w && warp != loader_w && d < 0) return;  // spare warp
-
-  // chunk sequence (identical in every warp): K rows, clipped at the CTA end and at
-  // the source's part boundary
-  auto chunk_end = [&](int64_t r0) -> int64_t {
-    int64_t e = r0 + C::K < row_end ? r0 + C::K : row_end;
-    const int64_t lim = src.limit(r0);
-    return e < lim ? e : lim;
-  };
-  auto chunk_rows = [&](int64_t r0, int64_t r1) -> int {  // raw rows present in the source
-    const int64_t av = src.avail(r0);
-    const int64_t nr = r1 - r0 < av ? r1 - r0 : av;
-    return nr > 0 ? (int)nr : 0;
-  };
-
-  if (warp == loader_w) {
-    // ================= loader warp
-    uint32_t ph_tma = 0, ph_free = 0;
-    int64_t nchunk = 0;
-    for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0), ++nchunk) {
-      const int64_t r1 = chunk_end(r0);
-      const int nr = chunk_rows(r0, r1);
-      const int rcol = src.rc(r0);
-      const int nel = nr * rcol;
-      if (nchunk > 0) {  // the data warps have copied the previous chunk out of raw
-        mbar_wait(bar_free, ph_free);
-        ph_free ^= 1;
-      }
-      if (flags & 1) {
-        if (lane == 0) bulk_fetch(bar_tma, raw, src.ptr(r0), uint32_t(nel) * 8u & ~15u);
-        mbar_wait(bar_tma, ph_tma);
-        ph_tma ^= 1;
-        if ((nel & 1) && lane == 0) raw[nel - 1] = __ldg(src.ptr(r0) + nel - 1);
-      } else {
-        const double* p = src.ptr(r0);
-        for (int e = lane; e < nel; e += 32) raw[e] = __ldg(p + e);
-      }
-      __syncwarp();
-      if (!(flags & 4)) src.template prep_warp<C>(raw, S, scratch, r0, nr, lane);  // 4: timing experiment only
-      if (lane == 0) mbar_arrive(bar_ready);
-    }
-    return;
-  }
-
-  if (warp == chain_w) {
-    // ================= chain warp
-    WS_DECL
-    for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0)) {
-#pragma unroll 1
-      for (int p = 0; p < C::NLT; ++p) {
-        const int par = p & 1;
-        WS_MARK(1);
-        named_bar(BAR_ALL, (C::DW + 1) * 32);  // A_p: Gram partials of panel p are in Zp[.][p]
-        WS_MARK(0);
-        double G[2] = {0.0, 0.0};
-#pragma unroll
-        for (int w = 0; w < C::DW; ++w) {
-          const double2 gg = *reinterpret_cast<const double2*>(Zp + (w * C::NLT + p) * 64 + 2 * lane);
-          G[0] += gg.x;
-          G[1] += gg.y;
-        }
-        double* Tc = smem_dyn + C::OFF_T + par * 8 * C::LDT;
-        double* Mc = smem_dyn + C::OFF_M + par * 8 * C::LDT;
-        const int j0 = 8 * p;
-        WS_MARK(3);
-        double Rb[2];
-        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, Tc, Mc, smem_dyn + C::OFF_U, smem_dyn + C::OFF_TAU,
-                                             smem_dyn + C::OFF_SC, lane, diag_of(G, lane)) && !(flags & 2);
-        WS_MARK(1);
-        if (ok) {
-          if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
-          if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];
-        }
-        if (lane == 0) flag[par] = ok ? 1.0 : 0.0;
-        WS_MARK(4);
-        named_bar(BAR_ALL, (C::DW + 1) * 32);  // B_p
-        WS_MARK(2);
-      }
-    }
-    WS_FLUSH(0);
-    named_bar(BAR_ALL, (C::DW + 1) * 32);  // R final
-  } else {
-    // ================= data warps
-    double* Ytw = smem_dyn + C::OFF_YT + d * C::SZ_YT;
-    double* U = smem_dyn + C::OFF_U;
-    double* taus = smem_dyn + C::OFF_TAU;
-    double* scs = smem_dyn + C::OFF_SC;
-    double* P = smem_dyn + C::OFF_P;
-    double c[C::NLT][C::KWT][2];
-    uint32_t ph_ready = 0;
-
-    // tile q of panel pp (rows 8 pp..): Z^T = R^T + S M', W^T = Z^T T, R -= W, Ws = -W^T M'^T
-    auto reduce_tile = [&](int q, int pp, const double* Tq, const double* Mq) {
-      const int jr = 8 * pp, l0 = 8 * q;
-      const int r0i = rix<C>(jr + 2 * t, l0 + g), r1i = rix<C>(jr + 2 * t + 1, l0 + g);
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int w = 0; w < C::DW; ++w) {
-        const double2 zz = *reinterpret_cast<const double2*>(Zp + (w * C::NLT + q) * 64 + 2 * lane);
-        s0 += zz.x;
-        s1 += zz.y;
-      }
-      double zt[2] = {R[r0i], R[r1i]};
-      dmma(zt, s0, Mq[(2 * t) * C::LDT + g]);
-      dmma(zt, s1, Mq[(2 * t + 1) * C::LDT + g]);
-      double wv[2] = {0.0, 0.0};
-      dmma(wv, zt[0], Tq[(2 * t) * C::LDT + g]);
-      dmma(wv, zt[1], Tq[(2 * t + 1) * C::LDT + g]);
-      R[r0i] -= wv[0];
-      R[r1i] -= wv[1];
-      double vv[2] = {0.0, 0.0};
-      dmma(vv, wv[0], Mq[g * C::LDT + 2 * t]);
-      dmma(vv, wv[1], Mq[g * C::LDT + 2 * t + 1]);
-      *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-vv[0], -vv[1]);
-    };
-
-    WS_DECL
-    for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0)) {
-      const int64_t r1 = chunk_end(r0);
-      const int nr = chunk_rows(r0, r1);
-      const int rcol = src.rc(r0);
-      mbar_wait(bar_ready, ph_ready);
-      WS_MARK(7);
-      ph_ready ^= 1;
-#pragma unroll
-      for (int q = 0; q < C::NLT; ++q) {
-        const int l = q * 8 + g;
-#pragma unroll
-        for (int it = 0; it < C::KWT; ++it)
-#pragma unroll
-          for (int b = 0; b < 2; ++b)
-            c[q][it][b] = src.template value<C>(raw, scratch, r0, d * C::KW + 8 * it + 2 * t + b, l, nr, rcol);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_free);
-      WS_MARK(6);
-
-#pragma unroll 1
-      for (int p = 0; p < C::NLT; ++p) {
-        const int j0 = 8 * p, par = p & 1;
-        const double* Tp = smem_dyn + C::OFF_T + (par ^ 1) * 8 * C::LDT;  // panel p-1
-        const double* Mp = smem_dyn + C::OFF_M + (par ^ 1) * 8 * C::LDT;
-        // (1) tile p with panel p-1 (lookahead: the chain of panel p needs it first)
-        if (p > 0) {
-          if (d == p % C::DW) reduce_tile(p, p - 1, Tp, Mp);
-          named_bar(BAR_DATA, C::DW * 32);
-#pragma unroll
-          for (int q = 0; q < C::NLT; ++q) {
-            if (q == p) {
-              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
-#pragma unroll
-              for (int it = 0; it < C::KWT; ++it) {
-                dmma(c[q][it], nw.x, Ytw[(2 * t) * C::LDYT + 8 * it + g]);
-                dmma(c[q][it], nw.y, Ytw[(2 * t + 1) * C::LDYT + 8 * it + g]);
-              }
-            }
-          }
-        }
-        WS_MARK(0);
-        // (2) Gram partial of panel p -> the chain warp
-        double cp[C::KWT][2];
-#pragma unroll
-        for (int q = 0; q < C::NLT; ++q)
-          if (q == p)
-#pragma unroll
-            for (int it = 0; it < C::KWT; ++it) { cp[it][0] = c[q][it][0]; cp[it][1] = c[q][it][1]; }
-        {
-          double z[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0};
-#pragma unroll
-          for (int it = 0; it < C::KWT; ++it) {
-            dmma(z, cp[it][0], cp[it][0]);
-            dmma(z2, cp[it][1], cp[it][1]);
-          }
-          *reinterpret_cast<double2*>(Zp + (d * C::NLT + p) * 64 + 2 * lane) = make_double2(z[0] + z2[0], z[1] + z2[1]);
-        }
-        WS_MARK(1);
-        named_bar(BAR_ALL, (C::DW + 1) * 32);  // A_p
-        WS_MARK(2);
-        // (3) tiles q > p with panel p-1, while the chain runs
-        if (p > 0) {
-          for (int q = p + 1 + ((d - (p + 1)) % C::DW + C::DW) % C::DW; q < C::NLT; q += C::DW)
-            reduce_tile(q, p - 1, Tp, Mp);
-          named_bar(BAR_DATA, C::DW * 32);
-#pragma unroll
-          for (int q = 0; q < C::NLT; ++q) {
-            if (q > p) {
-              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
-#pragma unroll
-              for (int it = 0; it < C::KWT; ++it) {
-                dmma(c[q][it], nw.x, Ytw[(2 * t) * C::LDYT + 8 * it + g]);
-                dmma(c[q][it], nw.y, Ytw[(2 * t + 1) * C::LDYT + 8 * it + g]);
-              }
-            }
-          }
-        }
-        __syncwarp();
-        WS_MARK(3);
-        // (4) X^T of panel p for its own update, partial (X^T C_q)^T of the tiles q > p
-#pragma unroll
-        for (int it = 0; it < C::KWT; ++it)
-          *reinterpret_cast<double2*>(Ytw + g * C::LDYT + 8 * it + 2 * t) = make_double2(cp[it][0], cp[it][1]);
-#pragma unroll
-        for (int q = 0; q < C::NLT; ++q) {
-          if (q > p) {
-            double z[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0};
-#pragma unroll
-            for (int it = 0; it < C::KWT; ++it) {
-              dmma(z, c[q][it][0], cp[it][0]);
-              dmma(z2, c[q][it][1], cp[it][1]);
-            }
-            *reinterpret_cast<double2*>(Zp + (d * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0] + z2[0], z[1] + z2[1]);
-          }
-        }
-        WS_MARK(4);
-        named_bar(BAR_ALL, (C::DW + 1) * 32);  // B_p: T, M', R rows of panel p
-        if (flag[par] == 0.0) {
-          // cancellation in the Gram chain: explicit panel from the row data (rare)
-          double* Tc = smem_dyn + C::OFF_T + par * 8 * C::LDT;
-          double* Mc = smem_dyn + C::OFF_M + par * 8 * C::LDT;
-          factor_panel_all<C, C::DW, BAR_DATA>(cp, R, j0, Ytw, Tc, U, taus, scs, P, d, lane);
-          if (d == 0) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int e = 2 * lane + k, r = e >> 3, cc = e & 7;
-              Mc[r * C::LDT + cc] = r == cc ? 1.0 : 0.0;
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < C::NLT; ++q) {
-            if (q > p) {
-              double z[2] = {0.0, 0.0};
-#pragma unroll
-              for (int it = 0; it < C::KWT; ++it) {
-                dmma(z, c[q][it][0], cp[it][0]);
-                dmma(z, c[q][it][1], cp[it][1]);
-              }
-              *reinterpret_cast<double2*>(Zp + (d * C::NLT + q) * 64 + 2 * lane) = make_double2(z[0], z[1]);
-            }
-          }
-          named_bar(BAR_DATA, C::DW * 32);
-        }
-        WS_MARK(5);
-      }
-    }
-    WS_FLUSH(8);
-    named_bar(BAR_ALL, (C::DW + 1) * 32);  // R final
-  }
-
-  // ---- write R (chain + data warps; zeros strictly below the diagonal)
-  double* out = r_out + cta * C::NP * C::NP;
-  for (int idx = (warp == chain_w ? 0 : (d + 1) * 32) + lane; idx < C::NP * C::NP; idx += (C::DW + 1) * 32) {
-    const int r = idx / C::NP, c2 = idx - r * C::NP;
-    out[idx] = c2 >= r ? R[rix<C>(r, c2)] : 0.0;
-  }
-}
-
-// ------------------------------------------------------------------ ws2: chain-only critical path
-// Same roles as tsqr_ws_kernel, but the chain warp also performs, right after B_p,
+// ------------------------------------------------------------------ the kernel (ws2)
+// The chain warp also performs, right after B_p,
 // the update of tile p+1 by panel p (S = sum of the (X^T C)^T partials, Z, W = T^T Z,
 // R rows, V = M' W) and derives the Gram of the updated tile without touching its
 // rows:  (C - X V)^T (C - X V) = C^T C - V^T S - S^T V + V^T (X^T X) V,  from the

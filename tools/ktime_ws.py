@@ -1,4 +1,4 @@
-"""Per-role phase breakdown of tsqr_ws_kernel (lib/libjoinqr_ktime.so: make -C csrc ktime).
+"""Timeline of tsqr_ws2_kernel (CTA 0: chain warp, data warp 0, loader) and Gram-panel rejections (lib/libjoinqr_ktime.so: make -C csrc ktime).
 
 JOINQR_LIB=.../libjoinqr_ktime.so python tools/ktime_ws.py --m 2000000 --n 64 [--variant footnote]
 """
@@ -18,26 +18,12 @@ A = torch.empty((a.m, a.n), dtype=torch.float64, device="cuda")
 B = torch.empty((a.m, a.n), dtype=torch.float64, device="cuda")
 datagen.uniform(1, a.m, a.n, out=A); datagen.uniform(2, a.m, a.n, out=B)
 P.figaro_r(P.Table(A), P.Table(B))
-fn = N.lib().jq_debug_ktime_ws; fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = (ctypes.c_ulonglong * 16)()
-fn(buf, 1)
-P.figaro_r(P.Table(A), P.Table(B))
-torch.cuda.synchronize()
-fn(buf, 1)
 t = N.last_timing()
 print(f"variant={a.variant} tsqr_ms={t['tsqr_ms']:.2f} ctas={t['tsqr_ctas']}")
-names = ["chain: wait A", "chain: 8 steps", "chain: wait B", "chain: G sum", "chain: commit/flag", "", "", "",
-         "data: step1 reduce/apply tile p", "data: step2 Gram", "data: wait A", "data: step3 update q>p",
-         "data: step4 Xt+Zp", "data: wait B (+fallback)", "data: fill", "data: wait READY"]
-for base in (0, 8):
-    tot = sum(buf[base + i] for i in range(8)) or 1
-    for i in range(8):
-        if names[base + i]:
-            print(f"  {names[base + i]:34s} {buf[base + i] / tot:6.1%} {buf[base + i] / 1e6:10.1f} Mcyc")
 ff = N.lib().jq_debug_gram_fail; ff.argtypes = [ctypes.c_void_p, ctypes.c_int]
 fb = (ctypes.c_ulonglong * 16)()
 ff(fb, 1)
-print("gram chain rejections by step:", list(fb[:8]))
+print("Gram panels rejected (explicit fallback):", fb[0])
 tf = N.lib().jq_debug_trace; tf.argtypes = [ctypes.c_void_p, ctypes.c_int]; tf.restype = ctypes.c_int
 tb = (ctypes.c_longlong * 4096)()
 tf(tb, 1)
