@@ -201,10 +201,13 @@ def main():
                          "reported under 'variants')")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="(testing) run the multi-GPU code path even with one rank (torchrun, 1 process)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    sharded_path = world > 1 or args.force_sharded
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = CONFIGS[args.config]
@@ -235,7 +238,7 @@ def main():
     torch.cuda.set_device(local)
     N.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:
+    if sharded_path:
         dist.init_process_group("nccl", device_id=device)
 
     A, B, ka, kb, a0 = make_inputs(args.config, rank, world, device)
@@ -250,7 +253,7 @@ def main():
 
     def step():
         N.use_torch_stream(A)
-        if world == 1:
+        if not sharded_path:
             if cfg.get("want_v"):
                 return P.figaro_svd(P.Table(A, ka), P.Table(B, kb), want_vectors=True).values
             return P.figaro_r(P.Table(A, ka), P.Table(B, kb))
@@ -359,7 +362,7 @@ def main():
                 "variants": {args.variant: {"ms_per_step": ms, "value": value},
                              other: ({"ms_per_step": ms_o, "value": jrows / (ms_o / 1e3)} if ms_o else None)}}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded_path:
         dist.destroy_process_group()
 
 
