@@ -75,6 +75,52 @@ __global__ void __launch_bounds__(256) segscan_tile_kernel(
   }
   int seg = gid ? gid[r0] : 0;
   int any_start = (r0 == 0) || (gid && gid[r0 - 1] != seg);
+  if (gid && cols <= 64) {
+    // keyed, <= 64 columns: the loads of 4 rows are issued before their sequential
+    // segment logic (same additions in the same order as the generic loop below)
+    const bool h0 = lane < cols, h1 = lane + 32 < cols;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t r = r0;
+    auto row_step = [&](int64_t rr, int sr, double v0, double v1) {
+      const bool start = (rr == 0) || (rr > r0 && sr != seg);
+      if (start && rr > r0) {
+        if (seg >= 0) {
+          if (h0) totals[(int64_t)seg * cols + lane] = s0;
+          if (h1) totals[(int64_t)seg * cols + lane + 32] = s1;
+        }
+        any_start = 1;
+      }
+      seg = sr;
+      s0 = start ? v0 : s0 + v0;
+      s1 = start ? v1 : s1 + v1;
+    };
+    for (; r + 4 <= r1; r += 4) {
+      int g4[4];
+      double v[2][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        g4[u] = gid[r + u];
+        const double* row = x + (r + u) * cols;
+        v[0][u] = h0 ? __ldg(row + lane) : 0.0;
+        v[1][u] = h1 ? __ldg(row + lane + 32) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) row_step(r + u, g4[u], v[0][u], v[1][u]);
+    }
+    for (; r < r1; ++r) {
+      const double* row = x + r * cols;
+      row_step(r, gid[r], h0 ? __ldg(row + lane) : 0.0, h1 ? __ldg(row + lane + 32) : 0.0);
+    }
+    const bool ends_here = (r1 == rows) || (gid[r1] != seg);
+    if (ends_here && seg >= 0) {
+      if (h0) totals[(int64_t)seg * cols + lane] = s0;
+      if (h1) totals[(int64_t)seg * cols + lane + 32] = s1;
+    }
+    if (h0) agg[t * cols + lane] = s0;
+    if (h1) agg[t * cols + lane + 32] = s1;
+    if (lane == 0) flag[t] = any_start;
+    return;
+  }
   for (int64_t r = r0; r < r1; ++r) {
     const int sr = gid ? gid[r] : 0;
     const bool start = (r == 0) || (r > r0 && sr != seg);
