@@ -817,7 +817,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   double* S = smem_dyn + C::OFF_S;
   double* scratch = smem_dyn + C::OFF_LD;
   double* Mg = smem_dyn + C::OFF_M;
-  volatile double* flag = smem_dyn + C::OFF_FLAG;
+  volatile int* flag = reinterpret_cast<volatile int*>(smem_dyn + C::OFF_FLAG);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_dyn + C::OFF_BAR);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -970,10 +970,10 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
           if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
           if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];
         }
-        if (lane == 0) flag[0] = ok ? 1.0 : 0.0;
+        if (lane == 0) flag[0] = ok ? 1 : 0;
       }
       __syncthreads();
-      if (flag[0] == 0.0) {
+      if (flag[0] == 0) {
         // cancellation: explicit factorisation from the row data (rare; CTA-uniform)
         factor_panel_all<C>(cp, R, j0, Ytw, T, U, taus, scs, P, warp, lane);  // cp <- Y, Ytw <- Y^T
         if (warp == 0) {
