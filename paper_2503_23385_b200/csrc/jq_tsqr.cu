@@ -307,11 +307,11 @@ struct FigaroSrc {
     double* c1 = scratch;
     double* c2 = scratch + C::K;
     double* mode = scratch + 2 * C::K;
-    static_assert(C::K % 32 == 0, "loader rows per lane");
     if (v0 < m1pad) {
 #pragma unroll
-      for (int ii = 0; ii < C::K / 32; ++ii) {  // independent rows: all in flight
+      for (int ii = 0; ii < (C::K + 31) / 32; ++ii) {  // independent rows: all in flight
         const int i = lane + 32 * ii;
+        if (i >= C::K) break;
         int g = -1;
         double m2g = 0.0;
         if (i < nrows) {
@@ -330,8 +330,9 @@ struct FigaroSrc {
     const int64_t b0 = v0 - m1pad;
     int* imode = reinterpret_cast<int*>(mode);  // B part: 0 no row / 1 group start / 2 tail row
 #pragma unroll
-    for (int ii = 0; ii < C::K / 32; ++ii) {
+    for (int ii = 0; ii < (C::K + 31) / 32; ++ii) {
       const int i = lane + 32 * ii;
+      if (i >= C::K) break;
       int md = 0;
       double a1 = 0.0, a2 = 0.0;
       if (i < nrows) {

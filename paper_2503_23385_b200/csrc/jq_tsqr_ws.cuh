@@ -26,14 +26,14 @@
 // per chain), two spare SMSP-0 warps.  (Two CTAs of 8 warps, 6 data warps each, were
 // measured 5% slower: their chains share SMSP 0 and the lookahead DMMAs of one CTA
 // queue behind the other's bulk update.)
-template <int NP_, int WARPS_ = 16, int DW_ = 12, int MINB_ = 1>
+template <int NP_, int WARPS_ = 16, int DW_ = 12, int MINB_ = 1, int KW_ = 16>
 struct CfgS {
   static constexpr int NP = NP_;
   static constexpr int NLT = NP / 8;
   static constexpr int WARPS = WARPS_;
   static constexpr int THREADS = WARPS * 32;
   static constexpr int DW = DW_;             // data warps
-  static constexpr int KW = 16;              // rows per data warp
+  static constexpr int KW = KW_;             // rows per data warp
   static constexpr int KWT = KW / 8;
   static constexpr int K = DW * KW;          // chunk rows
   static constexpr bool R_SMEM = true;
