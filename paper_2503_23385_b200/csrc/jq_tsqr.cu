@@ -108,8 +108,7 @@ struct Cfg {
   static constexpr int OFF_LD = OFF_S + NP;   // loader scratch: 3 per-row coefficients + 2 per thread
   static constexpr int SZ_LD = 3 * K + 2 * THREADS;
   static constexpr int OFF_M = OFF_LD + SZ_LD;    // M' (8 x LDT): Y = X M' of the Gram panel
-  static constexpr int OFF_RST = OFF_M + 8 * LDT; // staged R rows of the Gram panel (8 x 8)
-  static constexpr int OFF_FLAG = OFF_RST + 64;   // Gram panel accepted (1) / explicit fallback (0)
+  static constexpr int OFF_FLAG = OFF_M + 8 * LDT; // Gram panel accepted (1) / explicit fallback (0)
   static constexpr int OFF_BAR = OFF_FLAG + 2;    // mbarrier (8 bytes)
   static constexpr int TOTAL = OFF_BAR + 2;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
@@ -681,8 +680,8 @@ __device__ unsigned long long g_gram_fail[16];
 // the panel is redone by factor_panel_all (explicit row data).
 template <class C>
 __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2], const double* Rs,
-                                                  const int j0, double* T, double* Mg, double* Us, double* taus,
-                                                  double* scs, const int lane, const double Pg) {
+                                                  const int j0, double* T, double* Mg, const int lane,
+                                                  const double Pg) {
   // Rs/j0: R in shared memory (read only); Rb: on return the panel's new 8 x 8 R block
   // in accumulator layout (lane (g,t): R[g][c0], R[g][c1]), committed by the caller.
   const int g = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
@@ -695,7 +694,6 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
   double T0 = 0.0, T1 = 0.0;  // T[g][c0], T[g][c1], built one column per step
   double sc0 = 0.0, sc1 = 0.0;
   bool ok = true;
-  (void)Us; (void)taus; (void)scs;
   // row i of the R block (alpha = R[i][i], rg = R[i][g], r0/r1 = R[i][c0/c1]) from shared
   // memory, one step ahead (row i is only rewritten at step i, in registers)
   auto rrow = [&](int i, double& al, double& rg_, double& r0_, double& r1_) {
@@ -738,13 +736,9 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
     }
     // T column i: T[g][i] = -tau_i sum_m T[g][m] (y_m . y_i),  y_m . y_i = sc_m sc_i G[m][i]
     // (entries of T for columns >= i and scales of columns > i are still zero)
-#if defined(JQ_CHAIN_EXP) && (JQ_CHAIN_EXP & 1)  // timing experiment: no T
-    const double tp = 0.0;
-#else
     double tp = fma(T1 * sc1, d1, T0 * sc0 * d0);
     tp += __shfl_xor_sync(FULL, tp, 1);
     tp += __shfl_xor_sync(FULL, tp, 2);
-#endif
     const double tgi = g < i ? -tau * scale * tp : (g == i ? tau : 0.0);
     if (c0 == i) { sc0 = scale; T0 = tgi; }
     if (c1 == i) { sc1 = scale; T1 = tgi; }
@@ -965,8 +959,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
           G[1] += gg.y;
         }
         double Rb[2];
-        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, T, Mg, U, taus, scs, lane, diag_of(G, lane)) &&
-                        !(use_tma & 2);
+        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, T, Mg, lane, diag_of(G, lane)) && !(use_tma & 2);
         if (ok) {  // commit the panel's R rows
           if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
           if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];

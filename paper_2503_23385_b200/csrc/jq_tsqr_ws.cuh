@@ -51,8 +51,7 @@ struct CfgS {
   static constexpr int OFF_WS = OFF_ZP + DW * NLT * 64;   // [NLT][64]      -V^T per tile
   static constexpr int OFF_T = OFF_WS + NLT * 64;         // [2][8 x LDT]   T by panel parity
   static constexpr int OFF_M = OFF_T + 16 * LDT;          // [2][8 x LDT]   M' by panel parity
-  static constexpr int OFF_RST = OFF_M + 16 * LDT;        // staged R rows of the chain
-  static constexpr int OFF_U = OFF_RST + 64;              // explicit fallback: U, taus, scales, partials
+  static constexpr int OFF_U = OFF_M + 16 * LDT;          // explicit fallback: U, taus, scales, partials
   static constexpr int OFF_TAU = OFF_U + 64;
   static constexpr int OFF_SC = OFF_TAU + 8;
   static constexpr int OFF_P = OFF_SC + 8;                // [2][DW][8]
@@ -242,8 +241,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
         const double G0[2] = {G[0], G[1]};  // X^T X of panel p (before the chain)
         TR(0, 1);
         double Rb[2];
-        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, Tc, Mc, smem_dyn + C::OFF_U, smem_dyn + C::OFF_TAU,
-                                             smem_dyn + C::OFF_SC, lane, Pg) && !(flags & 2);
+        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, Tc, Mc, lane, Pg) && !(flags & 2);
         if (ok) {
           if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
           if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];

@@ -10,8 +10,8 @@ __global__ void __launch_bounds__(256, 1) gchain(long long* cyc, double* sink, i
   const int off2 = threadIdx.x >= 32 ? 4096 : 0;
   double* T = smem_dyn + C::OFF_T + off2; double* U = smem_dyn + C::OFF_U + off2;
   double* taus = smem_dyn + C::OFF_TAU; double* scs = smem_dyn + C::OFF_SC;
-  double* Mg = smem_dyn + C::OFF_M + off2; double* Rst = smem_dyn + C::OFF_RST + off2;
-  (void)U; (void)Rst;
+  double* Mg = smem_dyn + C::OFF_M + off2;
+  (void)U; (void)taus; (void)scs;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const bool second_chain = busy == 6 && (threadIdx.x >> 5) == 4;
   if (threadIdx.x >= 32 && !second_chain) {  // other warps: DMMA (busy=1) or DFMA (busy=2) streams on the same SM
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256, 1) gchain(long long* cyc, double* sink, i
   for (int r = 0; r < reps; ++r) {
     double Gc[2] = {G[0], G[1]};
     double Rb[2] = {R[rix<C>(g, 2 * t)], R[rix<C>(g, 2 * t + 1)]};
-    okall &= factor_panel_gram<C>(Gc, Rb, T, Mg, lane);
+    okall &= factor_panel_gram<C>(Gc, Rb, R, 0, T, Mg, lane, jq::diag_of(Gc, lane));
     __syncwarp();
     __syncwarp();
     G[0] += 1e-9 * T[(lane & 7) * C::LDT];

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256, 2) gchain2(long long* cyc, double* sink, 
   for (int r = 0; r < reps; ++r) {
     double Gc[2] = {G[0], G[1]};
     double Rb[2];
-    okall &= factor_panel_gram<C>(Gc, Rb, R, 0, T, Mg, U, taus, scs, lane, jq::diag_of(Gc, lane));
+    okall &= factor_panel_gram<C>(Gc, Rb, R, 0, T, Mg, lane, jq::diag_of(Gc, lane));
     __syncwarp();
     G[0] += 1e-9 * T[(lane & 7) * C::LDT] + 1e-12 * Rb[0];
   }
