@@ -276,63 +276,123 @@ int segscan_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const 
 // Tail rows of every segment: row r of x with in-group index rr >= 1 goes to output
 // row base(g) + rr - 1, columns [col0, col0 + cols), scaled by sqrt(count(g)); columns
 // [0, col0) of that output row are zeroed (the exact-zero block).
+//   tail_rr = (sqrt(rr) x - S / sqrt(rr)) / sqrt(rr + 1) sqrt(c) = a1 x - a2 S,
+//   a2 = sqrt(c) / sqrt(rr (rr + 1)),  a1 = rr a2   (MUFU rsqrt + one cubic step).
+// One warp per TILE_ROWS tile; lane j derives the scalars of row j of each batch of
+// 32 rows (shuffled to the warp when the row is processed) and four rows' loads are
+// issued before their sequential prefix updates.
+template <int MC>  // columns per lane: cols <= 32 MC (few registers -> many warps in flight)
 __global__ void __launch_bounds__(256) tail_emit_kernel(
     const double* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ gid,
     const int64_t* __restrict__ gstart, const int64_t* __restrict__ scale_count, double scale_all,
     const int64_t* __restrict__ out_base, int64_t out_base_all, int out_ld, int col0,
     const double* __restrict__ carry, int64_t ntiles, double* __restrict__ out) {
+  const unsigned FULLM = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= ntiles) return;
   const int64_t r0 = t * TILE_ROWS, r1 = min(rows, r0 + TILE_ROWS);
-  double s[MAXC];
+  double s[MC];
 #pragma unroll
-  for (int k = 0; k < MAXC; ++k) s[k] = (k * 32 + lane < cols) ? carry[t * cols + k * 32 + lane] : 0.0;
-  for (int64_t r = r0; r < r1; ++r) {
-    const int g = gid ? gid[r] : 0;
-    const double* row = x + r * cols;
-    if (g < 0) continue;
-    const int64_t rr = r - (gid ? gstart[g] : 0);
-    if (rr == 0) {
-#pragma unroll
-      for (int k = 0; k < MAXC; ++k)
-        if (k * 32 + lane < cols) s[k] = __ldg(row + k * 32 + lane);
-      continue;
+  for (int k = 0; k < MC; ++k) s[k] = (k * 32 + lane < cols) ? carry[t * cols + k * 32 + lane] : 0.0;
+  for (int64_t rb = r0; rb < r1; rb += 32) {
+    int kind = 0;  // 0 no output (key absent), 1 group start (head row), 2 tail row
+    double a1 = 0.0, a2 = 0.0;
+    int64_t orow = 0;
+    {
+      const int64_t r = rb + lane;
+      if (r < r1) {
+        const int g = gid ? gid[r] : 0;
+        if (g >= 0) {
+          const int64_t rr = r - (gid ? gstart[g] : 0);
+          if (rr == 0) {
+            kind = 1;
+          } else {
+            kind = 2;
+            const double rd = (double)rr;
+            const double c = scale_count ? (double)scale_count[g] : scale_all;
+            a2 = (c * rsqrt_nr(c)) * rsqrt_nr(rd * (rd + 1.0));
+            a1 = rd * a2;
+            orow = (gid ? out_base[g] : out_base_all) + rr - 1;
+          }
+        }
+      }
     }
-    const double si = sqrt((double)rr), si1 = sqrt((double)rr + 1.0);
-    const double sc = sqrt(scale_count ? (double)scale_count[g] : scale_all);
-    double* orow = out + ((gid ? out_base[g] : out_base_all) + rr - 1) * out_ld;
-    for (int c = lane; c < col0; c += 32) orow[c] = 0.0;
+    const int nb = r1 - rb < 32 ? (int)(r1 - rb) : 32;
+    for (int j0 = 0; j0 < nb; j0 += 4) {
+      double v[4][MC];
 #pragma unroll
-    for (int k = 0; k < MAXC; ++k) {
-      const int c = k * 32 + lane;
-      if (c < cols) {
-        const double v = __ldg(row + c);
-        orow[col0 + c] = (si * v - s[k] / si) / si1 * sc;
-        s[k] += v;
+      for (int u = 0; u < 4; ++u) {
+        const double* row = x + (rb + j0 + u) * cols;
+        const bool in = j0 + u < nb;
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+          const int c = k * 32 + lane;
+          v[u][k] = (in && c < cols) ? __ldg(row + c) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u;
+        const int kj = __shfl_sync(FULLM, kind, j & 31);
+        const double b1 = __shfl_sync(FULLM, a1, j & 31), b2 = __shfl_sync(FULLM, a2, j & 31);
+        const int64_t oj = __shfl_sync(FULLM, orow, j & 31);
+        if (j >= nb || kj == 0) continue;
+        if (kj == 1) {
+#pragma unroll
+          for (int k = 0; k < MC; ++k) s[k] = v[u][k];
+          continue;
+        }
+        double* orw = out + oj * out_ld;
+        for (int c = lane; c < col0; c += 32) orw[c] = 0.0;
+#pragma unroll
+        for (int k = 0; k < MC; ++k) {
+          const int c = k * 32 + lane;
+          if (c < cols) orw[col0 + c] = fma(b1, v[u][k], -b2 * s[k]);
+          s[k] += v[u][k];
+        }
       }
     }
   }
 }
 
 // Top block rows: A row i of group g -> output row red_off[g] + (i - a_start[g]):
-// [sqrt(m2g) A_i | totals_b[g] / sqrt(m2g)].
+// [sqrt(m2g) A_i | totals_b[g] / sqrt(m2g)].  One warp per row, lanes
+// over the columns; the row scale from MUFU rsqrt + one cubic step.
 __global__ void top_emit_kernel(const double* __restrict__ a, int64_t m1, int n1,
                                 const int32_t* __restrict__ gid_a, const int64_t* __restrict__ a_start,
                                 const int64_t* __restrict__ b_count, int64_t m2_all,
                                 const int64_t* __restrict__ red_off, const double* __restrict__ b_totals,
                                 int n2, double* __restrict__ out) {
   const int n = n1 + n2;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m1 * n;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx / n;
-    const int c = (int)(idx - i * n);
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < m1;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int g = gid_a ? gid_a[i] : 0;
     if (g < 0) continue;
     const double m2g = gid_a ? (double)b_count[g] : (double)m2_all;
+    const double rs = rsqrt_nr(m2g), sq = m2g * rs;
     const int64_t orow = gid_a ? red_off[g] + (i - a_start[g]) : i;
-    out[orow * n + c] = c < n1 ? a[i * n1 + c] * sqrt(m2g) : b_totals[(int64_t)g * n2 + (c - n1)] / sqrt(m2g);
+    const double* arow = a + i * n1;
+    const double* brow = b_totals + (int64_t)g * n2;
+    double* o = out + orow * n;
+    for (int c = lane; c < n; c += 32) o[c] = c < n1 ? __ldg(arow + c) * sq : brow[c - n1] * rs;
   }
+}
+
+static void launch_tail_emit(jq_ctx* ctx, int cols, unsigned grid, const double* x, int64_t rows,
+                             const int32_t* gid, const int64_t* gstart, const int64_t* scale_count,
+                             double scale_all, const int64_t* out_base, int64_t out_base_all, int out_ld,
+                             int col0, const double* carry, int64_t ntiles, double* out) {
+  if (cols <= 64)
+    tail_emit_kernel<2><<<grid, 256, 0, ctx->stream>>>(x, rows, cols, gid, gstart, scale_count, scale_all,
+                                                       out_base, out_base_all, out_ld, col0, carry, ntiles, out);
+  else if (cols <= 128)
+    tail_emit_kernel<4><<<grid, 256, 0, ctx->stream>>>(x, rows, cols, gid, gstart, scale_count, scale_all,
+                                                       out_base, out_base_all, out_ld, col0, carry, ntiles, out);
+  else
+    tail_emit_kernel<8><<<grid, 256, 0, ctx->stream>>>(x, rows, cols, gid, gstart, scale_count, scale_all,
+                                                       out_base, out_base_all, out_ld, col0, carry, ntiles, out);
 }
 
 __global__ void tail_base_kernel(const int64_t* __restrict__ red_off, const int64_t* __restrict__ a_count,
@@ -381,9 +441,8 @@ extern "C" int jq_head_tail(jq_ctx* ctx, const double* m, int64_t rows, int64_t 
   JQ_TRY(segscan_dev(ctx, dm, rows, cols, nullptr, nullptr, nullptr, nullptr, 1, &ss));
   head_row_kernel<<<1, 256, 0, ctx->stream>>>(ss.totals, (int)cols, (double)rows, dout);
   JQ_CHECK_LAUNCH(ctx);
-  tail_emit_kernel<<<(unsigned)cdiv(ss.ntiles, 8), 256, 0, ctx->stream>>>(
-      dm, rows, (int)cols, nullptr, nullptr, nullptr, 1.0, nullptr, 1, (int)cols, 0, ss.carry,
-      ss.ntiles, dout);
+  launch_tail_emit(ctx, (int)cols, (unsigned)cdiv(ss.ntiles, 8), dm, rows, nullptr, nullptr, nullptr, 1.0, nullptr,
+                   1, (int)cols, 0, ss.carry, ss.ntiles, dout);
   JQ_CHECK_LAUNCH(ctx);
   JQ_TRY(copy_out(ctx, out, (const double*)dout, rows * cols));
   return sync_and_check_flags(ctx);
@@ -466,7 +525,7 @@ extern "C" int jq_reduce(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, c
   } else {
     JQ_TRY(segscan_dev(ctx, db, 0, cols_b, nullptr, nullptr, nullptr, nullptr, cap, &ss));
   }
-  top_emit_kernel<<<grid_for(m1 * n), 256, 0, ctx->stream>>>(
+  top_emit_kernel<<<grid_for(m1 * 32), 256, 0, ctx->stream>>>(
       da, m1, (int)n1, keyed ? gr.gid_a : nullptr, keyed ? gr.a_start : nullptr,
       keyed ? gr.b_count : nullptr, m2, keyed ? gr.red_off : nullptr, ss.totals, (int)n2, dout);
   JQ_CHECK_LAUNCH(ctx);
@@ -477,9 +536,9 @@ extern "C" int jq_reduce(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, c
       tail_base_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(gr.red_off, gr.a_count, gr.d_n, base);
       JQ_CHECK_LAUNCH(ctx);
     }
-    tail_emit_kernel<<<(unsigned)cdiv(ss.ntiles, 8), 256, 0, ctx->stream>>>(
-        db, m2, (int)n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
-        keyed ? gr.a_count : nullptr, (double)m1, base, m1, (int)n, (int)n1, ss.carry, ss.ntiles, dout);
+    launch_tail_emit(ctx, (int)n2, (unsigned)cdiv(ss.ntiles, 8), db, m2, keyed ? gr.gid_b : nullptr,
+                     keyed ? gr.b_start : nullptr, keyed ? gr.a_count : nullptr, (double)m1, base, m1, (int)n,
+                     (int)n1, ss.carry, ss.ntiles, dout);
     JQ_CHECK_LAUNCH(ctx);
   }
   JQ_TRY(copy_out(ctx, out, (const double*)dout, total_rows * n));

@@ -53,23 +53,6 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// 1/x and 1/sqrt(x) from the MUFU approximations (~1e-6 relative) plus ONE cubically
-// convergent correction each: r (1 + e + e^2) and y (1 + e/2 + 3e^2/8), measured at
-// <= 2.2e-16 relative (tools/microbench/approx_acc.cu) -- the accuracy of two Newton
-// steps with a shorter dependent chain (3 and 4 fp64 ops) on the panel's critical path.
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double e = fma(-x, r, 1.0);
-  return fma(r, fma(e, e, e), r);
-}
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double e = fma(-x * y, y, 1.0);
-  return fma(y * e, fma(0.375, e, 0.5), y);
-}
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

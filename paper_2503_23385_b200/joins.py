@@ -51,7 +51,8 @@ def _reduce(a, ka, b, kb) -> ReducedMatrix:
     else:
         red_off = group_keys(ka, kb)[5]
         total = int(red_off[-1])
-        gb = [(int(red_off[g]), int(red_off[g + 1])) for g in range(len(red_off) - 1)]
+        ro = red_off.tolist()
+        gb = list(zip(ro[:-1], ro[1:]))
     out = like((total, n1 + n2), a, b)
     if total:
         rows = np.zeros(1, dtype=np.int64)
@@ -91,8 +92,9 @@ def group_keys(keys_a, keys_b):
     ka = as_keys(keys_a, len(keys_a))
     kb = as_keys(keys_b, len(keys_b))
     cap = max(1, min(len(ka), len(kb)))
-    outs = [np.zeros(cap, dtype=np.int64) for _ in range(5)]
-    red = np.zeros(cap + 1, dtype=np.int64)
+    # np.empty: only the first ng entries are written (no 5 x cap zero fill on the host)
+    outs = [np.empty(cap, dtype=np.int64) for _ in range(5)]
+    red = np.empty(cap + 1, dtype=np.int64)
     ng = np.zeros(1, dtype=np.int64)
     N.use_torch_stream(ka, kb)
     N.check(N.lib().jq_group_keys(N.ctx(), N.ptr(ka), len(ka), N.ptr(kb), len(kb), cap,
