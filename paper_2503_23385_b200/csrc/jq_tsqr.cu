@@ -1218,10 +1218,10 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
                            bool canonical, double* r_out, int use_tma) {
   switch (np_for(n)) {
     case 16:
-      if (leaf_impl() == 0) return run_stream_ws<CfgS<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 0) return run_stream_ws<CfgS<16, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 32:
-      if (leaf_impl() == 0) return run_stream_ws<CfgS<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 0) return run_stream_ws<CfgS<32, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 64:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
