@@ -1183,9 +1183,9 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
     const char* e = getenv("JQ_TSQR_EXPLICIT");
     return e && e[0] == '1';
   }();
-  static const int debug_flags = [] {  // JQ_TSQR_DEBUG=4: loader skips the transform (timing only)
+  static const int debug_flags = [] {  // JQ_TSQR_DEBUG=8: ignore %warpid (fallback role layout; tests)
     const char* e = getenv("JQ_TSQR_DEBUG");
-    return e ? atoi(e) & 4 : 0;
+    return e ? atoi(e) & 8 : 0;
   }();
   align = std::max<int64_t>(align, 8);
   int64_t max_ctas = int64_t(ctx->sms) * occ;

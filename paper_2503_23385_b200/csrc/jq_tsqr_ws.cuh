@@ -154,7 +154,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       ++ndata;
     }
   }
-  const bool mapped = chain_w >= 0 && loader_w >= 0 && ndata == C::DW;
+  const bool mapped = !(flags & 8) && chain_w >= 0 && loader_w >= 0 && ndata == C::DW;
   if (!mapped) { chain_w = 0; loader_w = 1; }
   int d = -1;
   {

@@ -1,6 +1,7 @@
-"""The TSQR leaf kernel has three implementations (warp-specialised default, CTA-wide,
-explicit-panel fallback forced) selected by environment variables that the library
-reads once per process; each is checked in a subprocess against the same parity tests."""
+"""The TSQR leaf kernel has several paths (warp-specialised default, CTA-wide,
+explicit-panel fallback forced, warp roles assigned without %warpid) selected by
+environment variables that the library reads once per process; each is checked in a
+subprocess against the same parity tests."""
 
 import os
 import subprocess
@@ -13,8 +14,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"JQ_TSQR_IMPL": "cta"}, {"JQ_TSQR_EXPLICIT": "1"},
-                                 {"JQ_TSQR_IMPL": "cta", "JQ_TSQR_EXPLICIT": "1"}],
-                         ids=["cta", "ws-explicit", "cta-explicit"])
+                                 {"JQ_TSQR_IMPL": "cta", "JQ_TSQR_EXPLICIT": "1"},
+                                 {"JQ_TSQR_DEBUG": "8"}],
+                         ids=["cta", "ws-explicit", "cta-explicit", "ws-fixed-roles"])
 def test_leaf_impl_parity(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
