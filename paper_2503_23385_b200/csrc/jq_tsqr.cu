@@ -133,6 +133,13 @@ struct DenseSrc {
   __device__ int64_t limit(int64_t) const { return INT64_MAX; }
   template <class C>
   __device__ void prep_warp(double*, double*, double*, int64_t, int, int) const {}
+  template <class C>
+  __device__ void seg_coeffs(double*, int64_t, int, int, int, int) const {}
+  template <class C>
+  __device__ void seg_pass1(const double*, const double*, double*, int64_t, int, int, int, int) const {}
+  template <class C>
+  __device__ void seg_pass2(double*, double*, const double*, const double*, double, double, int64_t, int, int, int,
+                            int, int, int) const {}
 };
 
 struct FigaroSrc {
@@ -410,6 +417,124 @@ struct FigaroSrc {
     if (ha) S[ca] = sa;
     if (hb) S[cb] = sb;
     __syncwarp();
+  }
+
+  // ---- the same transform split over several loader warps (row segments [i0, i1)):
+  // per-row scalars, then per-column (sum since the last group start, group start seen)
+  // of each segment, then each segment's carry-in from S and the earlier segments and
+  // the in-place transform.  lsr: [segment][2][64].
+  template <class C>
+  __device__ void seg_coeffs(double* scratch, int64_t v0, int nrows, int lane, int i0, int i1) const {
+    double* c1 = scratch;
+    double* c2 = scratch + C::K;
+    double* mode = scratch + 2 * C::K;
+    if (v0 < m1pad) {
+      for (int i = i0 + lane; i < i1; i += 32) {
+        int g = -1;
+        double m2g = 0.0;
+        if (i < nrows) {
+          const int64_t r = v0 + i;
+          g = fa.gid_a ? fa.gid_a[r] : 0;
+          if (g >= 0) m2g = fa.gid_a ? (double)fa.b_count[g] : (double)fa.m2_global;
+        }
+        const double rs2 = g >= 0 && m2g > 0.0 ? rsqrt_nr(m2g) : 0.0;
+        c1[i] = m2g * rs2;
+        c2[i] = rs2;
+        mode[i] = (double)g;
+      }
+      return;
+    }
+    const int64_t b0 = v0 - m1pad;
+    int* imode = reinterpret_cast<int*>(mode);
+    for (int i = i0 + lane; i < i1; i += 32) {
+      int md = 0;
+      double a1 = 0.0, a2 = 0.0;
+      if (i < nrows) {
+        const int64_t br = b0 + i;
+        int64_t rr = 0;
+        double m1g = 0.0;
+        bool valid = true;
+        if (fa.gid_b) {
+          const int g = fa.gid_b[br];
+          valid = g >= 0;
+          if (valid) { rr = br - fa.b_start[g]; m1g = (double)fa.a_count[g]; }
+        } else {
+          rr = fa.b_row0 + br;
+          m1g = (double)fa.m1_global;
+        }
+        if (valid) {
+          if (rr == 0) {
+            md = 1;
+          } else {
+            const double rd = (double)rr;
+            md = 2;
+            a2 = (m1g * rsqrt_nr(m1g)) * rsqrt_nr(rd * (rd + 1.0));
+            a1 = rd * a2;
+          }
+        }
+      }
+      c1[i] = a1; c2[i] = a2; imode[i] = md;
+    }
+  }
+  template <class C>
+  __device__ void seg_pass1(const double* raw, const double* scratch, double* lsr, int64_t v0, int nrows, int lane,
+                            int i0, int i1) const {
+    if (v0 < m1pad) return;
+    const int* imode = reinterpret_cast<const int*>(scratch + 2 * C::K);
+    const int n2 = (int)fa.n2;
+    const int e = min(i1, nrows);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c >= n2) continue;
+      double loc = 0.0, reset = 0.0;
+      for (int i = i0; i < e; ++i) {
+        const double xv = raw[i * n2 + c];
+        const int md = imode[i];
+        if (md == 1) { loc = xv; reset = 1.0; }
+        else if (md == 2) loc += xv;
+      }
+      lsr[c] = loc;
+      lsr[64 + c] = reset;
+    }
+  }
+  // s_in0 / s_in1: S of this lane's columns read before the barrier that precedes this
+  // pass (the last segment rewrites S at its end)
+  template <class C>
+  __device__ void seg_pass2(double* raw, double* S, const double* scratch, const double* lsr_all, double s_in0,
+                            double s_in1, int64_t v0, int nrows, int lane, int i0, int i1, int seg, int nseg) const {
+    if (v0 < m1pad) return;
+    const double* c1 = scratch;
+    const double* c2 = scratch + C::K;
+    const int* imode = reinterpret_cast<const int*>(scratch + 2 * C::K);
+    const int n2 = (int)fa.n2;
+    const int e = min(i1, nrows);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c >= n2) continue;
+      double sv = h == 0 ? s_in0 : s_in1;
+      for (int k = 0; k < seg; ++k) {
+        const double l = lsr_all[k * 128 + c], r = lsr_all[k * 128 + 64 + c];
+        sv = r != 0.0 ? l : sv + l;
+      }
+      for (int ib = i0; ib < e; ib += 4) {
+        double xv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xv[k] = ib + k < e ? raw[(ib + k) * n2 + c] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (ib + k < e) {
+            const int md = imode[ib + k];
+            double out = 0.0;
+            if (md == 1) sv = xv[k];
+            else if (md == 2) { out = fma(c1[ib + k], xv[k], -c2[ib + k] * sv); sv += xv[k]; }
+            raw[(ib + k) * n2 + c] = out;
+          }
+        }
+      }
+      if (seg == nseg - 1) S[c] = sv;
+    }
   }
 
   template <class C>

@@ -9,8 +9,9 @@
 //   * the CHAIN warp: the Gram-panel chain (factor_panel_gram: T, M', R rows), then
 //     the update of the next tile (the lookahead tile) and its Gram, derived from
 //     partials -- the whole critical path;
-//   * the LOADER warp: TMA of the next chunk's raw rows and the Claim-1 / tail
-//     transform in place (prep_warp), one chunk ahead of the data warps;
+//   * the LOADER warp(s): TMA of the next chunk's raw rows and the Claim-1 / tail
+//     transform in place (prep_warp; for NP <= 32 three loader warps split the rows:
+//     segment sums, carries, transform), one chunk ahead of the data warps;
 // and the twelve warps on SMSPs 1-3 hold the chunk (DW x KW rows in registers) and
 // do all bulk DMMA work: partials, the reduces of the other tiles and the applies.
 // The role assignment only moves work between warps: results do not depend on it
@@ -60,7 +61,10 @@ struct CfgS {
   static constexpr int OFF_FLAG = OFF_S + NP;             // [2] chain accepted, by parity
   static constexpr int OFF_GP = OFF_FLAG + 2;             // [DW][64] C^T C partials of the next tile (ws2)
   static constexpr int OFF_GD = OFF_GP + DW * 64;         // [DW][64] direct Gram partials (ws2)
-  static constexpr int OFF_ROLE = OFF_GD + DW * 64;       // WARPS ints: SMSP of each warp
+  static constexpr int NLOAD = NP <= 32 ? 3 : 1;  // loader warps: narrow leaves are loader-bound; at
+  // NP = 64 two extra active warps on SMSP 0 slow the chain more than they help (4.62 vs 4.47 ms)
+  static constexpr int OFF_LSR = OFF_GD + DW * 64;        // [NLOAD][2][64] loader segment sums
+  static constexpr int OFF_ROLE = OFF_LSR + NLOAD * 128;  // WARPS ints: SMSP of each warp
   static constexpr int OFF_BAR = OFF_ROLE + WARPS / 2;    // mbarriers: TMA, READY, FREE, VREADY
   static constexpr int TOTAL = OFF_BAR + 4;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
@@ -87,6 +91,7 @@ __device__ long long g_trace[4096];
 
 constexpr int BAR_ALL = 1;   // chain + data warps
 constexpr int BAR_DATA = 2;  // data warps
+constexpr int BAR_LOAD = 3;  // loader warps
 
 // ------------------------------------------------------------------ the kernel (ws2)
 // The chain warp also performs, right after B_p,
@@ -145,28 +150,35 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  int chain_w = -1, loader_w = -1, ndata = 0;
+  // chain: the first warp on SMSP 0; loaders: the next NLOAD warps on SMSP 0; data
+  // warps: the DW warps elsewhere (any other layout falls back to chain 0, loaders
+  // 1..NLOAD, data warps after them)
+  int chain_w = -1, li = -1, nz = 0, ndata = 0;
   for (int w = 0; w < C::WARPS; ++w) {
     if (role[w] == 0) {
-      if (chain_w < 0) chain_w = w;
-      else if (loader_w < 0) loader_w = w;
+      if (nz == 0) chain_w = w;
+      else if (nz <= C::NLOAD && w == warp) li = nz - 1;
+      ++nz;
     } else {
       ++ndata;
     }
   }
-  const bool mapped = !(flags & 8) && chain_w >= 0 && loader_w >= 0 && ndata == C::DW;
-  if (!mapped) { chain_w = 0; loader_w = 1; }
-  int d = -1;
+  const bool mapped = !(flags & 8) && nz >= 1 + C::NLOAD && ndata == C::DW;
+  if (!mapped) {
+    chain_w = 0;
+    li = (warp >= 1 && warp <= C::NLOAD) ? warp - 1 : -1;
+  }
+  int d = -1;  // data-warp index
   {
     int k = 0;
     for (int w = 0; w < C::WARPS; ++w) {
-      const bool data = mapped ? role[w] != 0 : (w >= 2 && w < 2 + C::DW);
+      const bool data = mapped ? role[w] != 0 : (w >= 1 + C::NLOAD && w < 1 + C::NLOAD + C::DW);
       if (!data) continue;
       if (w == warp) d = k;
       ++k;
     }
   }
-  if (warp != chain_w && warp != loader_w && d < 0) return;
+  if (warp != chain_w && li < 0 && d < 0) return;
 
   auto chunk_end = [&](int64_t r0) -> int64_t {
     int64_t e = r0 + C::K < row_end ? r0 + C::K : row_end;
@@ -195,33 +207,49 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     out[1] = v[0].y;
   };
 
-  if (warp == loader_w) {
+  if (li >= 0) {
+    // ================= loader warp(s): li == 0 fetches; all transform a row segment
     uint32_t ph_tma = 0, ph_free = 0;
     int64_t nchunk = 0;
+    double* lsr = smem_dyn + C::OFF_LSR;
     for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0), ++nchunk) {
       const int64_t r1 = chunk_end(r0);
       const int nr = chunk_rows(r0, r1);
       const int rcol = src.rc(r0);
       const int nel = nr * rcol;
-      if (nchunk > 0) {
-        mbar_wait_idle(bar_free, ph_free);  // the loader sits next to the chain warp on SMSP 0
-        ph_free ^= 1;
+      if (li == 0) {
+        if (nchunk > 0) {
+          mbar_wait_idle(bar_free, ph_free);  // the loader sits next to the chain warp on SMSP 0
+          ph_free ^= 1;
+        }
+        TR(2, 1);
+        if (flags & 1) {
+          if (lane == 0) bulk_fetch(bar_tma, raw, src.ptr(r0), uint32_t(nel) * 8u & ~15u);
+          mbar_wait(bar_tma, ph_tma);
+          ph_tma ^= 1;
+          if ((nel & 1) && lane == 0) raw[nel - 1] = __ldg(src.ptr(r0) + nel - 1);
+        } else {
+          const double* p = src.ptr(r0);
+          for (int e = lane; e < nel; e += 32) raw[e] = __ldg(p + e);
+        }
+        __syncwarp();
+        TR(2, 2);
       }
-      TR(2, 1);
-      if (flags & 1) {
-        if (lane == 0) bulk_fetch(bar_tma, raw, src.ptr(r0), uint32_t(nel) * 8u & ~15u);
-        mbar_wait(bar_tma, ph_tma);
-        ph_tma ^= 1;
-        if ((nel & 1) && lane == 0) raw[nel - 1] = __ldg(src.ptr(r0) + nel - 1);
+      if (C::NLOAD == 1) {
+        src.template prep_warp<C>(raw, S, scratch, r0, nr, lane);
       } else {
-        const double* p = src.ptr(r0);
-        for (int e = lane; e < nel; e += 32) raw[e] = __ldg(p + e);
+        named_bar(BAR_LOAD, C::NLOAD * 32);  // raw rows of the chunk in shared memory
+        const int i0 = li * C::K / C::NLOAD, i1 = (li + 1) * C::K / C::NLOAD;
+        src.template seg_coeffs<C>(scratch, r0, nr, lane, i0, i1);
+        __syncwarp();
+        src.template seg_pass1<C>(raw, scratch, lsr + li * 128, r0, nr, lane, i0, i1);
+        const double s_in0 = lane < C::NP ? S[lane] : 0.0, s_in1 = lane + 32 < C::NP ? S[lane + 32] : 0.0;
+        named_bar(BAR_LOAD, C::NLOAD * 32);  // segment sums published, S read by every segment
+        src.template seg_pass2<C>(raw, S, scratch, lsr, s_in0, s_in1, r0, nr, lane, i0, i1, li, C::NLOAD);
+        named_bar(BAR_LOAD, C::NLOAD * 32);  // chunk transformed
       }
-      __syncwarp();
-      TR(2, 2);
-      if (!(flags & 4)) src.template prep_warp<C>(raw, S, scratch, r0, nr, lane);  // 4: timing experiment only
       TR(2, 3);
-      if (lane == 0) mbar_arrive(bar_ready);
+      if (li == 0 && lane == 0) mbar_arrive(bar_ready);
     }
     return;
   }
