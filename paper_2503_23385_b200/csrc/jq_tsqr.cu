@@ -351,23 +351,27 @@ struct FigaroSrc {
       c1[i] = a1; c2[i] = a2; imode[i] = md;
     }
     __syncwarp();
-    // lane = columns lane and lane + 32 (n2 <= 64), one pass over the rows in batches of
+    // lane = columns lane + 32 j (n2 <= 32 CPL), one pass over the rows in batches of
     // 4 (vector loads of the row scalars; a select-free path when the 4 rows are all
     // tail rows, the Cartesian case), the next batch's loads issued first
+    constexpr int CPL = C::NP <= 32 ? 1 : C::NP / 32;
     const int n2 = (int)fa.n2;
-    const int ca = lane, cb = lane + 32;
-    const bool ha = ca < n2, hb = cb < n2;
-    double sa = ha ? S[ca] : 0.0, sb = hb ? S[cb] : 0.0;
+    bool h[CPL];
+    double sc[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      h[j] = lane + 32 * j < n2;
+      sc[j] = h[j] ? S[lane + 32 * j] : 0.0;
+    }
     const int nfull = nrows & ~3;
-    double xa[4], xb[4];
+    double x[CPL][4];
     double2 q1[2], q2[2];
     int4 qm;
     auto load = [&](int ib) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        xa[k] = ha ? raw[(ib + k) * n2 + ca] : 0.0;
-        xb[k] = hb ? raw[(ib + k) * n2 + cb] : 0.0;
-      }
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) x[j][k] = h[j] ? raw[(ib + k) * n2 + lane + 32 * j] : 0.0;
       q1[0] = *reinterpret_cast<const double2*>(c1 + ib);
       q1[1] = *reinterpret_cast<const double2*>(c1 + ib + 2);
       q2[0] = *reinterpret_cast<const double2*>(c2 + ib);
@@ -376,46 +380,51 @@ struct FigaroSrc {
     };
     if (nfull > 0) load(0);
     for (int ib = 0; ib < nfull; ib += 4) {
-      const double ya[4] = {xa[0], xa[1], xa[2], xa[3]}, yb[4] = {xb[0], xb[1], xb[2], xb[3]};
+      double y[CPL][4];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) y[j][k] = x[j][k];
       const double b1[4] = {q1[0].x, q1[0].y, q1[1].x, q1[1].y}, b2[4] = {q2[0].x, q2[0].y, q2[1].x, q2[1].y};
       const int mk[4] = {qm.x, qm.y, qm.z, qm.w};
       if (ib + 4 < nfull) load(ib + 4);
-      double oa[4], ob[4];
+      double o[CPL][4];
       if ((mk[0] & mk[1] & mk[2] & mk[3]) == 2) {  // all tail rows
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          oa[k] = fma(b1[k], ya[k], -b2[k] * sa);
-          ob[k] = fma(b1[k], yb[k], -b2[k] * sb);
-          sa += ya[k];
-          sb += yb[k];
-        }
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int j = 0; j < CPL; ++j) {
+            o[j][k] = fma(b1[k], y[j][k], -b2[k] * sc[j]);
+            sc[j] += y[j][k];
+          }
       } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          oa[k] = mk[k] == 2 ? fma(b1[k], ya[k], -b2[k] * sa) : 0.0;
-          ob[k] = mk[k] == 2 ? fma(b1[k], yb[k], -b2[k] * sb) : 0.0;
-          sa = mk[k] == 1 ? ya[k] : (mk[k] == 2 ? sa + ya[k] : sa);
-          sb = mk[k] == 1 ? yb[k] : (mk[k] == 2 ? sb + yb[k] : sb);
-        }
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int j = 0; j < CPL; ++j) {
+            o[j][k] = mk[k] == 2 ? fma(b1[k], y[j][k], -b2[k] * sc[j]) : 0.0;
+            sc[j] = mk[k] == 1 ? y[j][k] : (mk[k] == 2 ? sc[j] + y[j][k] : sc[j]);
+          }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (ha) raw[(ib + k) * n2 + ca] = oa[k];
-        if (hb) raw[(ib + k) * n2 + cb] = ob[k];
-      }
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int j = 0; j < CPL; ++j)
+          if (h[j]) raw[(ib + k) * n2 + lane + 32 * j] = o[j][k];
     }
     for (int i = nfull; i < nrows; ++i) {  // tail of a partial chunk
-      const double x0 = ha ? raw[i * n2 + ca] : 0.0, x1 = hb ? raw[i * n2 + cb] : 0.0;
       const int mk = imode[i];
-      const double o0 = mk == 2 ? fma(c1[i], x0, -c2[i] * sa) : 0.0;
-      const double o1 = mk == 2 ? fma(c1[i], x1, -c2[i] * sb) : 0.0;
-      sa = mk == 1 ? x0 : (mk == 2 ? sa + x0 : sa);
-      sb = mk == 1 ? x1 : (mk == 2 ? sb + x1 : sb);
-      if (ha) raw[i * n2 + ca] = o0;
-      if (hb) raw[i * n2 + cb] = o1;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        const double xv = h[j] ? raw[i * n2 + lane + 32 * j] : 0.0;
+        const double ov = mk == 2 ? fma(c1[i], xv, -c2[i] * sc[j]) : 0.0;
+        sc[j] = mk == 1 ? xv : (mk == 2 ? sc[j] + xv : sc[j]);
+        if (h[j]) raw[i * n2 + lane + 32 * j] = ov;
+      }
     }
-    if (ha) S[ca] = sa;
-    if (hb) S[cb] = sb;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j)
+      if (h[j]) S[lane + 32 * j] = sc[j];
     __syncwarp();
   }
 
@@ -1351,7 +1360,9 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
     case 64:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
       return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-    case 128: return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+    case 128:  // (CfgS<128, 16, 8, 1, 8> -- 64-row chunks beside the 70 KB R -- measured slower:
+      // C4 dense 1094 vs 861 ms, C5 22.5 vs 21.6 ms; the chain cost is per panel, not per row)
+      return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
     case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
   }
   return fail(JQ_E_INVALID, "column count above 256 is not supported by the TSQR kernels");

@@ -1,4 +1,4 @@
-// Warp-specialised streaming-TSQR leaf (NP <= 64), included by jq_tsqr.cu.
+// Warp-specialised streaming-TSQR leaf (NP <= 128), included by jq_tsqr.cu.
 //
 // Measured on B200 (tools/microbench/gchain.cu): the 8-step Householder chain of a
 // panel takes ~3.5k cycles alone but ~8.6k when other warps issue DMMA on the SAME
@@ -69,7 +69,7 @@ struct CfgS {
   static constexpr int TOTAL = OFF_BAR + 4;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
   static_assert(SMEM <= (MIN_CTAS == 1 ? 227 : 113) * 1024, "shared memory per CTA");
-  static_assert(NP <= 64, "loader transform assumes <= 64 columns per side");
+  static_assert(NP <= 128, "loader transform assumes <= 128 columns per side");
 };
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned count) {
@@ -151,7 +151,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
   }
   __syncthreads();
   // chain: the first warp on SMSP 0; loaders: the next NLOAD warps on SMSP 0; data
-  // warps: the DW warps elsewhere (any other layout falls back to chain 0, loaders
+  // warps: the first DW warps elsewhere (any other layout falls back to chain 0, loaders
   // 1..NLOAD, data warps after them)
   int chain_w = -1, li = -1, nz = 0, ndata = 0;
   for (int w = 0; w < C::WARPS; ++w) {
@@ -163,7 +163,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       ++ndata;
     }
   }
-  const bool mapped = !(flags & 8) && nz >= 1 + C::NLOAD && ndata == C::DW;
+  const bool mapped = !(flags & 8) && nz >= 1 + C::NLOAD && ndata >= C::DW;
   if (!mapped) {
     chain_w = 0;
     li = (warp >= 1 && warp <= C::NLOAD) ? warp - 1 : -1;
@@ -173,7 +173,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     int k = 0;
     for (int w = 0; w < C::WARPS; ++w) {
       const bool data = mapped ? role[w] != 0 : (w >= 1 + C::NLOAD && w < 1 + C::NLOAD + C::DW);
-      if (!data) continue;
+      if (!data || k == C::DW) continue;
       if (w == warp) d = k;
       ++k;
     }
