@@ -11,6 +11,8 @@
 // stopping rule; results agree with the oracle to rounding.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include <cooperative_groups.h>
 
@@ -230,6 +232,253 @@ jacobi_coop_kernel(double* __restrict__ A, double* __restrict__ V, int n, int wa
     }
 }
 
+// Cluster variant (the default for n >= 31): one thread-block cluster of np/(2 WPC) CTAs
+// (<= 16; 8 warps each), one warp per column pair, A resident in the cluster's shared
+// memory for the whole solve.  Columns are stored by tournament POSITION: CTA c owns
+// the positions of pairs WPC c .. WPC c + WPC-1 (k and np-1-k), and between rounds
+// every player moves from position k to k-1 (1 -> np-1, 0 fixed), so a warp reads its
+// pair from local shared memory and writes the rotated columns to their next positions
+// -- local except at the band edges (two columns per CTA per round over distributed
+// shared memory), double-buffered by round parity.  One cluster barrier per round.
+// V is not carried: every rotation (c, s) is logged and jacobi_v_kernel replays the
+// log on the rows of V afterwards (rows of V are independent).  Same pairs and stopping
+// rule as jacobi_coop_kernel; the rotation is computed with the MUFU reciprocal /
+// reciprocal square root plus one cubic correction (<= 2.2e-16 relative, like the
+// TSQR chain), the acceptance test as ga^2 < tol^2 al be; lane l owns rows l, l + 32,
+// ... and the dot products are warp-tree sums (deterministic).  A round is
+// issue-bound (~300 instructions per pair), hence few warps per SM.
+constexpr int SVD_MAX_SWEEPS = 64;
+
+template <int WPC>
+__device__ __forceinline__ void pos_home(int k, int np, int& cta, int& slot) {
+  const int half = np >> 1;
+  const int pi = k < half ? k : np - 1 - k;
+  cta = pi / WPC;
+  slot = (k < half ? 0 : WPC) + pi % WPC;
+}
+
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32, 1)
+jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_sweeps, int* flags,
+                      double* __restrict__ sig, double2* __restrict__ rlog, int* __restrict__ nsweeps,
+                      double* __restrict__ values, int n_out) {
+  namespace cg = cooperative_groups;
+  constexpr int COLS = 2 * WPC, THREADS = WPC * 32;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double cols[];  // [2 buffers][COLS][np], by position; then the
+  // sweep's rotation log of this CTA's pairs [np - 1][WPC] (global stores inside the round
+  // loop would make every cluster barrier wait for them)
+  double2* slog = reinterpret_cast<double2*>(cols + 2 * COLS * np);
+  __shared__ int rotf[3];
+  __shared__ double red[WPC];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)cluster.block_rank(), nct = (int)cluster.num_blocks();
+  const int half = np >> 1;
+  for (int idx = tid; idx < COLS * np; idx += THREADS) {
+    const int sl = idx / np, i = idx - sl * np;
+    const int pi = rank * WPC + (sl % WPC);
+    const int k = sl < WPC ? pi : np - 1 - pi;  // round 0: player k at position k
+    cols[idx] = A[(size_t)k * np + i];
+  }
+  // |R|_F^2, the same fixed-order sum in every CTA -> negligible-column threshold
+  double f = 0.0;
+  for (int idx = tid; idx < np * np; idx += THREADS) f = fma(A[idx], A[idx], f);
+  f = warp_sum(f);
+  if (lane == 0) red[warp] = f;
+  if (tid < 3) rotf[tid] = 0;
+  __syncthreads();
+  double fro = 0.0;
+  for (int w = 0; w < WPC; ++w) fro += red[w];
+  const double eps = 2.220446049250313e-16;
+  const double tiny = (double(np) * eps) * (double(np) * eps) * fro;
+  const double tol2 = tol * tol;
+  const int pi = rank * WPC + warp;
+  const int klo = pi, khi = np - 1 - pi;
+  // next positions of the two players and where they live
+  int dlo_c, dlo_s, dhi_c, dhi_s;
+  pos_home<WPC>(klo == 0 ? 0 : (klo == 1 ? np - 1 : klo - 1), np, dlo_c, dlo_s);
+  pos_home<WPC>(khi - 1, np, dhi_c, dhi_s);
+  double* const wlo0 = dlo_c == rank ? cols + dlo_s * np : cluster.map_shared_rank(cols + dlo_s * np, dlo_c);
+  double* const whi0 = dhi_c == rank ? cols + dhi_s * np : cluster.map_shared_rank(cols + dhi_s * np, dhi_c);
+  const size_t bufsz = size_t(COLS) * np;
+  constexpr int RPL = 256 / 32;  // rows per lane (np <= 256, a multiple of 32: warp-uniform bounds)
+  const int nk = np >> 5;
+  cluster.sync();
+
+  int sweep = 0, cur = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) rotf[(sweep + 1) % 3] = 0;  // read two sweeps ago, before this sweep's barriers
+    bool rotated = false;
+    int plo = klo, phi = khi;  // players at the two positions (round 0: identity)
+    for (int r = 0; r < np - 1; ++r, cur ^= 1) {
+      const bool lo_is_p = plo < phi;
+      const double* src = cols + cur * bufsz;
+      const double* cp = src + (lo_is_p ? warp : WPC + warp) * np;
+      const double* cq = src + (lo_is_p ? WPC + warp : warp) * np;
+      double x[RPL], y[RPL];
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        x[k] = k < nk ? cp[lane + 32 * k] : 0.0;
+        y[k] = k < nk ? cq[lane + 32 * k] : 0.0;
+      }
+      double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        al = fma(x[k], x[k], al);
+        be = fma(y[k], y[k], be);
+        ga = fma(x[k], y[k], ga);
+      }
+      al = warp_sum(al);
+      be = warp_sum(be);
+      ga = warp_sum(ga);
+      const bool rot = !(al <= tiny || be <= tiny || ga == 0.0 || ga * ga < tol2 * (al * be));
+      double c = 1.0, sn = 0.0;
+      if (rot) {
+        const double zeta = (be - al) * rcp_nr(2.0 * ga);
+        const double az = fabs(zeta);
+        double t;
+        if (az < 1e100) {
+          const double q = fma(az, az, 1.0);
+          t = rcp_nr(fma(q, rsqrt_nr(q), az));  // 1 / (|zeta| + sqrt(1 + zeta^2))
+        } else {
+          t = 0.5 * rcp_nr(az);
+        }
+        t = zeta >= 0.0 ? t : -t;
+        c = rsqrt_nr(fma(t, t, 1.0));
+        sn = c * t;
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) {
+          const double xk = x[k], yk = y[k];
+          x[k] = c * xk - sn * yk;
+          y[k] = sn * xk + c * yk;
+        }
+        rotated = true;
+      }
+      if (lane == 0) slog[r * WPC + warp] = make_double2(c, sn);
+      // players to their next positions (buffer cur ^ 1)
+      double* wlo = wlo0 + (cur ^ 1) * bufsz;
+      double* whi = whi0 + (cur ^ 1) * bufsz;
+      double* wp = lo_is_p ? wlo : whi;
+      double* wq = lo_is_p ? whi : wlo;
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        if (k < nk) {
+          wp[lane + 32 * k] = x[k];
+          wq[lane + 32 * k] = y[k];
+        }
+      }
+      plo = plo == 0 ? 0 : (plo == np - 1 ? 1 : plo + 1);
+      phi = phi == np - 1 ? 1 : phi + 1;
+      cluster.sync();
+    }
+    if (rotated && lane == 0) rotf[sweep % 3] = 1;
+    __syncthreads();
+    for (int e = tid; e < (np - 1) * WPC; e += THREADS) {  // this sweep's log out
+      const int r = e / WPC, w = e - r * WPC;
+      rlog[((size_t)sweep * (np - 1) + r) * half + rank * WPC + w] = slog[e];
+    }
+    cluster.sync();
+    int any = 0;
+    for (int b = 0; b < nct; ++b) any |= *cluster.map_shared_rank(&rotf[sweep % 3], b);
+    if (!any) break;
+  }
+  if (rank == 0 && tid == 0) {
+    if (sweep == max_sweeps) atomicOr(flags, FLAG_NOCONV);
+    *nsweeps = sweep;  // sweeps with rotations (the last, clean one is not replayed)
+  }
+  // after whole sweeps every player is back at its own position: sigma_j = |column j|
+  const double* fin = cols + cur * bufsz;
+  for (int sl = warp; sl < COLS; sl += WPC) {
+    const int pj = rank * WPC + (sl % WPC);
+    const int j = sl < WPC ? pj : np - 1 - pj;
+    double sq = 0.0;
+    for (int i = lane; i < np; i += 32) sq = fma(fin[sl * np + i], fin[sl * np + i], sq);
+    sq = warp_sum(sq);
+    if (lane == 0) sig[j] = sqrt(sq);
+  }
+  cluster.sync();
+  for (int sl = warp; sl < COLS; sl += WPC) {
+    const int pj = rank * WPC + (sl % WPC);
+    const int j = sl < WPC ? pj : np - 1 - pj;
+    const double sj = sig[j];
+    int rk = 0;
+    for (int k = lane; k < np; k += 32) {
+      const double sk = sig[k];
+      rk += (sk > sj) || (sk == sj && k < j);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+    if (rk < n_out && lane == 0) values[rk] = sj;
+  }
+}
+
+// Row i of V (one warp per row): replay the logged rotations of jacobi_cluster_kernel
+// on V[i, :] (V = I at the start), rounds in order, lane l doing pairs l, l + 32, ...
+// (the same element arithmetic as a carried V); then vout[i][rank(j)] = V[i][j] for the
+// n_out largest sigma.
+constexpr int SVDV_WARPS = 4, SVDV_BATCH = 4;
+
+__global__ void __launch_bounds__(SVDV_WARPS * 32)
+jacobi_v_kernel(const double2* __restrict__ rlog, const int* __restrict__ nsweeps, int np,
+                const double* __restrict__ sig, double* __restrict__ vout, int n_out) {
+  __shared__ double rows[SVDV_WARPS][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = np >> 1;
+  const int i = blockIdx.x * SVDV_WARPS + warp;
+  if (i >= n_out) return;
+  double* row = rows[warp];
+  for (int j = lane; j < np; j += 32) row[j] = i == j ? 1.0 : 0.0;
+  __syncwarp();
+  const int rounds = *nsweeps * (np - 1);
+  int plo[4], phi[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    plo[k] = lane + 32 * k;
+    phi[k] = np - 1 - (lane + 32 * k);
+  }
+  double2 nx[SVDV_BATCH][4];  // the next batch of (c, s), loaded one batch ahead
+  auto load = [&](int r0) {
+#pragma unroll
+    for (int b = 0; b < SVDV_BATCH; ++b)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int pi = lane + 32 * k;
+        nx[b][k] = (pi < half && r0 + b < rounds) ? rlog[(size_t)(r0 + b) * half + pi] : make_double2(1.0, 0.0);
+      }
+  };
+  load(0);
+  for (int r0 = 0; r0 < rounds; r0 += SVDV_BATCH) {
+    double2 cs[SVDV_BATCH][4];
+#pragma unroll
+    for (int b = 0; b < SVDV_BATCH; ++b)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cs[b][k] = nx[b][k];
+    if (r0 + SVDV_BATCH < rounds) load(r0 + SVDV_BATCH);
+#pragma unroll
+    for (int b = 0; b < SVDV_BATCH; ++b) {
+      if (r0 + b >= rounds) break;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (lane + 32 * k < half) {
+          const int p = min(plo[k], phi[k]), q = max(plo[k], phi[k]);
+          const double c = cs[b][k].x, s = cs[b][k].y;
+          const double u = row[p], w = row[q];
+          row[p] = c * u - s * w;
+          row[q] = s * u + c * w;
+          plo[k] = plo[k] == 0 ? 0 : (plo[k] == np - 1 ? 1 : plo[k] + 1);
+          phi[k] = phi[k] == np - 1 ? 1 : phi[k] + 1;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  for (int j = lane; j < np; j += 32) {
+    const double sj = sig[j];
+    int rk = 0;
+    for (int k = 0; k < np; ++k) rk += (sig[k] > sj) || (sig[k] == sj && k < j);
+    if (rk < n_out) vout[(size_t)i * n_out + rk] = row[j];
+  }
+}
+
 // A_cm[j*np + i] = R[i*n + j] (zero padded to np), V = I
 __global__ void svd_init_kernel(const double* __restrict__ r, int n, int np, double* __restrict__ A,
                                 double* __restrict__ V) {
@@ -241,13 +490,78 @@ __global__ void svd_init_kernel(const double* __restrict__ r, int n, int np, dou
 }
 
 size_t svd_ws_bytes(int64_t n) {
-  const int64_t np = n + (n & 1);
-  return 2 * ws_bytes(size_t(np) * np, 8) + ws_bytes(512, 8) + ws_bytes(128, 4);
+  const int64_t np = (n + 31) / 32 * 32;  // covers both paths' padding
+  return 2 * ws_bytes(size_t(np) * np, 8) + ws_bytes(512, 8) + ws_bytes(128, 4) + ws_bytes(256, 8) +
+         ws_bytes(4, 4) + ws_bytes(size_t(SVD_MAX_SWEEPS) * std::max<int64_t>(np - 1, 1) * (np / 2), 16);
+}
+
+// one cluster over the np/2 pairs: 8 warps per CTA (a 16-CTA cluster at np = 256, opt-in
+// non-portable size), else 16 warps per CTA when the device refuses clusters above 8
+template <int WPC>
+static int launch_cluster_wpc(jq_ctx* ctx, const double* A, int np, double* sig, double2* rlog, int* nsw,
+                              double* values, int n_out) {
+  auto kern = jacobi_cluster_kernel<WPC>;
+  const int nct = (np / 2 + WPC - 1) / WPC;
+  const size_t smem = size_t(2) * 2 * WPC * np * sizeof(double) + size_t(np - 1) * WPC * sizeof(double2);
+  JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (nct > 8) JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nct);
+  cfg.blockDim = dim3(WPC * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = nct;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
+    cudaGetLastError();
+    return -1;  // not launchable with this shape
+  }
+  const double tol = 1e-14;
+  JQ_CUDA(cudaLaunchKernelEx(&cfg, kern, A, np, tol, SVD_MAX_SWEEPS, ctx->d_flags, sig, rlog, nsw, values, n_out));
+  JQ_CHECK_LAUNCH(ctx);
+  return JQ_OK;
+}
+
+static int launch_jacobi_cluster(jq_ctx* ctx, const double* A, int np, double* sig, double2* rlog, int* nsw,
+                                 double* values, int n_out) {
+  int rc = launch_cluster_wpc<8>(ctx, A, np, sig, rlog, nsw, values, n_out);
+  if (rc == -1) rc = launch_cluster_wpc<16>(ctx, A, np, sig, rlog, nsw, values, n_out);
+  if (rc == -1) return fail(JQ_E_CUDA, "no cluster shape is launchable for the Jacobi SVD");
+  return rc;
 }
 
 int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values, double* v) {
   if (n > 256) return fail(JQ_E_INVALID, "svd_of_r supports n <= 256");
   if (n == 0) return JQ_OK;
+  static const bool coop = [] {  // JQ_SVD_IMPL=coop: the grid-barrier kernel (A/B tests)
+    const char* e = getenv("JQ_SVD_IMPL");
+    return e && strcmp(e, "coop") == 0;
+  }();
+  if (n >= 31 && !coop) {
+    // cluster path: zero columns pad the tournament to a multiple of 32 (never rotated,
+    // sigma 0, ranked after every real column)
+    const int npc = (int)((n + 31) / 32 * 32);
+    double* A = ws_alloc<double>(ctx, size_t(npc) * npc);
+    double* sig = ws_alloc<double>(ctx, 256);
+    int* nsw = ws_alloc<int>(ctx, 4);
+    double2* rlog = ws_alloc<double2>(ctx, size_t(SVD_MAX_SWEEPS) * (npc - 1) * (npc / 2));
+    if (!A || !sig || !nsw || !rlog) return fail(JQ_E_OOM, "workspace exhausted (svd)");
+    svd_init_kernel<<<(unsigned)cdiv(int64_t(npc) * npc, 256), 256, 0, ctx->stream>>>(r, (int)n, npc, A, nullptr);
+    JQ_CHECK_LAUNCH(ctx);
+    JQ_TRY(launch_jacobi_cluster(ctx, A, npc, sig, rlog, nsw, values, (int)n));
+    if (want_v) {
+      jacobi_v_kernel<<<(unsigned)cdiv(n, SVDV_WARPS), SVDV_WARPS * 32, 0, ctx->stream>>>(rlog, nsw, npc, sig, v,
+                                                                                        (int)n);
+      JQ_CHECK_LAUNCH(ctx);
+    }
+    return JQ_OK;
+  }
   const int np = (int)(n + (n & 1));  // the tournament needs an even count; pad a zero column
   double* A = ws_alloc<double>(ctx, size_t(np) * np);
   double* V = ws_alloc<double>(ctx, size_t(np) * np);

@@ -1,4 +1,4 @@
-"""The TSQR leaf kernel has several paths (warp-specialised default, CTA-wide,
+"""The TSQR leaf kernel and the Jacobi SVD have several paths (warp-specialised default, CTA-wide,
 explicit-panel fallback forced, warp roles assigned without %warpid) selected by
 environment variables that the library reads once per process; each is checked in a
 subprocess against the same parity tests."""
@@ -21,5 +21,15 @@ def test_leaf_impl_parity(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "figaro or householder or shard"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_svd_coop_impl_parity():
+    # JQ_SVD_IMPL=coop: the grid-barrier Jacobi kernel instead of the cluster kernel
+    e = dict(os.environ, JQ_SVD_IMPL="coop")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "svd"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -222,6 +222,21 @@ def test_svd_rank_deficient_and_zero(P):
     assert np.max(np.abs(s.values - ref)) <= 1e-10 * ref[0]
 
 
+@pytest.mark.parametrize("n", [40, 200, 256])
+def test_svd_rank_deficient_cluster(P, n):
+    # rank n/2: half the columns go numerically to zero and are never rotated again
+    rng = np.random.default_rng(100 + n)
+    m = rng.standard_normal((2 * n, n // 2)) @ rng.standard_normal((n // 2, n))
+    r = np.linalg.qr(m, mode="r")
+    s = P.svd_of_r(r, True)
+    ref = np.linalg.svd(r, compute_uv=False)
+    assert np.max(np.abs(s.values - ref)) <= 1e-10 * ref[0]
+    v = np.asarray(s.right_vectors)
+    assert np.abs(v.T @ v - np.eye(n)).max() <= 1e-10
+    rec = v @ np.diag(s.values ** 2) @ v.T
+    assert np.abs(r.T @ r - rec).max() <= 1e-8 * s.values[0] ** 2
+
+
 @pytest.mark.parametrize("m,n,groups", [(1000, 4, None), (3000, 16, None), (5000, 64, None), (4000, 16, 300)])
 def test_figaro_svd_matches_oracle(P, variant, m, n, groups):
     rng = np.random.default_rng(m + n)
