@@ -131,6 +131,74 @@ __global__ void footnote_stack_kernel(const double* __restrict__ rh, const doubl
   }
 }
 
+// blockdiag(R_A, R_B) (n x n): the two tail factors already form an upper-triangular R
+__global__ void blockdiag_kernel(const double* __restrict__ ra, int n1, const double* __restrict__ rb, int n2,
+                                 double* __restrict__ out) {
+  const int n = n1 + n2;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * n; idx += gridDim.x * blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    out[idx] = (r < n1 && c < n1) ? ra[r * n1 + c] : (r >= n1 && c >= n1) ? rb[(r - n1) * n2 + (c - n1)] : 0.0;
+  }
+}
+
+// Absorb `count` rows (row-major count x n) into the upper-triangular R (n x n, row-major,
+// in place) by Givens rotations, row after row, column j of the row zeroed against R[j][j]
+// (one CTA, thread = column; row j + 1 of R is fetched while step j runs).  For the few
+// head rows of the footnote variant (one for a Cartesian product) this replaces the
+// head-row TSQR and the 3-factor stack (two NP x NP combines).
+constexpr int GIVENS_THREADS = 256;
+__global__ void __launch_bounds__(GIVENS_THREADS) givens_absorb_kernel(double* __restrict__ R,
+                                                                       const double* __restrict__ rows, int count,
+                                                                       int n) {
+  __shared__ double w[GIVENS_THREADS];
+  __shared__ double rot[2];
+  const int k = threadIdx.x;
+  for (int row = 0; row < count; ++row) {
+    if (k < n) w[k] = rows[(size_t)row * n + k];
+    double rj = k < n ? R[k] : 0.0;  // R[0][k]
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+      const double rnext = (j + 1 < n && k < n) ? R[(size_t)(j + 1) * n + k] : 0.0;
+      if (k == j) {
+        const double a = rj, b = w[j];
+        double c = 1.0, s = 0.0;
+        if (b != 0.0) {
+          const double r = hypot(a, b);
+          c = a / r;
+          s = b / r;
+        }
+        rot[0] = c;
+        rot[1] = s;
+      }
+      __syncthreads();
+      if (k >= j && k < n) {
+        const double c = rot[0], s = rot[1], wk = w[k];
+        R[(size_t)j * n + k] = fma(c, rj, s * wk);
+        w[k] = k == j ? 0.0 : fma(-s, rj, c * wk);
+      }
+      rj = rnext;
+      __syncthreads();
+    }
+  }
+}
+
+// R from blockdiag(R_A, R_B) and `ng` head rows (few): blockdiag, then Givens.
+static int footnote_small_head(jq_ctx* ctx, const double* ra, int64_t n1, const double* rb, int64_t n2,
+                               const double* heads, int64_t ng, bool canonical, double* tmp, double* r_out) {
+  const int64_t n = n1 + n2;
+  double* R = canonical ? tmp : r_out;
+  blockdiag_kernel<<<(unsigned)cdiv(n * n, 256), 256, 0, ctx->stream>>>(n1 > 0 ? ra : nullptr, (int)n1,
+                                                                        n2 > 0 ? rb : nullptr, (int)n2, R);
+  JQ_CHECK_LAUNCH(ctx);
+  if (ng > 0) {
+    givens_absorb_kernel<<<1, GIVENS_THREADS, 0, ctx->stream>>>(R, heads, (int)ng, (int)n);
+    JQ_CHECK_LAUNCH(ctx);
+  }
+  if (canonical) JQ_TRY(canonicalize_dev(ctx, R, n, r_out));
+  return JQ_OK;
+}
+constexpr int64_t FOOTNOTE_GIVENS_MAX_HEADS = 8;
+
 static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
                                  const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
   const bool keyed = ka != nullptr;
@@ -147,13 +215,14 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   }
   cudaEventRecord(ctx->ev[1], ctx->stream);
   const int64_t cap = keyed ? gr.cap : 1;
+  // A's scan in full; the tile pass of B's scan (the HBM-heavy part) runs on the spare
+  // warps of A's TSQR leaf (FigaroArgs::side), B's carries right after it
   SegScan sa{}, sb{};
+  SideScan side_b;
   if (n1 > 0)
     JQ_TRY(segscan_dev(ctx, a, m1, n1, keyed ? gr.gid_a : nullptr, keyed ? gr.a_start : nullptr,
                        keyed ? gr.a_count : nullptr, keyed ? gr.d_n : nullptr, cap, &sa));
-  if (n2 > 0)
-    JQ_TRY(segscan_dev(ctx, b, m2, n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
-                       keyed ? gr.b_count : nullptr, keyed ? gr.d_n : nullptr, cap, &sb));
+  if (n2 > 0) JQ_TRY(segscan_begin(ctx, b, m2, n2, keyed ? gr.gid_b : nullptr, cap, &sb, &side_b));
   cudaEventRecord(ctx->ev[2], ctx->stream);
   double* ra = ws_alloc<double>(ctx, std::max<int64_t>(n1 * n1, 1));
   double* rb = ws_alloc<double>(ctx, std::max<int64_t>(n2 * n2, 1));
@@ -174,10 +243,16 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     fa.a_count = keyed ? gr.b_count : nullptr;
     fa.b_carry = sa.carry;
     fa.m1_global = m2; fa.m2_global = m1; fa.b_row0 = 0;
+    fa.side = side_b;
     int rc = figaro_tsqr_dev(ctx, fa, ra, false);
     if (rc) { ctx->record_tsqr_events = true; return rc; }
+  } else {
+    JQ_TRY(segscan_tiles(ctx, side_b));
   }
   if (n2 > 0) {
+    int rc = segscan_end(ctx, keyed ? gr.b_start : nullptr, keyed ? gr.b_count : nullptr, keyed ? gr.d_n : nullptr,
+                         cap, &sb);
+    if (rc) { ctx->record_tsqr_events = true; return rc; }
     FigaroArgs fb{};
     fb.b = b; fb.m2 = m2; fb.n2 = n2;
     fb.gid_b = keyed ? gr.gid_b : nullptr;
@@ -185,13 +260,23 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     fb.a_count = keyed ? gr.a_count : nullptr;
     fb.b_carry = sb.carry;
     fb.m1_global = m1; fb.m2_global = m2; fb.b_row0 = 0;
-    int rc = figaro_tsqr_dev(ctx, fb, rb, false);
+    rc = figaro_tsqr_dev(ctx, fb, rb, false);
     if (rc) { ctx->record_tsqr_events = true; return rc; }
   }
   cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (ng <= FOOTNOTE_GIVENS_MAX_HEADS) {
+    if (ng > 0) {
+      head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng * n, 256), 4096), 256, 0, ctx->stream>>>(
+          sa.totals, (int)n1, sb.totals, (int)n2, keyed ? gr.a_count : nullptr, keyed ? gr.b_count : nullptr,
+          ng, m1, m2, heads);
+      JQ_CHECK_LAUNCH(ctx);
+    }
+    const int rc = footnote_small_head(ctx, ra, n1, rb, n2, heads, ng, true, rh, r_out);
+    ctx->record_tsqr_events = true;
+    cudaEventRecord(ctx->ev[5], ctx->stream);
+    return rc;
+  }
   // head rows (G x n) -> R_H, then the final 3-factor stack -> canonical R
-  const double* zeros_dummy = nullptr;
-  (void)zeros_dummy;
   if (ng > 0) {
     head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng * n, 256), 4096), 256, 0, ctx->stream>>>(
         sa.totals, (int)n1, sb.totals, (int)n2, keyed ? gr.a_count : nullptr, keyed ? gr.b_count : nullptr,
@@ -234,15 +319,15 @@ static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int6
                               const double* b_total, bool include_head, double* r_out) {
   const int64_t n = n1 + n2;
   SegScan sa{}, sb{};
+  SideScan side_b;  // B's tile pass on the spare warps of A's leaf (as in figaro_r_footnote_dev)
   if (n1 > 0) JQ_TRY(segscan_dev(ctx, a, a_rows, n1, nullptr, nullptr, nullptr, nullptr, 1, &sa));
-  if (n2 > 0) JQ_TRY(segscan_dev(ctx, b, b_rows, n2, nullptr, nullptr, nullptr, nullptr, 1, &sb));
+  if (n2 > 0) JQ_TRY(segscan_begin(ctx, b, b_rows, n2, nullptr, 1, &sb, &side_b));
   cudaEventRecord(ctx->ev[2], ctx->stream);
   double* ra = ws_alloc<double>(ctx, std::max<int64_t>(n1 * n1, 1));
   double* rb = ws_alloc<double>(ctx, std::max<int64_t>(n2 * n2, 1));
   double* rh = ws_alloc<double>(ctx, n * n);
-  double* stack = ws_alloc<double>(ctx, 3 * n * n);
   double* heads = ws_alloc<double>(ctx, n);
-  if (!ra || !rb || !rh || !stack || !heads) return fail(JQ_E_OOM, "workspace exhausted (footnote shard)");
+  if (!ra || !rb || !rh || !heads) return fail(JQ_E_OOM, "workspace exhausted (footnote shard)");
   ctx->record_tsqr_events = false;
   cudaEventRecord(ctx->ev[3], ctx->stream);
   int rc = JQ_OK;
@@ -251,8 +336,12 @@ static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int6
     fa.b = a; fa.m2 = a_rows; fa.n2 = n1;
     fa.b_carry = sa.carry; fa.b_prefix0 = a_prefix;
     fa.m1_global = m2; fa.m2_global = m1; fa.b_row0 = a_row0;
+    fa.side = side_b;
     rc = figaro_tsqr_dev(ctx, fa, ra, false);
+  } else {
+    rc = segscan_tiles(ctx, side_b);
   }
+  if (!rc && n2 > 0) rc = segscan_end(ctx, nullptr, nullptr, nullptr, 1, &sb);
   if (!rc && n2 > 0) {
     FigaroArgs fb{};
     fb.b = b; fb.m2 = b_rows; fb.n2 = n2;
@@ -263,18 +352,13 @@ static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int6
   ctx->record_tsqr_events = true;
   if (rc) return rc;
   cudaEventRecord(ctx->ev[4], ctx->stream);
+  // one head row at most: blockdiag(R_A, R_B) plus a Givens absorb of the head row
   if (include_head) {
     head_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(a_total, (int)n1, b_total, (int)n2, nullptr,
                                                                         nullptr, 1, m1, m2, heads);
     JQ_CHECK_LAUNCH(ctx);
-    JQ_TRY(tsqr_dense_dev(ctx, heads, 1, n, rh, false));
-  } else {
-    JQ_CUDA(cudaMemsetAsync(rh, 0, n * n * 8, ctx->stream));
   }
-  footnote_stack_kernel<<<(unsigned)cdiv(3 * n * n, 256), 256, 0, ctx->stream>>>(
-      rh, n1 > 0 ? ra : nullptr, (int)n1, n2 > 0 ? rb : nullptr, (int)n2, stack);
-  JQ_CHECK_LAUNCH(ctx);
-  rc = tsqr_stack_dev(ctx, stack, 3, n, r_out, false);
+  rc = footnote_small_head(ctx, ra, n1, rb, n2, heads, include_head ? 1 : 0, false, rh, r_out);
   cudaEventRecord(ctx->ev[5], ctx->stream);
   return rc;
 }

@@ -17,142 +17,20 @@
 #include <cmath>
 
 #include "jq_internal.cuh"
+#include "jq_segscan.cuh"
 
 namespace jq {
 
 constexpr int MAXC = 8;  // columns per lane (cols <= 256)
 
-// One warp per TILE_ROWS tile.  Segment id of row r: gid[r] (or 0 when gid is
-// null = one segment).  Writes agg[t] (sum of the segment open at the tile end,
-// restricted to the tile), flag[t] (tile contains a segment start) and, for each
-// segment that ends inside the tile, its in-tile partial sum into totals[seg].
+// One warp per TILE_ROWS tile (segscan_tile, jq_segscan.cuh).
 __global__ void __launch_bounds__(256) segscan_tile_kernel(
     const double* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ gid,
     int64_t ntiles, double* __restrict__ agg, int* __restrict__ flag, double* __restrict__ totals) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= ntiles) return;
-  const int64_t r0 = t * TILE_ROWS, r1 = min(rows, r0 + TILE_ROWS);
-  double s[MAXC];
-#pragma unroll
-  for (int k = 0; k < MAXC; ++k) s[k] = 0.0;
-  if (!gid && cols <= 64) {
-    // one segment (Cartesian): plain column sums, 4 rows in flight per lane and
-    // a fixed-order combine (deterministic); the segment starts at global row 0
-    double a[2][4];
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) a[k][u] = 0.0;
-    const bool h0 = lane < cols, h1 = lane + 32 < cols;
-    int64_t r = r0;
-    for (; r + 4 <= r1; r += 4) {
-      double v[2][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double* row = x + (r + u) * cols;
-        v[0][u] = h0 ? __ldg(row + lane) : 0.0;
-        v[1][u] = h1 ? __ldg(row + lane + 32) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { a[0][u] += v[0][u]; a[1][u] += v[1][u]; }
-    }
-    for (; r < r1; ++r) {
-      const double* row = x + r * cols;
-      if (h0) a[0][0] += __ldg(row + lane);
-      if (h1) a[1][0] += __ldg(row + lane + 32);
-    }
-    s[0] = (a[0][0] + a[0][1]) + (a[0][2] + a[0][3]);
-    s[1] = (a[1][0] + a[1][1]) + (a[1][2] + a[1][3]);
-    if (r1 == rows) {
-      if (h0) totals[lane] = s[0];
-      if (h1) totals[lane + 32] = s[1];
-    }
-    if (h0) agg[t * cols + lane] = s[0];
-    if (h1) agg[t * cols + lane + 32] = s[1];
-    if (lane == 0) flag[t] = r0 == 0;
-    return;
-  }
-  int seg = gid ? gid[r0] : 0;
-  int any_start = (r0 == 0) || (gid && gid[r0 - 1] != seg);
-  if (gid && cols <= 64) {
-    // keyed, <= 64 columns: the loads of 4 rows are issued before their sequential
-    // segment logic (same additions in the same order as the generic loop below)
-    const bool h0 = lane < cols, h1 = lane + 32 < cols;
-    double s0 = 0.0, s1 = 0.0;
-    int64_t r = r0;
-    auto row_step = [&](int64_t rr, int sr, double v0, double v1) {
-      const bool start = (rr == 0) || (rr > r0 && sr != seg);
-      if (start && rr > r0) {
-        if (seg >= 0) {
-          if (h0) totals[(int64_t)seg * cols + lane] = s0;
-          if (h1) totals[(int64_t)seg * cols + lane + 32] = s1;
-        }
-        any_start = 1;
-      }
-      seg = sr;
-      s0 = start ? v0 : s0 + v0;
-      s1 = start ? v1 : s1 + v1;
-    };
-    for (; r + 4 <= r1; r += 4) {
-      int g4[4];
-      double v[2][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        g4[u] = gid[r + u];
-        const double* row = x + (r + u) * cols;
-        v[0][u] = h0 ? __ldg(row + lane) : 0.0;
-        v[1][u] = h1 ? __ldg(row + lane + 32) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) row_step(r + u, g4[u], v[0][u], v[1][u]);
-    }
-    for (; r < r1; ++r) {
-      const double* row = x + r * cols;
-      row_step(r, gid[r], h0 ? __ldg(row + lane) : 0.0, h1 ? __ldg(row + lane + 32) : 0.0);
-    }
-    const bool ends_here = (r1 == rows) || (gid[r1] != seg);
-    if (ends_here && seg >= 0) {
-      if (h0) totals[(int64_t)seg * cols + lane] = s0;
-      if (h1) totals[(int64_t)seg * cols + lane + 32] = s1;
-    }
-    if (h0) agg[t * cols + lane] = s0;
-    if (h1) agg[t * cols + lane + 32] = s1;
-    if (lane == 0) flag[t] = any_start;
-    return;
-  }
-  for (int64_t r = r0; r < r1; ++r) {
-    const int sr = gid ? gid[r] : 0;
-    const bool start = (r == 0) || (r > r0 && sr != seg);
-    if (start && r > r0) {
-      // previous segment ended at r-1 inside this tile
-      if (seg >= 0)
-#pragma unroll
-        for (int k = 0; k < MAXC; ++k)
-          if (k * 32 + lane < cols) totals[(int64_t)seg * cols + k * 32 + lane] = s[k];
-      any_start = 1;
-    }
-    seg = sr;
-    const double* row = x + r * cols;
-#pragma unroll
-    for (int k = 0; k < MAXC; ++k) {
-      const int c = k * 32 + lane;
-      if (c < cols) {
-        const double v = __ldg(row + c);
-        s[k] = start ? v : s[k] + v;
-      }
-    }
-  }
-  // open segment at the tile end
-  const bool ends_here = (r1 == rows) || (gid && gid[r1] != seg) ;
-  if (ends_here && seg >= 0)
-#pragma unroll
-    for (int k = 0; k < MAXC; ++k)
-      if (k * 32 + lane < cols) totals[(int64_t)seg * cols + k * 32 + lane] = s[k];
-#pragma unroll
-  for (int k = 0; k < MAXC; ++k)
-    if (k * 32 + lane < cols) agg[t * cols + k * 32 + lane] = s[k];
-  if (lane == 0) flag[t] = any_start;
+  segscan_tile(x, rows, cols, gid, t, agg, flag, totals, lane);
 }
 
 // Segmented carry over tiles, two-level with FIXED association (deterministic):
@@ -231,11 +109,15 @@ size_t segscan_ws_bytes(int64_t rows, int64_t cols, int64_t groups_cap) {
          ws_bytes(size_t(std::max<int64_t>(groups_cap, 1)) * cols, 8);
 }
 
-int segscan_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int32_t* gid,
-                const int64_t* gstart, const int64_t* gcount, const int64_t* d_ngroups,
-                int64_t groups_cap, SegScan* s) {
+// The scan in three steps, so the tile pass (the only HBM-heavy one) can run inside
+// another kernel (SideScan): begin = workspace + zeroed totals, tiles = the tile pass,
+// end = the carry scan over tiles and the fix-up of groups that span tiles.
+int segscan_begin(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int32_t* gid,
+                  int64_t groups_cap, SegScan* s, SideScan* side) {
   if (cols > 32 * MAXC) return fail(JQ_E_INVALID, "more than 256 columns per table");
   s->ntiles = std::max<int64_t>(1, cdiv(rows, TILE_ROWS));
+  s->rows = rows;
+  s->cols = cols;
   s->carry = ws_alloc<double>(ctx, size_t(s->ntiles) * cols);
   s->tile_agg = ws_alloc<double>(ctx, size_t(s->ntiles) * cols);
   s->tile_flag = ws_alloc<int>(ctx, s->ntiles);
@@ -243,14 +125,35 @@ int segscan_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const 
   if (!s->carry || !s->tile_agg || !s->tile_flag || !s->totals)
     return fail(JQ_E_OOM, "workspace exhausted (head/tail scan)");
   JQ_CUDA(cudaMemsetAsync(s->totals, 0, size_t(std::max<int64_t>(groups_cap, 1)) * cols * 8, ctx->stream));
+  *side = SideScan{};
   if (rows == 0) {
     JQ_CUDA(cudaMemsetAsync(s->carry, 0, size_t(s->ntiles) * cols * 8, ctx->stream));
     return JQ_OK;
   }
+  side->x = x;
+  side->rows = rows;
+  side->cols = (int)cols;
+  side->gid = gid;
+  side->ntiles = s->ntiles;
+  side->agg = s->tile_agg;
+  side->flag = s->tile_flag;
+  side->totals = s->totals;
+  return JQ_OK;
+}
+
+int segscan_tiles(jq_ctx* ctx, const SideScan& side) {
+  if (!side.x || side.ntiles == 0) return JQ_OK;
   const int wpb = 8;
-  segscan_tile_kernel<<<(unsigned)cdiv(s->ntiles, wpb), 32 * wpb, 0, ctx->stream>>>(
-      x, rows, (int)cols, gid, s->ntiles, s->tile_agg, s->tile_flag, s->totals);
+  segscan_tile_kernel<<<(unsigned)cdiv(side.ntiles, wpb), 32 * wpb, 0, ctx->stream>>>(
+      side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
   JQ_CHECK_LAUNCH(ctx);
+  return JQ_OK;
+}
+
+int segscan_end(jq_ctx* ctx, const int64_t* gstart, const int64_t* gcount, const int64_t* d_ngroups,
+                int64_t groups_cap, SegScan* s) {
+  if (s->rows == 0) return JQ_OK;
+  const int64_t cols = s->cols;
   {
     const int64_t nblk = cdiv(s->ntiles, CB);
     double* bagg = ws_alloc<double>(ctx, size_t(nblk) * cols);
@@ -266,10 +169,19 @@ int segscan_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const 
     JQ_CHECK_LAUNCH(ctx);
   }
   group_fixup_kernel<<<(unsigned)std::min<int64_t>(cdiv(std::max<int64_t>(groups_cap, 1) * cols, 256), 4096),
-                       256, 0, ctx->stream>>>(gstart, gcount, d_ngroups, rows, (int)cols, s->carry,
+                       256, 0, ctx->stream>>>(gstart, gcount, d_ngroups, s->rows, (int)cols, s->carry,
                                               s->totals);
   JQ_CHECK_LAUNCH(ctx);
   return JQ_OK;
+}
+
+int segscan_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int32_t* gid,
+                const int64_t* gstart, const int64_t* gcount, const int64_t* d_ngroups,
+                int64_t groups_cap, SegScan* s) {
+  SideScan side;
+  JQ_TRY(segscan_begin(ctx, x, rows, cols, gid, groups_cap, s, &side));
+  JQ_TRY(segscan_tiles(ctx, side));
+  return segscan_end(ctx, gstart, gcount, d_ngroups, groups_cap, s);
 }
 
 // ------------------------------------------------------------------ emit kernels

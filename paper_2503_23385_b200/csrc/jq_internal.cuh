@@ -180,12 +180,30 @@ int group_keys_dev(jq_ctx* ctx, const int64_t* ka, int64_t m1, const int64_t* kb
 constexpr int TILE_ROWS = 1024;
 struct SegScan {
   int64_t ntiles = 0;
+  int64_t rows = 0, cols = 0;
   double* carry = nullptr;   // ntiles x cols
   double* tile_agg = nullptr;
   int* tile_flag = nullptr;
   double* totals = nullptr;  // ngroups_cap x cols (group sums)
 };
+// The tile pass of a segmented scan as a job description: run by segscan_tiles, or by
+// the spare warps of a TSQR leaf (FigaroArgs::side) while it factors the other side.
+struct SideScan {
+  const double* x = nullptr;  // nullptr: nothing to do
+  int64_t rows = 0;
+  int cols = 0;
+  const int32_t* gid = nullptr;
+  int64_t ntiles = 0;
+  double* agg = nullptr;
+  int* flag = nullptr;
+  double* totals = nullptr;
+};
 size_t segscan_ws_bytes(int64_t rows, int64_t cols, int64_t groups_cap);
+int segscan_begin(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int32_t* gid,
+                  int64_t groups_cap, SegScan* s, SideScan* side);
+int segscan_tiles(jq_ctx* ctx, const SideScan& side);
+int segscan_end(jq_ctx* ctx, const int64_t* gstart, const int64_t* gcount, const int64_t* d_ngroups,
+                int64_t groups_cap, SegScan* s);
 int segscan_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int32_t* gid,
                 const int64_t* gstart, const int64_t* gcount, const int64_t* d_ngroups,
                 int64_t groups_cap, SegScan* s);
@@ -216,6 +234,7 @@ struct FigaroArgs {
   const double* b_prefix0;       // shard: sum of B rows before this shard (n2), or nullptr
   // Cartesian shard extras (jq_figaro_r_shard): global sizes and row offset of B
   int64_t m1_global, m2_global, b_row0;
+  SideScan side;                 // tile pass of another scan to run alongside (or nothing)
 };
 int figaro_tsqr_dev(jq_ctx* ctx, const FigaroArgs& fa, double* r_out, bool canonical);
 size_t figaro_tsqr_ws_bytes(int64_t m1, int64_t m2, int64_t n, int sms);

@@ -42,6 +42,7 @@
 #include <cstdlib>
 
 #include "jq_internal.cuh"
+#include "jq_segscan.cuh"
 
 namespace jq {
 
@@ -140,6 +141,8 @@ struct DenseSrc {
   template <class C>
   __device__ void seg_pass2(double*, double*, const double*, const double*, double, double, int64_t, int, int, int,
                             int, int, int) const {}
+  SideScan side_job() const { return SideScan{}; }
+  __device__ void side_scan(int, int, int) const {}
 };
 
 struct FigaroSrc {
@@ -159,6 +162,15 @@ struct FigaroSrc {
       if (fa.b_prefix0) s += fa.b_prefix0[c];
       S[c] = s;
     }
+  }
+  // the tile pass of another segmented scan (fa.side), run by the leaf's spare warps:
+  // spare warp si of nsp per CTA takes tiles blockIdx.x * nsp + si, strided by the grid
+  SideScan side_job() const { return fa.side; }
+  __device__ void side_scan(int si, int nsp, int lane) const {
+    const SideScan& sd = fa.side;
+    if (!sd.x) return;
+    for (int64_t t = (int64_t)blockIdx.x * nsp + si; t < sd.ntiles; t += (int64_t)gridDim.x * nsp)
+      segscan_tile(sd.x, sd.rows, sd.cols, sd.gid, t, sd.agg, sd.flag, sd.totals, lane);
   }
   __device__ int rc(int64_t v0) const { return v0 < m1pad ? (int)fa.n1 : (int)fa.n2; }
   __device__ const double* ptr(int64_t v0) const {
@@ -1278,6 +1290,7 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   ctx->timing.tsqr_ctas += leaves;
   ctx->timing.reduced_rows += vrows;
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
+  JQ_TRY(segscan_tiles(ctx, src.side_job()));  // this leaf has no spare warps for it
   JQ_TRY((launch_tsqr<C, Src, false>(ctx, (int)leaves, src, rows_per_cta, vrows, nullptr, 0, a, use_tma)));
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
   double* fin = nullptr;
@@ -1333,6 +1346,7 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
   ctx->timing.tsqr_ctas += ctas;
   ctx->timing.reduced_rows += vrows;
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
+  if (CS::NSPARE == 0) JQ_TRY(segscan_tiles(ctx, src.side_job()));  // else the spare warps run it
   auto kern = tsqr_ws2_kernel<CS, Src>;
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM));
   kern<<<(int)ctas, CS::THREADS, CS::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a,

@@ -63,6 +63,7 @@ struct CfgS {
   static constexpr int OFF_GD = OFF_GP + DW * 64;         // [DW][64] direct Gram partials (ws2)
   static constexpr int NLOAD = NP <= 32 ? 3 : 1;  // loader warps: narrow leaves are loader-bound; at
   // NP = 64 two extra active warps on SMSP 0 slow the chain more than they help (4.62 vs 4.47 ms)
+  static constexpr int NSPARE = WARPS - 1 - NLOAD - DW;  // spare warps: the side scan (FigaroSrc::side_scan)
   static constexpr int OFF_LSR = OFF_GD + DW * 64;        // [NLOAD][2][64] loader segment sums
   static constexpr int OFF_ROLE = OFF_LSR + NLOAD * 128;  // WARPS ints: SMSP of each warp
   static constexpr int OFF_BAR = OFF_ROLE + WARPS / 2;    // mbarriers: TMA, READY, FREE, VREADY
@@ -178,7 +179,22 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       ++k;
     }
   }
-  if (warp != chain_w && li < 0 && d < 0) return;
+  if (warp != chain_w && li < 0 && d < 0) {
+    // spare warp: the tile pass of the other side's scan, if the host attached one
+    int si = 0, zc = 0, dk = 0;
+    for (int w = 0; w < warp; ++w) {
+      bool busy;
+      if (mapped) {
+        busy = role[w] == 0 ? zc <= C::NLOAD : dk < C::DW;
+        if (role[w] == 0) ++zc; else ++dk;
+      } else {
+        busy = w < 1 + C::NLOAD + C::DW;
+      }
+      si += busy ? 0 : 1;
+    }
+    src.side_scan(si, C::NSPARE, lane);
+    return;
+  }
 
   auto chunk_end = [&](int64_t r0) -> int64_t {
     int64_t e = r0 + C::K < row_end ? r0 + C::K : row_end;

@@ -172,7 +172,12 @@ def variant(request, P):
     (1000, 4, 1000, 4, None), (3000, 8, 2000, 8, None), (4000, 32, 5000, 32, None),
     (2500, 64, 2500, 64, None), (3000, 100, 2000, 120, None), (5000, 128, 4000, 128, None),
     (400, 5, 300, 6, 40), (6000, 16, 7000, 16, 600), (20000, 32, 20000, 32, 100),
-    (3000, 7, 2000, 3, 2500)])
+    (3000, 7, 2000, 3, 2500),
+    # footnote: B's scan tiles on the spare warps of A's leaf (33..64 columns), a B side
+    # with many more tiles than A has spare warps, keyed groups spanning tiles
+    (2000, 50, 50000, 60, None), (3000, 40, 40000, 56, 30), (30000, 48, 25000, 40, 70),
+    # footnote with few join groups: head rows absorbed by Givens rotations
+    (5000, 20, 4000, 24, 3), (3000, 100, 3000, 120, 5)])
 def test_figaro_r_matches_oracle(P, variant, m1, n1, m2, n2, groups):
     rng = np.random.default_rng(m1 + 3 * m2 + n1 + (groups or 0))
     a, b = rand_tables(rng, m1, n1, m2, n2, groups)
