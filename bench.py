@@ -44,9 +44,10 @@ CONFIGS = {
 }
 METRIC = "join rows/sec (m1*m2/t), time-to-R"
 # dram__bytes_read.sum + dram__bytes_write.sum per leaf-kernel launch (ncu --set full)
-NCU_TRAFFIC = {(4, "footnote"): {"bytes": 51.224204e9 + 14.270464e6,
-                                 "note": "per tsqr_ws2_kernel launch (one side, 1e8 x 64 f64 = 51.2e9 algorithmic "
-                                         "bytes): no re-reads; profiles/r01_ncu_ws2_c4.md"}}
+NCU_TRAFFIC = {(4, "footnote"): {"bytes": 102.441363e9 + 113.473024e6,
+                                 "note": "first tsqr_ws2_kernel launch (side A, capture v10): its own 1e8 x 64 f64 "
+                                         "rows (51.2e9 algorithmic bytes) + side B's scan tile pass on the spare "
+                                         "warps (51.2e9): every byte read once; profiles/r01_ncu_ws2_c4.md"}}
 
 
 def peaks():
@@ -334,7 +335,9 @@ def main():
                 "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 figure",
                 "algorithmic": alg, "share_of_step": stage_avg["tsqr_ms"] / ms}
         pk = peaks()
-        sides = 2 if args.variant == "footnote" else 1
+        # one side in the scan interval: dense scans B only (Claim 1); footnote scans A there
+        # and runs B's tile pass inside A's TSQR interval (spare warps of the leaf)
+        sides = 1
         gbs = (8.0 * m * n * sides) / (stage_avg["scan_ms"] / 1e3) / 1e9 if stage_avg["scan_ms"] > 0 else None
         if gbs:
             roof_hbm = {"kernel": "segscan (head/tail prefix pass, tile sums + carry scan)", "bound": "hbm",

@@ -117,16 +117,15 @@ __global__ void head_rows_kernel(const double* __restrict__ totA, int n1, const 
   }
 }
 
-// stack [R_H ; R_A (top-left) ; R_B (bottom-right)] as three n x n factors
+// [blockdiag(R_A, R_B); R_H]: two n x n factors (the first already upper triangular)
 __global__ void footnote_stack_kernel(const double* __restrict__ rh, const double* __restrict__ ra, int n1,
                                       const double* __restrict__ rb, int n2, double* __restrict__ out) {
   const int n = n1 + n2;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 3 * n * n; idx += gridDim.x * blockDim.x) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * n * n; idx += gridDim.x * blockDim.x) {
     const int k = idx / (n * n), rem = idx - k * n * n, r = rem / n, c = rem - r * n;
-    double v = 0.0;
-    if (k == 0) v = rh ? rh[rem] : 0.0;
-    else if (k == 1) v = (r < n1 && c < n1) ? ra[r * n1 + c] : 0.0;
-    else v = (r >= n1 && c >= n1) ? rb[(r - n1) * n2 + (c - n1)] : 0.0;
+    double v;
+    if (k == 1) v = rh ? rh[rem] : 0.0;
+    else v = (r < n1 && c < n1) ? ra[r * n1 + c] : (r >= n1 && c >= n1) ? rb[(r - n1) * n2 + (c - n1)] : 0.0;
     out[idx] = v;
   }
 }
@@ -227,7 +226,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   double* ra = ws_alloc<double>(ctx, std::max<int64_t>(n1 * n1, 1));
   double* rb = ws_alloc<double>(ctx, std::max<int64_t>(n2 * n2, 1));
   double* rh = ws_alloc<double>(ctx, n * n);
-  double* stack = ws_alloc<double>(ctx, 3 * n * n);
+  double* stack = ws_alloc<double>(ctx, 2 * n * n);
   double* heads = ws_alloc<double>(ctx, std::max<int64_t>(ng, 1) * n);
   if (!ra || !rb || !rh || !stack || !heads) return fail(JQ_E_OOM, "workspace exhausted (footnote variant)");
   ctx->record_tsqr_events = false;
@@ -276,7 +275,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     cudaEventRecord(ctx->ev[5], ctx->stream);
     return rc;
   }
-  // head rows (G x n) -> R_H, then the final 3-factor stack -> canonical R
+  // head rows (G x n) -> R_H, then [blockdiag(R_A, R_B); R_H] -> canonical R
   if (ng > 0) {
     head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng * n, 256), 4096), 256, 0, ctx->stream>>>(
         sa.totals, (int)n1, sb.totals, (int)n2, keyed ? gr.a_count : nullptr, keyed ? gr.b_count : nullptr,
@@ -301,10 +300,10 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     fprintf(stderr, "footnote debug: R_A nan=%ld max=%g  R_B nan=%ld max=%g  R_H nan=%ld max=%g  heads nan=%ld max=%g\n",
             (long)a1.first, a1.second, (long)b1.first, b1.second, (long)h1.first, h1.second, (long)hh.first, hh.second);
   }
-  footnote_stack_kernel<<<(unsigned)cdiv(3 * n * n, 256), 256, 0, ctx->stream>>>(
+  footnote_stack_kernel<<<(unsigned)cdiv(2 * n * n, 256), 256, 0, ctx->stream>>>(
       rh, n1 > 0 ? ra : nullptr, (int)n1, n2 > 0 ? rb : nullptr, (int)n2, stack);
   JQ_CHECK_LAUNCH(ctx);
-  int rc = tsqr_stack_dev(ctx, stack, 3, n, r_out, true);
+  int rc = tsqr_stack_dev(ctx, stack, 2, n, r_out, true);
   ctx->record_tsqr_events = true;
   cudaEventRecord(ctx->ev[5], ctx->stream);
   return rc;
@@ -455,8 +454,7 @@ static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n
   double* pre[2] = {ws_alloc<double>(ctx, std::max<int64_t>(n1, 1)), ws_alloc<double>(ctx, std::max<int64_t>(n2, 1))};
   double* heads = ws_alloc<double>(ctx, n);
   double* rh = ws_alloc<double>(ctx, n * n);
-  double* stack = ws_alloc<double>(ctx, 3 * n * n);
-  if (!buf[1] || !stack) return fail(JQ_E_OOM, "workspace exhausted (streamed figaro)");
+  if (!buf[1] || !rh) return fail(JQ_E_OOM, "workspace exhausted (streamed figaro)");
   JQ_CUDA(cudaMemsetAsync(pre[0], 0, std::max<int64_t>(n1, 1) * 8, ctx->stream));
   JQ_CUDA(cudaMemsetAsync(pre[1], 0, std::max<int64_t>(n2, 1) * 8, ctx->stream));
   const size_t mark = ctx->ws.used;
@@ -527,13 +525,7 @@ static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n
     head_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(pre[0], (int)n1, pre[1], (int)n2, nullptr,
                                                                         nullptr, 1, m1, m2, heads);
     JQ_CHECK_LAUNCH(ctx);
-    rc = tsqr_dense_dev(ctx, heads, 1, n, rh, false);
-    if (!rc) {
-      footnote_stack_kernel<<<(unsigned)cdiv(3 * n * n, 256), 256, 0, ctx->stream>>>(
-          rh, n1 > 0 ? racc[0] : nullptr, (int)n1, n2 > 0 ? racc[1] : nullptr, (int)n2, stack);
-      JQ_CHECK_LAUNCH(ctx);
-      rc = tsqr_stack_dev(ctx, stack, 3, n, dr, true);
-    }
+    rc = footnote_small_head(ctx, racc[0], n1, racc[1], n2, heads, 1, true, rh, dr);
   }
   ctx->record_tsqr_events = true;
   cudaEventRecord(ctx->ev[5], ctx->stream);

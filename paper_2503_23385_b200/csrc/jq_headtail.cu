@@ -62,7 +62,25 @@ __global__ void carry_top_kernel(double* __restrict__ bagg, const int* __restric
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   double cur = 0.0;  // exclusive carry into block b, written in place
-  for (int64_t b = 0; b < nblk; ++b) {
+  // loads of 16 blocks issued together (the in-place stores would otherwise serialise
+  // every load behind the previous iteration); same additions in the same order
+  constexpr int U = 16;
+  int64_t b = 0;
+  for (; b + U <= nblk; b += U) {
+    double a[U];
+    int f[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = bagg[(b + u) * cols + c];
+      f[u] = bflag[b + u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      bagg[(b + u) * cols + c] = cur;
+      cur = f[u] ? a[u] : cur + a[u];
+    }
+  }
+  for (; b < nblk; ++b) {
     const double a = bagg[b * cols + c];
     bagg[b * cols + c] = cur;
     cur = bflag[b] ? a : cur + a;
