@@ -154,6 +154,20 @@ JQ_API int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64
  * the fixed binary TSQR tree — identical on every rank for the same input. */
 JQ_API int jq_tsqr_stack(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, double* r);
 
+/* ---- brute force (oracle module): the join matrix itself -------- */
+/* materialize_cartesian (ka == kb == NULL) / materialize_natural_join
+ * (SPEC.md:387): rows [A_i | B_j] ordered by key, then left row, then right row.
+ * out == NULL only reports *out_rows; otherwise out holds out_capacity rows of
+ * n1 + n2 doubles. */
+JQ_API int jq_materialize(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
+                   const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* out,
+                   int64_t out_capacity, int64_t* out_rows);
+/* Canonical R of the join matrix by TSQR over its rows, generated on the fly and
+ * never written: baseline_r without the materialisation -- the
+ * performance foil of figaro_r. */
+JQ_API int jq_join_r_bruteforce(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
+                         const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r);
+
 #ifdef __cplusplus
 }
 #endif

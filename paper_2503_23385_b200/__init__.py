@@ -6,7 +6,7 @@ public names, argument layout, return types and error behaviour
 reference (`__getattr__`, :65-73).  Every compute call goes through the C ABI
 of libjoinqr.so (include/joinqr.h) to hand-written sm_100a kernels; there is
 no CPU fallback.  Names of the reference that are not on the hot path
-(CSV IO, CLI/bench harness, brute-force oracle, Givens cross-check) raise an
+(CSV IO, CLI/bench harness, determinant / Givens cross-checks) raise an
 AttributeError that says so ("Out of scope").
 """
 
@@ -46,14 +46,15 @@ _EXPORTS = {
     "set_device": "._native",
     "set_variant": "._native",
     "last_timing": "._native",
+    "materialize_cartesian": ".bruteforce",
+    "materialize_natural_join": ".bruteforce",
+    "baseline_r": ".bruteforce",
+    "baseline_svd": ".bruteforce",
+    "join_r_bruteforce": ".bruteforce",
 }
 
 _OUT_OF_SCOPE = {
     "givens_r": "cross-validation reference only (SPEC.md:299)",
-    "materialize_cartesian": "brute-force oracle (CPU checker lives in oracle/)",
-    "materialize_natural_join": "brute-force oracle (CPU checker lives in oracle/)",
-    "baseline_r": "brute-force oracle (CPU checker lives in oracle/)",
-    "baseline_svd": "brute-force oracle (CPU checker lives in oracle/)",
     "det_lu": "oracle plumbing (CPU checker lives in oracle/)",
     "read_table": "CSV IO is excluded from the timed path (SPEC.md:532)",
     "read_matrix": "CSV IO is excluded from the timed path (SPEC.md:532)",

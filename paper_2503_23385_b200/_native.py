@@ -48,6 +48,8 @@ SIGNATURES = {
     "jq_colsums": [_P, _P, _I64, _I64, _P],
     "jq_figaro_r_shard": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, C.c_int, _P],
     "jq_tsqr_stack": [_P, _P, _I64, _I64, _P],
+    "jq_materialize": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _P, _I64, _P],
+    "jq_join_r_bruteforce": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _P],
 }
 _RESTYPE = {"jq_last_error": C.c_char_p, "jq_kernel_launches": C.c_int64}
 

@@ -237,6 +237,38 @@ struct FigaroArgs {
   SideScan side;                 // tile pass of another scan to run alongside (or nothing)
 };
 int figaro_tsqr_dev(jq_ctx* ctx, const FigaroArgs& fa, double* r_out, bool canonical);
+
+// The join matrix itself (brute force): row v = [A_i | B_j], rows by
+// key, then left row, then right row.  Cartesian when jo == nullptr (i = v / m2).
+struct JoinArgs {
+  const double* a; int64_t m1, n1;
+  const double* b; int64_t m2, n2;
+  const int64_t* jo;       // keyed: join-row offset of each matched group (ng + 1)
+  const int64_t* a_start;  // keyed: per matched group
+  const int64_t* b_start;
+  const int64_t* b_count;
+  int64_t ng;
+  int64_t rows;            // join rows
+};
+// join row v -> (A row, B row)
+__device__ __forceinline__ void join_row(const JoinArgs& ja, int64_t v, int64_t& ia, int64_t& ib) {
+  if (!ja.jo) {
+    ia = v / ja.m2;
+    ib = v - ia * ja.m2;
+    return;
+  }
+  int64_t lo = 0, hi = ja.ng - 1;  // last group with jo[g] <= v
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(ja.jo + mid) <= v) lo = mid; else hi = mid - 1;
+  }
+  const int64_t local = v - __ldg(ja.jo + lo), bc = __ldg(ja.b_count + lo);
+  const int64_t q = local / bc;
+  ia = __ldg(ja.a_start + lo) + q;
+  ib = __ldg(ja.b_start + lo) + (local - q * bc);
+}
+// canonical-or-not R of the join matrix, its rows generated inside the TSQR (never written)
+int join_tsqr_dev(jq_ctx* ctx, const JoinArgs& ja, double* r_out, bool canonical);
 size_t figaro_tsqr_ws_bytes(int64_t m1, int64_t m2, int64_t n, int sms);
 
 // SVD (jq_svd.cu).

@@ -145,6 +145,23 @@ struct DenseSrc {
   __device__ void side_scan(int, int, int) const {}
 };
 
+// Rows of the join matrix generated from A and B in every data warp (brute force; no
+// raw rows, no loader work: rc() = 0)
+struct JoinSrc : DenseSrc {
+  JoinArgs ja;
+  __device__ int rc(int64_t) const { return 0; }
+  __device__ const double* ptr(int64_t) const { return nullptr; }
+  __device__ int64_t avail(int64_t v0) const { return ja.rows - v0; }
+  template <class C>
+  __device__ double value(const double*, const double*, int64_t v0, int i, int l, int nrows, int) const {
+    const int n1 = (int)ja.n1;
+    if (i >= nrows || l >= n1 + (int)ja.n2) return 0.0;
+    int64_t ia, ib;
+    join_row(ja, v0 + i, ia, ib);
+    return l < n1 ? __ldg(ja.a + ia * n1 + l) : __ldg(ja.b + ib * ja.n2 + (l - n1));
+  }
+};
+
 struct FigaroSrc {
   FigaroArgs fa;
   int64_t m1pad;  // A-part padded to a TILE_ROWS multiple; B-part starts here
@@ -1387,6 +1404,15 @@ int tsqr_dense_dev(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, dou
   DenseSrc src{m, rows, cols};
   const int tma = (reinterpret_cast<uintptr_t>(m) & 15) == 0;
   return dispatch_stream(ctx, src, std::max<int64_t>(rows, 1), 64, (int)cols, canonical, r_out, tma);
+}
+
+int join_tsqr_dev(jq_ctx* ctx, const JoinArgs& ja, double* r_out, bool canonical) {
+  JoinSrc src;
+  src.m = nullptr;
+  src.rows = ja.rows;
+  src.cols = ja.n1 + ja.n2;
+  src.ja = ja;
+  return dispatch_stream(ctx, src, std::max<int64_t>(ja.rows, 1), 64, (int)(ja.n1 + ja.n2), canonical, r_out, 0);
 }
 
 __global__ void pad_stack_kernel(const double* __restrict__ rs, int64_t count, int n, int np,

@@ -52,7 +52,8 @@ def test_drop_in_names_match_reference_exports():
            "scale", "row_slice", "is_upper_triangular", "head", "tail", "head_tail", "Table",
            "ReducedMatrix", "reduce_cartesian", "reduce_natural_join", "reduce_join",
            "householder_r", "canonicalize", "figaro_r", "SvdResult", "svd_of_r", "figaro_svd",
-           "GenSpec", "gen_uniform"]
+           "GenSpec", "gen_uniform", "materialize_cartesian", "materialize_natural_join", "baseline_r",
+           "baseline_svd"]
     for n in ref:
         assert getattr(P, n) is getattr(joinqr, n)
     with pytest.raises(AttributeError, match="not part of the B200 hot path"):
