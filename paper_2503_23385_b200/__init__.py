@@ -6,7 +6,7 @@ public names, argument layout, return types and error behaviour
 reference (`__getattr__`, :65-73).  Every compute call goes through the C ABI
 of libjoinqr.so (include/joinqr.h) to hand-written sm_100a kernels; there is
 no CPU fallback.  Names of the reference that are not on the hot path
-(CSV IO, CLI/bench harness, determinant / Givens cross-checks) raise an
+(bench-harness objects, determinant / Givens cross-checks) raise an
 AttributeError that says so ("Out of scope").
 """
 
@@ -51,20 +51,20 @@ _EXPORTS = {
     "baseline_r": ".bruteforce",
     "baseline_svd": ".bruteforce",
     "join_r_bruteforce": ".bruteforce",
+    "read_table": ".tableio",
+    "read_matrix": ".tableio",
+    "write_matrix": ".tableio",
+    "write_table": ".tableio",
+    "write_svd": ".tableio",
 }
 
 _OUT_OF_SCOPE = {
     "givens_r": "cross-validation reference only (SPEC.md:299)",
     "det_lu": "oracle plumbing (CPU checker lives in oracle/)",
-    "read_table": "CSV IO is excluded from the timed path (SPEC.md:532)",
-    "read_matrix": "CSV IO is excluded from the timed path (SPEC.md:532)",
-    "write_matrix": "CSV IO is excluded from the timed path (SPEC.md:532)",
-    "write_table": "CSV IO is excluded from the timed path (SPEC.md:532)",
-    "write_svd": "CSV IO is excluded from the timed path (SPEC.md:532)",
-    "BenchCell": "bench harness: use bench.py",
-    "BenchReport": "bench harness: use bench.py",
-    "run_bench": "bench harness: use bench.py",
-    "track_peak_memory": "bench harness: use bench.py",
+    "BenchCell": "bench harness objects: use `joinqr bench` (cli.py) or bench.py",
+    "BenchReport": "bench harness objects: use `joinqr bench` (cli.py) or bench.py",
+    "run_bench": "bench harness objects: use `joinqr bench` (cli.py) or bench.py",
+    "track_peak_memory": "host allocation tracking of the CPU harness (no GPU counterpart)",
 }
 
 

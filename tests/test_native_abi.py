@@ -53,11 +53,11 @@ def test_drop_in_names_match_reference_exports():
            "ReducedMatrix", "reduce_cartesian", "reduce_natural_join", "reduce_join",
            "householder_r", "canonicalize", "figaro_r", "SvdResult", "svd_of_r", "figaro_svd",
            "GenSpec", "gen_uniform", "materialize_cartesian", "materialize_natural_join", "baseline_r",
-           "baseline_svd"]
+           "baseline_svd", "read_table", "read_matrix", "write_matrix", "write_table", "write_svd"]
     for n in ref:
         assert getattr(P, n) is getattr(joinqr, n)
     with pytest.raises(AttributeError, match="not part of the B200 hot path"):
-        P.read_table
+        P.det_lu
 
 
 def test_host_validation_errors_before_any_gpu_work():
