@@ -92,7 +92,8 @@ static size_t figaro_ws(int64_t m1, int64_t n1, int64_t m2, int64_t n2, bool key
   size_t foot = (keyed ? group_ws_bytes(m1, m2) : 0) + segscan_ws_bytes(m1, std::max<int64_t>(n1, 1), cap) +
                 segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) + tsqr_ws_bytes(m1 + TILE_ROWS, n1, sms) +
                 tsqr_ws_bytes(m2 + TILE_ROWS, n2, sms) + tsqr_ws_bytes(cap, n, sms) +
-                tsqr_ws_bytes(3 * n, n, sms) + ws_bytes(size_t(cap) * n, 8) + 8 * ws_bytes(size_t(n) * n, 8);
+                tsqr_ws_bytes(3 * n, n, sms) + ws_bytes(size_t(cap) * n, 8) + 8 * ws_bytes(size_t(n) * n, 8) +
+                tsqr_pair_ws_bytes(std::max(n1, n2), sms);
   return std::max(dense, foot);
 }
 
@@ -235,6 +236,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   cudaEventRecord(ctx->ev[3], ctx->stream);
   // tails of A scaled by sqrt(m2g): the "B-part" of a source with an empty A-part
   FigaroArgs fa{};
+  LeafSet leaves_a{};
   if (n1 > 0) {
     fa.b = a; fa.m2 = m1; fa.n2 = n1;
     fa.gid_b = keyed ? gr.gid_a : nullptr;
@@ -243,7 +245,8 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     fa.b_carry = sa.carry;
     fa.m1_global = m2; fa.m2_global = m1; fa.b_row0 = 0;
     fa.side = side_b;
-    int rc = figaro_tsqr_dev(ctx, fa, ra, false);
+    // both sides present: leaves now, the two trees later in shared launches
+    int rc = n2 > 0 ? figaro_tsqr_leaves(ctx, fa, &leaves_a) : figaro_tsqr_dev(ctx, fa, ra, false);
     if (rc) { ctx->record_tsqr_events = true; return rc; }
   } else {
     JQ_TRY(segscan_tiles(ctx, side_b));
@@ -259,7 +262,13 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     fb.a_count = keyed ? gr.a_count : nullptr;
     fb.b_carry = sb.carry;
     fb.m1_global = m1; fb.m2_global = m2; fb.b_row0 = 0;
-    rc = figaro_tsqr_dev(ctx, fb, rb, false);
+    if (n1 > 0) {
+      LeafSet leaves_b{};
+      rc = figaro_tsqr_leaves(ctx, fb, &leaves_b);
+      if (!rc) rc = tsqr_finish_pair(ctx, leaves_a, leaves_b, ra, rb);
+    } else {
+      rc = figaro_tsqr_dev(ctx, fb, rb, false);
+    }
     if (rc) { ctx->record_tsqr_events = true; return rc; }
   }
   cudaEventRecord(ctx->ev[4], ctx->stream);

@@ -237,6 +237,17 @@ struct FigaroArgs {
   SideScan side;                 // tile pass of another scan to run alongside (or nothing)
 };
 int figaro_tsqr_dev(jq_ctx* ctx, const FigaroArgs& fa, double* r_out, bool canonical);
+// TSQR leaves of a source without their tree (footnote: both sides' trees run in shared
+// launches, tsqr_finish_pair); R's are NOT canonical
+struct LeafSet {
+  double* leaves;  // count NP x NP factors
+  double* tmp;     // ceil(count / 2) factors (the single-stack tree's ping-pong buffer)
+  int64_t count;
+  int np, n;
+};
+int figaro_tsqr_leaves(jq_ctx* ctx, const FigaroArgs& fa, LeafSet* out);
+int tsqr_finish_pair(jq_ctx* ctx, const LeafSet& x, const LeafSet& y, double* rx, double* ry);
+size_t tsqr_pair_ws_bytes(int64_t n, int sms);
 
 // The join matrix itself (brute force): row v = [A_i | B_j], rows by
 // key, then left row, then right row.  Cartesian when jo == nullptr (i = v / m2).

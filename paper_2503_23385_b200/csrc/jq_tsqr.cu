@@ -975,9 +975,19 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
   Src s = src;
   int64_t row_begin, row_end;
   if constexpr (COMBINE) {
-    rinit = r_init + (2 * cta) * C::NP * C::NP;
-    if (2 * cta + 1 < init_count) {
-      s.m = r_init + (2 * cta + 1) * C::NP * C::NP;
+    // one stack (init_count elements), or -- rows_per_cta = k > 0 -- two stacks of k
+    // elements each, the first at r_init and the second at src.m, combined side by side
+    // (CTA c < ceil(k/2) works on the first; outputs stay contiguous)
+    const double* base = r_init;
+    int64_t j = cta, cnt = init_count;
+    if (rows_per_cta > 0) {
+      const int64_t half = (rows_per_cta + 1) / 2;
+      cnt = rows_per_cta;
+      if (cta >= half) { base = src.m; j = cta - half; }
+    }
+    rinit = base + (2 * j) * C::NP * C::NP;
+    if (2 * j + 1 < cnt) {
+      s.m = base + (2 * j + 1) * C::NP * C::NP;
       row_begin = 0; row_end = C::NP;
     } else {
       row_begin = row_end = 0;
@@ -1280,6 +1290,34 @@ static int tree_combine(jq_ctx* ctx, double* a, double* b, int64_t count, double
   return JQ_OK;
 }
 
+// Both sides' trees in the same launches (footnote variant): stacks a0 and a1 of k
+// elements each (one level = one launch of 2 ceil(k/2) CTAs); tmp holds
+// 2 * 2 * ceil(k/2) factors.  Same pairing per stack as tree_combine, so the same bits.
+template <class C>
+static int tree_combine_pair(jq_ctx* ctx, const double* a0, const double* a1, int64_t k, double* tmp,
+                             const double** r0, const double** r1) {
+  const size_t nn = size_t(C::NP) * C::NP;
+  double* t[2] = {tmp, tmp + 2 * size_t((k + 1) / 2) * nn};
+  int w = 0;
+  while (k > 1) {
+    const int64_t half = (k + 1) / 2;
+    DenseSrc ds{a1, C::NP, C::NP};
+    JQ_TRY((launch_tsqr<C, DenseSrc, true>(ctx, (int)(2 * half), ds, k, 0, a0, 0, t[w], 1)));
+    a0 = t[w];
+    a1 = t[w] + half * nn;
+    w ^= 1;
+    k = half;
+  }
+  *r0 = a0;
+  *r1 = a1;
+  return JQ_OK;
+}
+
+size_t tsqr_pair_ws_bytes(int64_t n, int sms) {
+  const int64_t np = n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256;
+  return 2 * ws_bytes(size_t(2 * (2 * sms + 1)) * np * np, 8);
+}
+
 size_t tsqr_ws_bytes(int64_t rows, int64_t n, int sms) {
   int np = np_for(n);
   if (np < 0) return 0;
@@ -1293,7 +1331,7 @@ size_t figaro_tsqr_ws_bytes(int64_t m1, int64_t m2, int64_t n, int sms) {
 
 template <class C, class Src>
 static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
-                      bool canonical, double* r_out, int use_tma) {
+                      bool canonical, double* r_out, int use_tma, LeafSet* defer = nullptr) {
   align = std::max<int64_t>(align, C::K);
   if (align % C::K) return fail(JQ_E_INVALID, "row alignment must be a multiple of the TSQR chunk");
   int64_t max_leaves = int64_t(ctx->sms) * ctas_per_sm<C, Src>();
@@ -1309,6 +1347,10 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
   JQ_TRY(segscan_tiles(ctx, src.side_job()));  // this leaf has no spare warps for it
   JQ_TRY((launch_tsqr<C, Src, false>(ctx, (int)leaves, src, rows_per_cta, vrows, nullptr, 0, a, use_tma)));
+  if (defer) {
+    *defer = LeafSet{a, b, leaves, C::NP, n};
+    return JQ_OK;
+  }
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
   double* fin = nullptr;
   JQ_TRY(tree_combine<C>(ctx, a, b, leaves, &fin));
@@ -1330,7 +1372,7 @@ static int leaf_impl() {
 
 template <class CS, class Src>
 static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
-                         bool canonical, double* r_out, int use_tma) {
+                         bool canonical, double* r_out, int use_tma, LeafSet* defer = nullptr) {
   using C = Cfg<CS::NP>;  // tree combine
   static int occ = [] {
     int o = 0;
@@ -1369,6 +1411,10 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
   kern<<<(int)ctas, CS::THREADS, CS::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a,
                                                           (use_tma ? 1 : 0) | (explicit_panels ? 2 : 0) | debug_flags);
   JQ_CHECK_LAUNCH(ctx);
+  if (defer) {
+    *defer = LeafSet{a, b, ctas, C::NP, n};
+    return JQ_OK;
+  }
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
   double* fin = nullptr;
   JQ_TRY(tree_combine<C>(ctx, a, b, ctas, &fin));
@@ -1380,23 +1426,92 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
 
 template <class Src>
 static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
-                           bool canonical, double* r_out, int use_tma) {
+                           bool canonical, double* r_out, int use_tma, LeafSet* defer = nullptr) {
   switch (np_for(n)) {
     case 16:
-      if (leaf_impl() == 0) return run_stream_ws<CfgS<16, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      return run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 0)
+        return run_stream_ws<CfgS<16, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
+      return run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 32:
-      if (leaf_impl() == 0) return run_stream_ws<CfgS<32, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 0)
+        return run_stream_ws<CfgS<32, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
+      return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 64:
-      if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-      return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
+      return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 128:  // (CfgS<128, 16, 8, 1, 8> -- 64-row chunks beside the 70 KB R -- measured slower:
       // C4 dense 1094 vs 861 ms, C5 22.5 vs 21.6 ms; the chain cost is per panel, not per row)
-      return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
-    case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out, use_tma);
+      return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
+    case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
   }
   return fail(JQ_E_INVALID, "column count above 256 is not supported by the TSQR kernels");
+}
+
+// the tree + finalize of deferred leaf sets: both in shared launches when they have the
+// same width and leaf count, else one after the other
+template <class C>
+static int finish_pair_np(jq_ctx* ctx, const LeafSet& x, const LeafSet& y, double* tmp, double* rx, double* ry) {
+  const double *fx = nullptr, *fy = nullptr;
+  if (x.count == y.count && tmp) {
+    JQ_TRY(tree_combine_pair<C>(ctx, x.leaves, y.leaves, x.count, tmp, &fx, &fy));
+  } else {
+    double* f = nullptr;
+    JQ_TRY(tree_combine<C>(ctx, x.leaves, x.tmp, x.count, &f));
+    fx = f;
+    JQ_TRY(tree_combine<C>(ctx, y.leaves, y.tmp, y.count, &f));
+    fy = f;
+  }
+  finalize_r_kernel<<<(int)cdiv(int64_t(x.n) * x.n, 256), 256, 0, ctx->stream>>>(fx, C::NP, x.n, false, rx);
+  JQ_CHECK_LAUNCH(ctx);
+  finalize_r_kernel<<<(int)cdiv(int64_t(y.n) * y.n, 256), 256, 0, ctx->stream>>>(fy, C::NP, y.n, false, ry);
+  JQ_CHECK_LAUNCH(ctx);
+  return JQ_OK;
+}
+
+template <class C>
+static int finish_one(jq_ctx* ctx, const LeafSet& x, double* rx) {
+  double* f = nullptr;
+  JQ_TRY(tree_combine<C>(ctx, x.leaves, x.tmp, x.count, &f));
+  finalize_r_kernel<<<(int)cdiv(int64_t(x.n) * x.n, 256), 256, 0, ctx->stream>>>(f, C::NP, x.n, false, rx);
+  JQ_CHECK_LAUNCH(ctx);
+  return JQ_OK;
+}
+
+static int finish_np(jq_ctx* ctx, const LeafSet& x, double* rx) {
+  switch (x.np) {
+    case 16: return finish_one<Cfg<16>>(ctx, x, rx);
+    case 32: return finish_one<Cfg<32>>(ctx, x, rx);
+    case 64: return finish_one<Cfg<64>>(ctx, x, rx);
+    case 128: return finish_one<Cfg<128>>(ctx, x, rx);
+    case 256: return finish_one<Cfg<256>>(ctx, x, rx);
+  }
+  return fail(JQ_E_INVALID, "bad leaf width");
+}
+
+int figaro_tsqr_leaves(jq_ctx* ctx, const FigaroArgs& fa, LeafSet* out) {
+  FigaroSrc src;
+  src.fa = fa;
+  src.m1pad = cdiv(fa.m1, TILE_ROWS) * TILE_ROWS;
+  src.n = (int)(fa.n1 + fa.n2);
+  int64_t vrows = src.m1pad + fa.m2;
+  const int tma = ((reinterpret_cast<uintptr_t>(fa.a) | reinterpret_cast<uintptr_t>(fa.b)) & 15) == 0;
+  return dispatch_stream(ctx, src, std::max<int64_t>(vrows, 1), TILE_ROWS, src.n, false, nullptr, tma, out);
+}
+
+int tsqr_finish_pair(jq_ctx* ctx, const LeafSet& x, const LeafSet& y, double* rx, double* ry) {
+  if (x.np != y.np) {
+    JQ_TRY(finish_np(ctx, x, rx));
+    return finish_np(ctx, y, ry);
+  }
+  double* tmp = x.count == y.count ? ws_alloc<double>(ctx, 4 * size_t((x.count + 1) / 2) * x.np * x.np) : nullptr;
+  switch (x.np) {
+    case 16: return finish_pair_np<Cfg<16>>(ctx, x, y, tmp, rx, ry);
+    case 32: return finish_pair_np<Cfg<32>>(ctx, x, y, tmp, rx, ry);
+    case 64: return finish_pair_np<Cfg<64>>(ctx, x, y, tmp, rx, ry);
+    case 128: return finish_pair_np<Cfg<128>>(ctx, x, y, tmp, rx, ry);
+    case 256: return finish_pair_np<Cfg<256>>(ctx, x, y, tmp, rx, ry);
+  }
+  return fail(JQ_E_INVALID, "bad leaf width");
 }
 
 int tsqr_dense_dev(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, double* r_out,
