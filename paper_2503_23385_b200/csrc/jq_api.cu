@@ -607,6 +607,8 @@ int jq_ctx_destroy(jq_ctx* ctx) {
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+  for (auto& e : ctx->aev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->pev) if (e) cudaEventDestroy(e);
   delete ctx;
   return JQ_OK;

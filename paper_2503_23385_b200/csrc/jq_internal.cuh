@@ -67,6 +67,8 @@ struct jq_ctx {
   cudaEvent_t ev[8]{};
   cudaStream_t copy_stream = nullptr;   // host -> device piece copies (streamed figaro)
   cudaEvent_t pev[4]{};                 // piece copied / consumed events
+  cudaStream_t aux_stream = nullptr;    // V replay beside the Jacobi sweeps (jq_svd.cu)
+  cudaEvent_t aev[2]{};
 };
 
 namespace jq {

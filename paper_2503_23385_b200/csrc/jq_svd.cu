@@ -28,6 +28,15 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // player at position k in round r of the circle method over n (even) players
 __device__ __forceinline__ int rr_player(int k, int r, int n) {
   return k == 0 ? 0 : ((k - 1 + r) % (n - 1)) + 1;
@@ -261,7 +270,7 @@ template <int WPC>
 __global__ void __launch_bounds__(WPC * 32, 1)
 jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_sweeps, int* flags,
                       double* __restrict__ sig, double2* __restrict__ rlog, int* __restrict__ nsweeps,
-                      double* __restrict__ values, int n_out) {
+                      int* __restrict__ progress, double* __restrict__ values, int n_out) {
   namespace cg = cooperative_groups;
   constexpr int COLS = 2 * WPC, THREADS = WPC * 32;
   cg::cluster_group cluster = cg::this_cluster();
@@ -377,7 +386,9 @@ jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_
       const int r = e / WPC, w = e - r * WPC;
       rlog[((size_t)sweep * (np - 1) + r) * half + rank * WPC + w] = slog[e];
     }
+    __threadfence();  // the log is read by jacobi_v_kernel while the sweeps go on
     cluster.sync();
+    if (rank == 0 && tid == 0) st_release_gpu(progress, sweep + 1);
     int any = 0;
     for (int b = 0; b < nct; ++b) any |= *cluster.map_shared_rank(&rotf[sweep % 3], b);
     if (!any) break;
@@ -386,6 +397,7 @@ jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_
     if (sweep == max_sweeps) atomicOr(flags, FLAG_NOCONV);
     *nsweeps = sweep;  // sweeps with rotations (the last, clean one is not replayed)
   }
+  int* const done = progress + 1;
   // after whole sweeps every player is back at its own position: sigma_j = |column j|
   const double* fin = cols + cur * bufsz;
   for (int sl = warp; sl < COLS; sl += WPC) {
@@ -410,17 +422,24 @@ jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_
     for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
     if (rk < n_out && lane == 0) values[rk] = sj;
   }
+  // sigma (global) and nsweeps published: the V replay may rank and finish
+  if (rank == 0 && tid == 0) {
+    __threadfence();
+    st_release_gpu(done, 1);
+  }
 }
 
 // Row i of V (one warp per row): replay the logged rotations of jacobi_cluster_kernel
 // on V[i, :] (V = I at the start), rounds in order, lane l doing pairs l, l + 32, ...
 // (the same element arithmetic as a carried V); then vout[i][rank(j)] = V[i][j] for the
-// n_out largest sigma.
+// n_out largest sigma.  Runs on a second stream WHILE the sweeps go on: a sweep is
+// replayed once progress[0] says its log is out, and the kernel ends when progress[1]
+// (done) is set and nsweeps sweeps are replayed (the final, clean sweep is skipped).
 constexpr int SVDV_WARPS = 4, SVDV_BATCH = 4;
 
 __global__ void __launch_bounds__(SVDV_WARPS * 32)
-jacobi_v_kernel(const double2* __restrict__ rlog, const int* __restrict__ nsweeps, int np,
-                const double* __restrict__ sig, double* __restrict__ vout, int n_out) {
+jacobi_v_kernel(const double2* __restrict__ rlog, const int* nsweeps, const int* progress, int np,
+                const double* sig, double* __restrict__ vout, int n_out) {
   __shared__ double rows[SVDV_WARPS][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = np >> 1;
   const int i = blockIdx.x * SVDV_WARPS + warp;
@@ -428,53 +447,68 @@ jacobi_v_kernel(const double2* __restrict__ rlog, const int* __restrict__ nsweep
   double* row = rows[warp];
   for (int j = lane; j < np; j += 32) row[j] = i == j ? 1.0 : 0.0;
   __syncwarp();
-  const int rounds = *nsweeps * (np - 1);
   int plo[4], phi[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     plo[k] = lane + 32 * k;
     phi[k] = np - 1 - (lane + 32 * k);
   }
-  double2 nx[SVDV_BATCH][4];  // the next batch of (c, s), loaded one batch ahead
-  auto load = [&](int r0) {
+  const int rps = np - 1;  // rounds per sweep
+  for (int s = 0;; ++s) {
+    // wait for sweep s's log, or for the end (then nsweeps says whether s is replayed)
+    int ready;
+    for (;;) {
+      ready = ld_acquire_gpu(progress);
+      if (ready > s || ld_acquire_gpu(progress + 1)) break;
+      __nanosleep(2000);
+    }
+    if (ld_acquire_gpu(progress + 1) && s >= *(volatile const int*)nsweeps) break;
+    const int r0s = s * rps, r1s = r0s + rps;
+    double2 nx[SVDV_BATCH][4];  // the next batch of (c, s), loaded one batch ahead
+    auto load = [&](int r0) {
 #pragma unroll
-    for (int b = 0; b < SVDV_BATCH; ++b)
+      for (int b = 0; b < SVDV_BATCH; ++b)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int pi = lane + 32 * k;
-        nx[b][k] = (pi < half && r0 + b < rounds) ? rlog[(size_t)(r0 + b) * half + pi] : make_double2(1.0, 0.0);
-      }
-  };
-  load(0);
-  for (int r0 = 0; r0 < rounds; r0 += SVDV_BATCH) {
-    double2 cs[SVDV_BATCH][4];
-#pragma unroll
-    for (int b = 0; b < SVDV_BATCH; ++b)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) cs[b][k] = nx[b][k];
-    if (r0 + SVDV_BATCH < rounds) load(r0 + SVDV_BATCH);
-#pragma unroll
-    for (int b = 0; b < SVDV_BATCH; ++b) {
-      if (r0 + b >= rounds) break;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (lane + 32 * k < half) {
-          const int p = min(plo[k], phi[k]), q = max(plo[k], phi[k]);
-          const double c = cs[b][k].x, s = cs[b][k].y;
-          const double u = row[p], w = row[q];
-          row[p] = c * u - s * w;
-          row[q] = s * u + c * w;
-          plo[k] = plo[k] == 0 ? 0 : (plo[k] == np - 1 ? 1 : plo[k] + 1);
-          phi[k] = phi[k] == np - 1 ? 1 : phi[k] + 1;
+        for (int k = 0; k < 4; ++k) {
+          const int pi = lane + 32 * k;
+          nx[b][k] = (pi < half && r0 + b < r1s) ? __ldcg(rlog + (size_t)(r0 + b) * half + pi)
+                                                 : make_double2(1.0, 0.0);
         }
+    };
+    load(r0s);
+    for (int r0 = r0s; r0 < r1s; r0 += SVDV_BATCH) {
+      double2 cs[SVDV_BATCH][4];
+#pragma unroll
+      for (int b = 0; b < SVDV_BATCH; ++b)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cs[b][k] = nx[b][k];
+      if (r0 + SVDV_BATCH < r1s) load(r0 + SVDV_BATCH);
+#pragma unroll
+      for (int b = 0; b < SVDV_BATCH; ++b) {
+        if (r0 + b >= r1s) break;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (lane + 32 * k < half) {
+            const int p = min(plo[k], phi[k]), q = max(plo[k], phi[k]);
+            const double c = cs[b][k].x, sn = cs[b][k].y;
+            const double u = row[p], w = row[q];
+            row[p] = c * u - sn * w;
+            row[q] = sn * u + c * w;
+            plo[k] = plo[k] == 0 ? 0 : (plo[k] == np - 1 ? 1 : plo[k] + 1);
+            phi[k] = phi[k] == np - 1 ? 1 : phi[k] + 1;
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   for (int j = lane; j < np; j += 32) {
-    const double sj = sig[j];
+    const double sj = __ldcg(sig + j);
     int rk = 0;
-    for (int k = 0; k < np; ++k) rk += (sig[k] > sj) || (sig[k] == sj && k < j);
+    for (int k = 0; k < np; ++k) {
+      const double sk = __ldcg(sig + k);
+      rk += (sk > sj) || (sk == sj && k < j);
+    }
     if (rk < n_out) vout[(size_t)i * n_out + rk] = row[j];
   }
 }
@@ -523,7 +557,8 @@ static int launch_cluster_wpc(jq_ctx* ctx, const double* A, int np, double* sig,
     return -1;  // not launchable with this shape
   }
   const double tol = 1e-14;
-  JQ_CUDA(cudaLaunchKernelEx(&cfg, kern, A, np, tol, SVD_MAX_SWEEPS, ctx->d_flags, sig, rlog, nsw, values, n_out));
+  JQ_CUDA(cudaLaunchKernelEx(&cfg, kern, A, np, tol, SVD_MAX_SWEEPS, ctx->d_flags, sig, rlog, nsw, nsw + 1, values,
+                             n_out));
   JQ_CHECK_LAUNCH(ctx);
   return JQ_OK;
 }
@@ -554,11 +589,23 @@ int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values,
     if (!A || !sig || !nsw || !rlog) return fail(JQ_E_OOM, "workspace exhausted (svd)");
     svd_init_kernel<<<(unsigned)cdiv(int64_t(npc) * npc, 256), 256, 0, ctx->stream>>>(r, (int)n, npc, A, nullptr);
     JQ_CHECK_LAUNCH(ctx);
+    // nsw = {nsweeps, sweeps whose log is out, done}
+    JQ_CUDA(cudaMemsetAsync(nsw, 0, 4 * sizeof(int), ctx->stream));
+    if (want_v && !ctx->aux_stream) {
+      JQ_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+      for (auto& e : ctx->aev) JQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    if (want_v) JQ_CUDA(cudaEventRecord(ctx->aev[0], ctx->stream));
     JQ_TRY(launch_jacobi_cluster(ctx, A, npc, sig, rlog, nsw, values, (int)n));
     if (want_v) {
-      jacobi_v_kernel<<<(unsigned)cdiv(n, SVDV_WARPS), SVDV_WARPS * 32, 0, ctx->stream>>>(rlog, nsw, npc, sig, v,
-                                                                                        (int)n);
+      // V replays each sweep's log on a second stream while the next sweeps run (launched
+      // only once the cluster kernel is queued: it waits on that kernel's progress flags)
+      JQ_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aev[0], 0));
+      jacobi_v_kernel<<<(unsigned)cdiv(n, SVDV_WARPS), SVDV_WARPS * 32, 0, ctx->aux_stream>>>(rlog, nsw, nsw + 1,
+                                                                                           npc, sig, v, (int)n);
       JQ_CHECK_LAUNCH(ctx);
+      JQ_CUDA(cudaEventRecord(ctx->aev[1], ctx->aux_stream));
+      JQ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aev[1], 0));
     }
     return JQ_OK;
   }
