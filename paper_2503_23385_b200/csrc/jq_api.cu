@@ -93,7 +93,9 @@ static size_t figaro_ws(int64_t m1, int64_t n1, int64_t m2, int64_t n2, bool key
                 segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) + tsqr_ws_bytes(m1 + TILE_ROWS, n1, sms) +
                 tsqr_ws_bytes(m2 + TILE_ROWS, n2, sms) + tsqr_ws_bytes(cap, n, sms) +
                 tsqr_ws_bytes(3 * n, n, sms) + ws_bytes(size_t(cap) * n, 8) + 8 * ws_bytes(size_t(n) * n, 8) +
-                tsqr_pair_ws_bytes(std::max(n1, n2), sms);
+                tsqr_pair_ws_bytes(std::max(n1, n2), sms) +
+                // carry-free leaves: block sums (the extra stack elements: tsqr_ws_bytes' slack)
+                2 * ws_bytes(size_t(sms) * 32 * n, 8);
   return std::max(dense, foot);
 }
 
@@ -116,6 +118,56 @@ __global__ void head_rows_kernel(const double* __restrict__ totA, int n1, const 
     out[idx] = c < n1 ? sqrt(m2g) * (totA[g * n1 + c] / sqrt(m1g))
                       : sqrt(m1g) * (totB[g * n2 + (c - n1)] / sqrt(m2g));
   }
+}
+
+// Between-block rows of carry-free leaves (Cartesian footnote).  Each leaf of side X
+// took its row block k (m_k rows, column sums s_k) as a group of its own: local tails
+// (prefix from 0), no local head.  The between-block part of the centred Gram of X is
+//   sum_{k >= 1} v_k v_k^T,  v_k = sqrt(W_k m_k / (W_k + m_k)) (s_k / m_k - S_k / W_k)
+// (W_k, S_k: rows and column sums of blocks 0..k-1; the pairwise scatter update), so
+// with the footnote scale these P - 1 rows stand in for the carries.  They are written
+// as dense NP-row elements behind the side's leaves at odd stack positions (the first
+// tree level absorbs element 2c + 1 as rows into R = element 2c; the even elements in
+// between are zero R's, block_stack_layout), so the side's own tree takes them in.
+// One thread per column (both sides), blocks in a fixed order: deterministic.  Also
+// the global head row [sqrt(m2) hA | sqrt(m1) hB] from the block sums.
+struct BlockSide {
+  const double* sums;
+  int64_t p, blk, m;
+  int nc;
+  double scale;       // sqrt(rows of the other side)
+  double* stack;      // the side's leaf stack (p leaves, then the extra elements)
+  int64_t first_d;    // stack index of the first dense element
+};
+__global__ void block_rows_kernel(BlockSide sa, BlockSide sb, int np, double* __restrict__ head) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= sa.nc + sb.nc) return;
+  const BlockSide& sd = c < sa.nc ? sa : sb;
+  const int cc = c < sa.nc ? c : c - sa.nc;
+  const size_t nn = size_t(np) * np;
+  double W = 0.0, Sk = 0.0;
+  for (int64_t k = 0; k < sd.p; ++k) {
+    const double mk = (double)min(sd.blk, sd.m - k * sd.blk);
+    const double sk = sd.sums[k * sd.nc + cc];
+    if (k > 0) {
+      const int64_t r = k - 1, j = r / np;
+      sd.stack[(sd.first_d + 2 * j) * nn + (r - j * np) * np + cc] =
+          sd.scale * sqrt(W * mk / (W + mk)) * (sk / mk - Sk / W);
+    }
+    W += mk;
+    Sk += sk;
+  }
+  head[c] = sd.scale * (Sk / sqrt((double)sd.m));  // sqrt(m_other) * total / sqrt(m)
+}
+
+// extra stack elements behind p leaves: a zero R when p is even, then D0, Z, D1, ..., so
+// every dense element D_j sits at an odd index; returns the new count
+static int64_t block_stack_layout(int64_t p, int np, int64_t* first_d) {
+  const int64_t e = p > 1 ? cdiv(p - 1, np) : 0;
+  if (e == 0) { *first_d = p; return p; }
+  const int64_t pad = (p % 2 == 0) ? 1 : 0;
+  *first_d = p + pad;
+  return p + pad + 2 * e - 1;
 }
 
 // [blockdiag(R_A, R_B); R_H]: two n x n factors (the first already upper triangular)
@@ -199,6 +251,75 @@ static int footnote_small_head(jq_ctx* ctx, const double* ra, int64_t n1, const 
 }
 constexpr int64_t FOOTNOTE_GIVENS_MAX_HEADS = 8;
 
+// Cartesian footnote variant with carry-free leaves (default; JQ_FOOTNOTE_CARRY=scan
+// restores the scan-carried leaves for A/B tests): no prefix-scan pass at all -- each
+// leaf transforms its own row block (FigaroArgs::blk_sums), block_rows_kernel turns the
+// block sums into each side's between-block rows (taken in by the side's own tree) and
+// the head row (absorbed by Givens rotations).
+static bool carry_free_leaves() {
+  static const bool on = [] {
+    const char* e = getenv("JQ_FOOTNOTE_CARRY");
+    return !(e && !strcmp(e, "scan"));
+  }();
+  return on;
+}
+constexpr int64_t BLOCK_LEAVES_MAX_PER_SM = 32;  // bound on leaves per side (workspace)
+
+static int figaro_r_footnote_blocks(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const double* b,
+                                    int64_t m2, int64_t n2, double* r_out) {
+  const int64_t n = n1 + n2;
+  const int64_t pmax = int64_t(ctx->sms) * BLOCK_LEAVES_MAX_PER_SM;
+  cudaEventRecord(ctx->ev[2], ctx->stream);  // no scan stage
+  double* ra = ws_alloc<double>(ctx, n1 * n1);
+  double* rb = ws_alloc<double>(ctx, n2 * n2);
+  double* rh = ws_alloc<double>(ctx, n * n);
+  double* sums_a = ws_alloc<double>(ctx, pmax * n1);
+  double* sums_b = ws_alloc<double>(ctx, pmax * n2);
+  double* head = ws_alloc<double>(ctx, n);
+  if (!ra || !rb || !rh || !sums_a || !sums_b || !head)
+    return fail(JQ_E_OOM, "workspace exhausted (footnote variant, carry-free leaves)");
+  ctx->record_tsqr_events = false;
+  ctx->timing.tsqr_ctas = 0;
+  ctx->timing.reduced_rows = 0;
+  cudaEventRecord(ctx->ev[3], ctx->stream);
+  FigaroArgs fa{};
+  fa.b = a; fa.m2 = m1; fa.n2 = n1;
+  fa.m1_global = m2; fa.m2_global = m1;
+  fa.blk_sums = sums_a;
+  FigaroArgs fb{};
+  fb.b = b; fb.m2 = m2; fb.n2 = n2;
+  fb.m1_global = m1; fb.m2_global = m2;
+  fb.blk_sums = sums_b;
+  LeafSet la{}, lb{};
+  int rc = figaro_tsqr_leaves(ctx, fa, &la);
+  if (!rc) rc = figaro_tsqr_leaves(ctx, fb, &lb);
+  if (!rc && (la.count > pmax || lb.count > pmax)) rc = fail(JQ_E_INVALID, "too many TSQR leaves for the block sums");
+  if (rc) { ctx->record_tsqr_events = true; return rc; }
+  // between-block rows into each side's stack (zeroed extra elements first)
+  BlockSide sd[2];
+  LeafSet* ls[2] = {&la, &lb};
+  const double* sums[2] = {sums_a, sums_b};
+  const int64_t ms[2] = {m1, m2}, mo[2] = {m2, m1}, ns[2] = {n1, n2};
+  for (int k = 0; k < 2; ++k) {
+    LeafSet& L = *ls[k];
+    const size_t nn = size_t(L.np) * L.np;
+    int64_t first_d = 0;
+    const int64_t cnt = block_stack_layout(L.count, L.np, &first_d);
+    if (cnt > L.count) JQ_CUDA(cudaMemsetAsync(L.leaves + L.count * nn, 0, (cnt - L.count) * nn * 8, ctx->stream));
+    sd[k] = BlockSide{sums[k], L.count, L.rows_per_leaf, ms[k], (int)ns[k], sqrt((double)mo[k]), L.leaves, first_d};
+    L.count = cnt;
+  }
+  block_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], la.np, head);
+  JQ_CHECK_LAUNCH(ctx);
+  rc = tsqr_finish_pair(ctx, la, lb, ra, rb);
+  if (rc) { ctx->record_tsqr_events = true; return rc; }
+  cudaEventRecord(ctx->ev[4], ctx->stream);
+  rc = footnote_small_head(ctx, ra, n1, rb, n2, head, 1, true, rh, r_out);
+  ctx->record_tsqr_events = true;
+  cudaEventRecord(ctx->ev[5], ctx->stream);
+  return rc;
+}
+
 static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
                                  const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
   const bool keyed = ka != nullptr;
@@ -215,6 +336,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   }
   cudaEventRecord(ctx->ev[1], ctx->stream);
   const int64_t cap = keyed ? gr.cap : 1;
+  if (!keyed && n1 > 0 && n2 > 0 && carry_free_leaves()) return figaro_r_footnote_blocks(ctx, a, m1, n1, b, m2, n2, r_out);
   // A's scan in full; the tile pass of B's scan (the HBM-heavy part) runs on the spare
   // warps of A's TSQR leaf (FigaroArgs::side), B's carries right after it
   SegScan sa{}, sb{};

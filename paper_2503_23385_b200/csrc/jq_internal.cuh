@@ -237,6 +237,12 @@ struct FigaroArgs {
   // Cartesian shard extras (jq_figaro_r_shard): global sizes and row offset of B
   int64_t m1_global, m2_global, b_row0;
   SideScan side;                 // tile pass of another scan to run alongside (or nothing)
+  // carry-free leaves (Cartesian footnote): every leaf's row block is its own group --
+  // prefix from 0 at the block start, block row index -- and the leaf writes its block's
+  // column sums to blk_sums[leaf][n2]; the between-block rows replace the carries
+  // (block_heads_kernel).  blk_rows is set by the launcher (the leaf's rows).
+  double* blk_sums;
+  int64_t blk_rows;
 };
 int figaro_tsqr_dev(jq_ctx* ctx, const FigaroArgs& fa, double* r_out, bool canonical);
 // TSQR leaves of a source without their tree (footnote: both sides' trees run in shared
@@ -246,6 +252,7 @@ struct LeafSet {
   double* tmp;     // ceil(count / 2) factors (the single-stack tree's ping-pong buffer)
   int64_t count;
   int np, n;
+  int64_t rows_per_leaf;
 };
 int figaro_tsqr_leaves(jq_ctx* ctx, const FigaroArgs& fa, LeafSet* out);
 int tsqr_finish_pair(jq_ctx* ctx, const LeafSet& x, const LeafSet& y, double* rx, double* ry);

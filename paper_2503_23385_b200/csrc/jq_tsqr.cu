@@ -143,6 +143,8 @@ struct DenseSrc {
                             int, int, int) const {}
   SideScan side_job() const { return SideScan{}; }
   __device__ void side_scan(int, int, int) const {}
+  // after the leaf's last chunk: S holds the running prefix (carry-free leaves export it)
+  __device__ void finish(const double*, int, int) const {}
 };
 
 // Rows of the join matrix generated from A and B in every data warp (brute force; no
@@ -175,10 +177,19 @@ struct FigaroSrc {
     if (brow >= fa.m2) return;
     int64_t tile = brow / TILE_ROWS;
     for (int c = threadIdx.x; c < fa.n2; c += C::THREADS) {
-      double s = fa.b_carry ? fa.b_carry[tile * fa.n2 + c] : 0.0;
-      if (fa.b_prefix0) s += fa.b_prefix0[c];
+      double s = 0.0;
+      if (!fa.blk_rows) {  // carry-free leaves start from 0
+        if (fa.b_carry) s = fa.b_carry[tile * fa.n2 + c];
+        if (fa.b_prefix0) s += fa.b_prefix0[c];
+      }
       S[c] = s;
     }
+  }
+  // Cartesian row index within the group: the global one, or within the leaf's block
+  __device__ int64_t cart_row(int64_t br) const { return fa.blk_rows ? br % fa.blk_rows : fa.b_row0 + br; }
+  __device__ void finish(const double* S, int i0, int stride) const {
+    if (!fa.blk_sums) return;
+    for (int c = i0; c < fa.n2; c += stride) fa.blk_sums[blockIdx.x * fa.n2 + c] = S[c];
   }
   // the tile pass of another segmented scan (fa.side), run by the leaf's spare warps:
   // spare warp si of nsp per CTA takes tiles blockIdx.x * nsp + si, strided by the grid
@@ -237,7 +248,7 @@ struct FigaroSrc {
           valid = g >= 0;
           if (valid) { rr = br - fa.b_start[g]; m1g = (double)fa.a_count[g]; }
         } else {
-          rr = fa.b_row0 + br;
+          rr = cart_row(br);
           m1g = (double)fa.m1_global;
         }
         if (valid) {
@@ -363,7 +374,7 @@ struct FigaroSrc {
           valid = g >= 0;
           if (valid) { rr = br - fa.b_start[g]; m1g = (double)fa.a_count[g]; }
         } else {
-          rr = fa.b_row0 + br;
+          rr = cart_row(br);
           m1g = (double)fa.m1_global;
         }
         if (valid) {
@@ -497,7 +508,7 @@ struct FigaroSrc {
           valid = g >= 0;
           if (valid) { rr = br - fa.b_start[g]; m1g = (double)fa.a_count[g]; }
         } else {
-          rr = fa.b_row0 + br;
+          rr = cart_row(br);
           m1g = (double)fa.m1_global;
         }
         if (valid) {
@@ -1197,6 +1208,7 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
     KT_MARK(4);
   }
   KT_FLUSH();
+  s.finish(S, tid, C::THREADS);
 
   // ---- write R (zeros strictly below the diagonal)
   double* out = r_out + cta * C::NP * C::NP;
@@ -1329,8 +1341,24 @@ size_t figaro_tsqr_ws_bytes(int64_t m1, int64_t m2, int64_t n, int sms) {
   return tsqr_ws_bytes(m1 + m2 + TILE_ROWS, n, sms);
 }
 
+// carry-free leaves: the leaf's row block size goes into the source (FigaroSrc only)
+template <class Src>
+static Src with_block(const Src& s, int64_t) { return s; }
+static FigaroSrc with_block(const FigaroSrc& s, int64_t rows_per_cta) {
+  FigaroSrc t = s;
+  if (t.fa.blk_sums) t.fa.blk_rows = rows_per_cta;
+  return t;
+}
+
+// room behind the leaves for the between-block row elements (block_stack_layout)
+template <class Src>
+static int64_t block_extra(const Src&, int64_t, int) { return 0; }
+static int64_t block_extra(const FigaroSrc& s, int64_t leaves, int np) {
+  return s.fa.blk_sums ? 2 * cdiv(leaves, np) + 2 : 0;
+}
+
 template <class C, class Src>
-static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
+static int run_stream(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t align, int n,
                       bool canonical, double* r_out, int use_tma, LeafSet* defer = nullptr) {
   align = std::max<int64_t>(align, C::K);
   if (align % C::K) return fail(JQ_E_INVALID, "row alignment must be a multiple of the TSQR chunk");
@@ -1339,8 +1367,10 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   int64_t leaves = std::min(max_leaves, units);
   int64_t rows_per_cta = cdiv(units, leaves) * align;
   leaves = std::max<int64_t>(1, cdiv(vrows, rows_per_cta));
-  double* a = ws_alloc<double>(ctx, size_t(leaves) * C::NP * C::NP);
-  double* b = ws_alloc<double>(ctx, size_t((leaves + 1) / 2) * C::NP * C::NP + 1);
+  const Src src = with_block(src_in, rows_per_cta);
+  const int64_t cap = leaves + block_extra(src, leaves, C::NP);
+  double* a = ws_alloc<double>(ctx, size_t(cap) * C::NP * C::NP);
+  double* b = ws_alloc<double>(ctx, size_t((cap + 1) / 2) * C::NP * C::NP + 1);
   if (!a || !b) return fail(JQ_E_OOM, "workspace exhausted (TSQR leaves)");
   ctx->timing.tsqr_ctas += leaves;
   ctx->timing.reduced_rows += vrows;
@@ -1348,7 +1378,7 @@ static int run_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align,
   JQ_TRY(segscan_tiles(ctx, src.side_job()));  // this leaf has no spare warps for it
   JQ_TRY((launch_tsqr<C, Src, false>(ctx, (int)leaves, src, rows_per_cta, vrows, nullptr, 0, a, use_tma)));
   if (defer) {
-    *defer = LeafSet{a, b, leaves, C::NP, n};
+    *defer = LeafSet{a, b, leaves, C::NP, n, rows_per_cta};
     return JQ_OK;
   }
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
@@ -1371,7 +1401,7 @@ static int leaf_impl() {
 }
 
 template <class CS, class Src>
-static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
+static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t align, int n,
                          bool canonical, double* r_out, int use_tma, LeafSet* defer = nullptr) {
   using C = Cfg<CS::NP>;  // tree combine
   static int occ = [] {
@@ -1399,8 +1429,10 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
   int64_t ctas = std::min(max_ctas, units);
   int64_t rows_per_cta = cdiv(units, ctas) * align;
   ctas = std::max<int64_t>(1, cdiv(vrows, rows_per_cta));
-  double* a = ws_alloc<double>(ctx, size_t(ctas) * C::NP * C::NP);
-  double* b = ws_alloc<double>(ctx, size_t((ctas + 1) / 2) * C::NP * C::NP + 1);
+  const Src src = with_block(src_in, rows_per_cta);
+  const int64_t cap = ctas + block_extra(src, ctas, C::NP);
+  double* a = ws_alloc<double>(ctx, size_t(cap) * C::NP * C::NP);
+  double* b = ws_alloc<double>(ctx, size_t((cap + 1) / 2) * C::NP * C::NP + 1);
   if (!a || !b) return fail(JQ_E_OOM, "workspace exhausted (TSQR leaves)");
   ctx->timing.tsqr_ctas += ctas;
   ctx->timing.reduced_rows += vrows;
@@ -1412,7 +1444,7 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t ali
                                                           (use_tma ? 1 : 0) | (explicit_panels ? 2 : 0) | debug_flags);
   JQ_CHECK_LAUNCH(ctx);
   if (defer) {
-    *defer = LeafSet{a, b, ctas, C::NP, n};
+    *defer = LeafSet{a, b, ctas, C::NP, n, rows_per_cta};
     return JQ_OK;
   }
   if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);

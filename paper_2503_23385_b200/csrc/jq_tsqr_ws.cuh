@@ -267,6 +267,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       TR(2, 3);
       if (li == 0 && lane == 0) mbar_arrive(bar_ready);
     }
+    if (li == 0) src.finish(S, lane, 32);  // S final: prep_warp's __syncwarp / the last BAR_LOAD
     return;
   }
 

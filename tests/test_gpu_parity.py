@@ -177,7 +177,11 @@ def variant(request, P):
     # with many more tiles than A has spare warps, keyed groups spanning tiles
     (2000, 50, 50000, 60, None), (3000, 40, 40000, 56, 30), (30000, 48, 25000, 40, 70),
     # footnote with few join groups: head rows absorbed by Givens rotations
-    (5000, 20, 4000, 24, 3), (3000, 100, 3000, 120, 5)])
+    (5000, 20, 4000, 24, 3), (3000, 100, 3000, 120, 5),
+    # Cartesian footnote, carry-free leaves: many between-block row elements (NP = 16,
+    # sides with different leaf counts: separate trees), an odd leaf count (147 leaves,
+    # three dense elements, both trees in shared launches), a partial last block
+    (200000, 8, 150000, 12, None), (150001, 64, 150001, 64, None)])
 def test_figaro_r_matches_oracle(P, variant, m1, n1, m2, n2, groups):
     rng = np.random.default_rng(m1 + 3 * m2 + n1 + (groups or 0))
     a, b = rand_tables(rng, m1, n1, m2, n2, groups)
@@ -187,6 +191,30 @@ def test_figaro_r_matches_oracle(P, variant, m1, n1, m2, n2, groups):
         check_r(r, O.canonicalize(O.householder_r_lapack(red)))
     g = O.gram(red)
     assert np.abs(r.T @ r - g).max() <= 1e-10 * max(1, np.abs(g).max())
+
+
+@pytest.mark.parametrize("m,n", [(150001, 64), (70000, 128), (3000, 20)])
+def test_carry_free_leaves_match_scan_carried(P, m, n):
+    """The Cartesian footnote default (carry-free leaves + between-block rows) against
+    the scan-carried leaves (JQ_FOOTNOTE_CARRY=scan, read once per process: run in a
+    child process) on the same device-generated tables: same R to rounding."""
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, %r); import paper_2503_23385_b200 as P; "
+            "from paper_2503_23385_b200 import datagen; P.set_variant('footnote'); "
+            "A = torch.empty((%d, %d), dtype=torch.float64, device='cuda'); B = torch.empty_like(A); "
+            "datagen.uniform(11, %d, %d, out=A); datagen.uniform(12, %d, %d, out=B); "
+            "np.save(sys.argv[1], P.figaro_r(P.Table(A), P.Table(B)).cpu().numpy())"
+            % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), m, n, m, n, m, n))
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        out = {}
+        for mode in ("scan", "blocks"):
+            f = os.path.join(d, mode + ".npy")
+            env = dict(os.environ, JQ_FOOTNOTE_CARRY=mode)
+            subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=300)
+            out[mode] = np.load(f)
+    check_r(out["blocks"], out["scan"], tol=1e-12)
 
 
 def test_figaro_r_empty_join_and_materialised(P, variant):
