@@ -44,10 +44,10 @@ CONFIGS = {
 }
 METRIC = "join rows/sec (m1*m2/t), time-to-R"
 # dram__bytes_read.sum + dram__bytes_write.sum per leaf-kernel launch (ncu --set full)
-NCU_TRAFFIC = {(4, "footnote"): {"bytes": 102.441363e9 + 113.473024e6,
-                                 "note": "first tsqr_ws2_kernel launch (side A, capture v10): its own 1e8 x 64 f64 "
-                                         "rows (51.2e9 algorithmic bytes) + side B's scan tile pass on the spare "
-                                         "warps (51.2e9): every byte read once; profiles/r01_ncu_ws2_c4.md"}}
+NCU_TRAFFIC = {(4, "footnote"): {"bytes": 51.218381e9 + 11.232512e6,
+                                 "note": "first tsqr_ws2_kernel launch (side A, carry-free leaves, capture v12): its "
+                                         "own 1e8 x 64 f64 rows = 51.2e9 algorithmic bytes, every byte read once; "
+                                         "profiles/r01_ncu_ws2_c4.md"}}
 
 
 def peaks():
@@ -338,7 +338,14 @@ def main():
         # one side in the scan interval: dense scans B only (Claim 1); footnote scans A there
         # and runs B's tile pass inside A's TSQR interval (spare warps of the leaf)
         sides = 1
-        gbs = (8.0 * m * n * sides) / (stage_avg["scan_ms"] / 1e3) / 1e9 if stage_avg["scan_ms"] > 0 else None
+        gbs = (8.0 * m * n * sides) / (stage_avg["scan_ms"] / 1e3) / 1e9 if stage_avg["scan_ms"] > 0.05 else None
+        if gbs is None:
+            # Cartesian footnote default: carry-free leaves, no prefix-scan pass in the step
+            roof_hbm = {"kernel": None, "bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "note": "no HBM-bound pass in this step: the carry-free TSQR leaves transform their own "
+                                "row blocks in the loader warp (every input byte read once, by TMA); the head/tail "
+                                "kernels' own roofline (reduced-matrix API, keyed configs) is in "
+                                "profiles/r01_ncu_headtail.md and the C3 line"}
         if gbs:
             roof_hbm = {"kernel": "segscan (head/tail prefix pass, tile sums + carry scan)", "bound": "hbm",
                         "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
