@@ -440,6 +440,96 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   return rc;
 }
 
+// The shard's own between-shard row per side (carry-free leaves on a row shard): the
+// shard is block number k of the global group with W = row0 rows and column sums
+// `prefix` before it, and local sums s = sum of its leaves' block sums (fixed order), so
+//   v = scale sqrt(W m / (W + m)) (s / m - prefix / W)      (W > 0; none for shard 0).
+// rows[0] = [v_A | 0], rows[1] = [0 | v_B]; a side with W = 0 gets a zero row.
+__global__ void shard_rows_kernel(BlockSide sa, const double* __restrict__ pre_a, int64_t row0_a, BlockSide sb,
+                                  const double* __restrict__ pre_b, int64_t row0_b, double* __restrict__ rows) {
+  const int n = sa.nc + sb.nc;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const bool side_a = c < sa.nc;
+  const BlockSide& sd = side_a ? sa : sb;
+  const int cc = side_a ? c : c - sa.nc;
+  double sl = 0.0;
+  for (int64_t k = 0; k < sd.p; ++k) sl += sd.sums[k * sd.nc + cc];
+  const double W = (double)(side_a ? row0_a : row0_b), ml = (double)sd.m;
+  const double* pre = side_a ? pre_a : pre_b;
+  const double v = (W > 0.0 && ml > 0.0) ? sd.scale * sqrt(W * ml / (W + ml)) * (sl / ml - pre[cc] / W) : 0.0;
+  rows[(side_a ? 0 : n) + c] = v;
+  rows[(side_a ? n : 0) + c] = 0.0;
+}
+
+// Carry-free leaves on one Cartesian row shard: the shard's leaves take their blocks as
+// groups (block_rows_kernel: within-shard between-block rows into the shard's trees),
+// shard_rows_kernel adds the shard's own between-shard row per side (from a_prefix /
+// a_row0, b_prefix / b_row0), and shard 0 adds the global head row: at most three rows
+// for the Givens absorb.  The stacked shard R's then have the Gram of the whole join.
+static int footnote_shard_blocks(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1,
+                                 int64_t a_row0, const double* a_prefix, const double* a_total, const double* b,
+                                 int64_t b_rows, int64_t n2, int64_t m2, int64_t b_row0, const double* b_prefix,
+                                 const double* b_total, bool include_head, double* r_out) {
+  const int64_t n = n1 + n2;
+  const int64_t pmax = int64_t(ctx->sms) * BLOCK_LEAVES_MAX_PER_SM;
+  cudaEventRecord(ctx->ev[2], ctx->stream);  // no scan stage
+  double* ra = ws_alloc<double>(ctx, n1 * n1);
+  double* rb = ws_alloc<double>(ctx, n2 * n2);
+  double* rh = ws_alloc<double>(ctx, n * n);
+  double* sums_a = ws_alloc<double>(ctx, pmax * n1);
+  double* sums_b = ws_alloc<double>(ctx, pmax * n2);
+  double* rows = ws_alloc<double>(ctx, 3 * n);
+  if (!ra || !rb || !rh || !sums_a || !sums_b || !rows)
+    return fail(JQ_E_OOM, "workspace exhausted (footnote shard, carry-free leaves)");
+  ctx->record_tsqr_events = false;
+  cudaEventRecord(ctx->ev[3], ctx->stream);
+  FigaroArgs fa{};
+  fa.b = a; fa.m2 = a_rows; fa.n2 = n1;
+  fa.m1_global = m2; fa.m2_global = m1;
+  fa.blk_sums = sums_a;
+  FigaroArgs fb{};
+  fb.b = b; fb.m2 = b_rows; fb.n2 = n2;
+  fb.m1_global = m1; fb.m2_global = m2;
+  fb.blk_sums = sums_b;
+  LeafSet la{}, lb{};
+  int rc = figaro_tsqr_leaves(ctx, fa, &la);
+  if (!rc) rc = figaro_tsqr_leaves(ctx, fb, &lb);
+  if (!rc && (la.count > pmax || lb.count > pmax)) rc = fail(JQ_E_INVALID, "too many TSQR leaves for the block sums");
+  if (rc) { ctx->record_tsqr_events = true; return rc; }
+  BlockSide sd[2];
+  LeafSet* ls[2] = {&la, &lb};
+  const double* sums[2] = {sums_a, sums_b};
+  const int64_t ms[2] = {a_rows, b_rows}, mo[2] = {m2, m1}, ns[2] = {n1, n2};
+  for (int k = 0; k < 2; ++k) {
+    LeafSet& L = *ls[k];
+    const size_t nn = size_t(L.np) * L.np;
+    int64_t first_d = 0;
+    const int64_t cnt = block_stack_layout(L.count, L.np, &first_d);
+    if (cnt > L.count) JQ_CUDA(cudaMemsetAsync(L.leaves + L.count * nn, 0, (cnt - L.count) * nn * 8, ctx->stream));
+    sd[k] = BlockSide{sums[k], L.count, L.rows_per_leaf, ms[k], (int)ns[k], sqrt((double)mo[k]), L.leaves, first_d};
+  }
+  // the shard's rows (uses the leaf counts before the layout change), then the blocks'
+  shard_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], a_prefix, a_row0, sd[1], b_prefix,
+                                                                    b_row0, rows + (include_head ? n : 0));
+  JQ_CHECK_LAUNCH(ctx);
+  block_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], la.np, rh);  // rh: scratch head
+  JQ_CHECK_LAUNCH(ctx);
+  for (int k = 0; k < 2; ++k) ls[k]->count = block_stack_layout(ls[k]->count, ls[k]->np, &sd[k].first_d);
+  rc = tsqr_finish_pair(ctx, la, lb, ra, rb);
+  if (rc) { ctx->record_tsqr_events = true; return rc; }
+  cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (include_head) {
+    head_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(a_total, (int)n1, b_total, (int)n2, nullptr,
+                                                                        nullptr, 1, m1, m2, rows);
+    JQ_CHECK_LAUNCH(ctx);
+  }
+  rc = footnote_small_head(ctx, ra, n1, rb, n2, rows, include_head ? 3 : 2, false, rh, r_out);
+  ctx->record_tsqr_events = true;
+  cudaEventRecord(ctx->ev[5], ctx->stream);
+  return rc;
+}
+
 // Footnote variant on one Cartesian row shard: tails of the local A rows (global
 // row index a_row0 + i, prefix a_prefix, scale sqrt(m2)) and of the local B rows,
 // plus the global head row when include_head.  Output: local R (n x n, not canonical).
@@ -448,6 +538,9 @@ static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int6
                               int64_t n2, int64_t m2, int64_t b_row0, const double* b_prefix,
                               const double* b_total, bool include_head, double* r_out) {
   const int64_t n = n1 + n2;
+  if (n1 > 0 && n2 > 0 && carry_free_leaves())
+    return footnote_shard_blocks(ctx, a, a_rows, n1, m1, a_row0, a_prefix, a_total, b, b_rows, n2, m2, b_row0,
+                                 b_prefix, b_total, include_head, r_out);
   SegScan sa{}, sb{};
   SideScan side_b;  // B's tile pass on the spare warps of A's leaf (as in figaro_r_footnote_dev)
   if (n1 > 0) JQ_TRY(segscan_dev(ctx, a, a_rows, n1, nullptr, nullptr, nullptr, nullptr, 1, &sa));
