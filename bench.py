@@ -259,6 +259,8 @@ def main():
                 return P.figaro_svd(P.Table(A, ka), P.Table(B, kb), want_vectors=True).values
             return P.figaro_r(P.Table(A, ka), P.Table(B, kb))
         from paper_2503_23385_b200 import sharded
+        if N.get_variant() == "footnote":
+            return sharded.figaro_r_sharded_local(A, B, m, m, a0, a0)  # one all-gather (R + sums) over NCCL
         return sharded.figaro_r_sharded(A, B, m, m, a0, a0)   # carry + R all-gathers over NCCL
 
     def timed(variant, steps):

@@ -150,6 +150,17 @@ JQ_API int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64
                              const double* b, int64_t b_rows, int64_t n2, int64_t m2, int64_t b_row0,
                              const double* b_prefix, const double* b_total, int include_head,
                              double* r_local);
+/* Footnote variant with carry-free leaves on one Cartesian row shard (A rows
+ * a_rows of an m1-row table, B rows b_rows of an m2-row table, n1, n2 > 0): the
+ * shard's local R (its blocks' tails and between-block rows, scaled by sqrt(m2) /
+ * sqrt(m1); no head row, no between-shard row) and sums[n1 + n2] = the shard's
+ * column sums (A then B).  Needs no prefix: the between-shard rows and the head row
+ * follow from the all-gathered sums (paper_2503_23385_b200/sharded.py), so one
+ * all-gather carries R and sums.  Replaces the carry exchange of jq_figaro_r_shard
+ * for the same R (SPEC.md:278-286 by Gram). */
+JQ_API int jq_figaro_r_shard_local(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1,
+                                   const double* b, int64_t b_rows, int64_t n2, int64_t m2, double* r_local,
+                                   double* sums);
 /* Canonical R of the row stack [R_0; R_1; ...; R_{count-1}] (each n x n), by
  * the fixed binary TSQR tree — identical on every rank for the same input. */
 JQ_API int jq_tsqr_stack(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, double* r);

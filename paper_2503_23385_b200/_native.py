@@ -47,6 +47,7 @@ SIGNATURES = {
     "jq_gen_zipf_sorted_keys": [_P, C.c_uint64, _I64, _P, _I64, _P],
     "jq_colsums": [_P, _P, _I64, _I64, _P],
     "jq_figaro_r_shard": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, C.c_int, _P],
+    "jq_figaro_r_shard_local": [_P, _P, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P, _P],
     "jq_tsqr_stack": [_P, _P, _I64, _I64, _P],
     "jq_materialize": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _P, _I64, _P],
     "jq_join_r_bruteforce": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _P],
@@ -108,6 +109,10 @@ def set_device(device: int) -> None:
 
 VARIANTS = {"dense": 0, "footnote": 1, "auto": 2}
 _variant = VARIANTS[os.environ.get("JOINQR_VARIANT", "auto")]
+
+
+def get_variant() -> str:
+    return {v: k for k, v in VARIANTS.items()}[_variant]
 
 
 def set_variant(name: str) -> None:

@@ -462,6 +462,17 @@ __global__ void shard_rows_kernel(BlockSide sa, const double* __restrict__ pre_a
   rows[(side_a ? n : 0) + c] = 0.0;
 }
 
+// Column sums of the shard (A then B) from its leaves' block sums, in block order.
+__global__ void block_total_kernel(BlockSide sa, BlockSide sb, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= sa.nc + sb.nc) return;
+  const BlockSide& sd = c < sa.nc ? sa : sb;
+  const int cc = c < sa.nc ? c : c - sa.nc;
+  double t = 0.0;
+  for (int64_t k = 0; k < sd.p; ++k) t += sd.sums[k * sd.nc + cc];
+  out[c] = t;
+}
+
 // Carry-free leaves on one Cartesian row shard: the shard's leaves take their blocks as
 // groups (block_rows_kernel: within-shard between-block rows into the shard's trees),
 // shard_rows_kernel adds the shard's own between-shard row per side (from a_prefix /
@@ -470,7 +481,8 @@ __global__ void shard_rows_kernel(BlockSide sa, const double* __restrict__ pre_a
 static int footnote_shard_blocks(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1,
                                  int64_t a_row0, const double* a_prefix, const double* a_total, const double* b,
                                  int64_t b_rows, int64_t n2, int64_t m2, int64_t b_row0, const double* b_prefix,
-                                 const double* b_total, bool include_head, double* r_out) {
+                                 const double* b_total, bool include_head, double* r_out,
+                                 double* sums_out = nullptr) {
   const int64_t n = n1 + n2;
   const int64_t pmax = int64_t(ctx->sms) * BLOCK_LEAVES_MAX_PER_SM;
   cudaEventRecord(ctx->ev[2], ctx->stream);  // no scan stage
@@ -515,6 +527,10 @@ static int footnote_shard_blocks(jq_ctx* ctx, const double* a, int64_t a_rows, i
   JQ_CHECK_LAUNCH(ctx);
   block_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], la.np, rh);  // rh: scratch head
   JQ_CHECK_LAUNCH(ctx);
+  if (sums_out) {
+    block_total_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], sums_out);
+    JQ_CHECK_LAUNCH(ctx);
+  }
   for (int k = 0; k < 2; ++k) ls[k]->count = block_stack_layout(ls[k]->count, ls[k]->np, &sd[k].first_d);
   rc = tsqr_finish_pair(ctx, la, lb, ra, rb);
   if (rc) { ctx->record_tsqr_events = true; return rc; }
@@ -1006,6 +1022,37 @@ int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, 
   }
   JQ_TRY(copy_out(ctx, r_local, (const double*)dr, n * n));
   rc = sync_and_check_flags(ctx);
+  record_timing(ctx, false);
+  return rc;
+}
+
+int jq_figaro_r_shard_local(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1, const double* b,
+                            int64_t b_rows, int64_t n2, int64_t m2, double* r_local, double* sums) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (a_rows <= 0 || b_rows <= 0 || n1 <= 0 || n2 <= 0 || n1 + n2 > 256)
+    return fail(JQ_E_INVALID, "bad shard geometry (both sides need rows and columns)");
+  if (m1 < a_rows || m2 < b_rows) return fail(JQ_E_INVALID, "bad global sizes for the shard");
+  if (!r_local || !sums) return fail(JQ_E_INVALID, "null output");
+  JQ_TRY(begin_call(ctx));
+  const int64_t n = n1 + n2;
+  JQ_TRY(ws_reserve(ctx, stage_bytes(a, a_rows * n1) + stage_bytes(b, b_rows * n2) +
+                             stage_bytes((const double*)r_local, n * n) + stage_bytes((const double*)sums, n) +
+                             figaro_ws(a_rows, n1, b_rows, n2, false, ctx->sms)));
+  const double *da, *db;
+  double *dr, *ds;
+  JQ_TRY(stage_in(ctx, a, a_rows * n1, &da));
+  JQ_TRY(stage_in(ctx, b, b_rows * n2, &db));
+  JQ_TRY(stage_out(ctx, r_local, n * n, &dr));
+  JQ_TRY(stage_out(ctx, sums, n, &ds));
+  ctx->timing.tsqr_ctas = 0;
+  ctx->timing.reduced_rows = 0;
+  cudaEventRecord(ctx->ev[0], ctx->stream);
+  cudaEventRecord(ctx->ev[1], ctx->stream);
+  JQ_TRY(footnote_shard_blocks(ctx, da, a_rows, n1, m1, 0, nullptr, nullptr, db, b_rows, n2, m2, 0, nullptr, nullptr,
+                               false, dr, ds));
+  JQ_TRY(copy_out(ctx, r_local, (const double*)dr, n * n));
+  JQ_TRY(copy_out(ctx, sums, (const double*)ds, n));
+  const int rc = sync_and_check_flags(ctx);
   record_timing(ctx, false);
   return rc;
 }

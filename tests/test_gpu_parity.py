@@ -333,6 +333,34 @@ def test_shard_r_and_stack_equal_single_device(P, variant):
         P.set_variant("dense")
 
 
+@pytest.mark.parametrize("m1,n1,m2,n2", [(5000, 6, 7000, 5), (300000, 64, 250000, 64), (40000, 128, 40000, 128)])
+def test_shard_local_carry_free_equal_single_device(P, m1, n1, m2, n2):
+    """Carry-free shards (jq_figaro_r_shard_local + between_shard_rows + the stack):
+    the orchestration of sharded.figaro_r_sharded_local, ranks played in turn on one
+    device, == unsharded figaro_r."""
+    import torch
+    from paper_2503_23385_b200 import sharded
+    rng = np.random.default_rng(m1 + n1)
+    A, B = rng.random((m1, n1)), rng.random((m2, n2))
+    n = n1 + n2
+    ref = np.asarray(P.figaro_r(P.Table(A), P.Table(B)))
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    for parts in (1, 2, 3, 8):
+        rs, sums = [], []
+        for p in range(parts):
+            a0, a1 = sharded.shard_range(m1, parts, p)
+            b0, b1 = sharded.shard_range(m2, parts, p)
+            r, s = sharded._native_shard_local(dA[a0:a1].contiguous(), dB[b0:b1].contiguous(), m1, m2)
+            rs.append(r)
+            sums.append(s)
+        sizes_a = [sharded.shard_range(m1, parts, p)[1] - sharded.shard_range(m1, parts, p)[0] for p in range(parts)]
+        sizes_b = [sharded.shard_range(m2, parts, p)[1] - sharded.shard_range(m2, parts, p)[0] for p in range(parts)]
+        extra = sharded._native_householder(
+            sharded.between_shard_rows(torch.stack(sums), sizes_a, sizes_b, m1, m2, n1).contiguous())
+        r = sharded._native_stack(torch.cat([torch.stack(rs), extra.reshape(1, n, n)]).contiguous())
+        check_r(r.cpu().numpy(), ref, 1e-12)
+
+
 def test_colsums(P):
     from paper_2503_23385_b200 import _native as N
     x = np.random.default_rng(1).random((10_000, 40))

@@ -47,6 +47,21 @@ def cpu_shard_r(a, b, m1, m2, a_row0, b_row0, a_prefix, a_total, prefix, total, 
     return torch.from_numpy(O.householder_r_lapack(red))
 
 
+def cpu_shard_local(a, b, m1, m2):
+    """Carry-free shard (jq_figaro_r_shard_local): the shard's own tails of A (scale
+    sqrt(m2)) and of B (scale sqrt(m1)) -- the shard is one block -- and its sums."""
+    a, b = a.numpy(), b.numpy()
+    n1, n2 = a.shape[1], b.shape[1]
+    ta, tb = O.tail(a) * np.sqrt(m2), O.tail(b) * np.sqrt(m1)
+    red = np.vstack([np.hstack([ta, np.zeros((len(ta), n2))]), np.hstack([np.zeros((len(tb), n1)), tb])])
+    r = O.householder_r_lapack(red) if len(red) else np.zeros((n1 + n2, n1 + n2))
+    return torch.from_numpy(r), torch.from_numpy(np.concatenate([a.sum(0), b.sum(0)]))
+
+
+def cpu_householder(rows):
+    return torch.from_numpy(O.householder_r_lapack(rows.numpy()))
+
+
 def cpu_stack(rs):
     return torch.from_numpy(O.canonicalize(O.householder_r_lapack(rs.reshape(-1, rs.shape[-1]).numpy())))
 
@@ -62,6 +77,10 @@ def _worker(rank, world, port, m1, m2, n1, n2, out):
     r = sharded.figaro_r_sharded(torch.from_numpy(A[a0:a1].copy()), torch.from_numpy(B[b0:b1].copy()),
                                  m1, m2, a0, b0, colsums=cpu_colsums, shard_r=cpu_shard_r, stack=cpu_stack)
     out[rank] = r.numpy().tolist()
+    r2 = sharded.figaro_r_sharded_local(torch.from_numpy(A[a0:a1].copy()), torch.from_numpy(B[b0:b1].copy()),
+                                        m1, m2, a0, b0, shard_local=cpu_shard_local, householder=cpu_householder,
+                                        stack=cpu_stack)
+    out[("local", rank)] = r2.numpy().tolist()
     dist.destroy_process_group()
 
 
@@ -80,3 +99,10 @@ def test_sharded_matches_single(world, m1, m2, n1, n2):
     assert np.abs(rs[0].T @ rs[0] - g).max() <= 1e-10 * np.abs(g).max()
     if m1 + m2 - 1 >= n1 + n2:
         assert np.linalg.norm(np.abs(rs[0]) - np.abs(ref)) <= 1e-10 * np.linalg.norm(ref)
+    # carry-free shards: one all-gather of R + sums, between-shard rows on every rank
+    rl = [np.array(out[("local", r)]) for r in range(world)]
+    for r in rl[1:]:
+        assert np.array_equal(r, rl[0]), "ranks must hold the identical R (carry-free shards)"
+    assert np.abs(rl[0].T @ rl[0] - g).max() <= 1e-10 * np.abs(g).max()
+    if m1 + m2 - 1 >= n1 + n2:
+        assert np.linalg.norm(np.abs(rl[0]) - np.abs(ref)) <= 1e-10 * np.linalg.norm(ref)
