@@ -138,12 +138,14 @@ struct BlockSide {
   double scale;       // sqrt(rows of the other side)
   double* stack;      // the side's leaf stack (p leaves, then the extra elements)
   int64_t first_d;    // stack index of the first dense element
+  int np;             // the side's leaf width (stack elements are np x np)
 };
-__global__ void block_rows_kernel(BlockSide sa, BlockSide sb, int np, double* __restrict__ head) {
+__global__ void block_rows_kernel(BlockSide sa, BlockSide sb, double* __restrict__ head) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= sa.nc + sb.nc) return;
   const BlockSide& sd = c < sa.nc ? sa : sb;
   const int cc = c < sa.nc ? c : c - sa.nc;
+  const int np = sd.np;
   const size_t nn = size_t(np) * np;
   double W = 0.0, Sk = 0.0;
   for (int64_t k = 0; k < sd.p; ++k) {
@@ -306,10 +308,11 @@ static int figaro_r_footnote_blocks(jq_ctx* ctx, const double* a, int64_t m1, in
     int64_t first_d = 0;
     const int64_t cnt = block_stack_layout(L.count, L.np, &first_d);
     if (cnt > L.count) JQ_CUDA(cudaMemsetAsync(L.leaves + L.count * nn, 0, (cnt - L.count) * nn * 8, ctx->stream));
-    sd[k] = BlockSide{sums[k], L.count, L.rows_per_leaf, ms[k], (int)ns[k], sqrt((double)mo[k]), L.leaves, first_d};
+    sd[k] = BlockSide{sums[k], L.count, L.rows_per_leaf, ms[k], (int)ns[k], sqrt((double)mo[k]), L.leaves, first_d,
+                     L.np};
     L.count = cnt;
   }
-  block_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], la.np, head);
+  block_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], head);
   JQ_CHECK_LAUNCH(ctx);
   rc = tsqr_finish_pair(ctx, la, lb, ra, rb);
   if (rc) { ctx->record_tsqr_events = true; return rc; }
@@ -519,13 +522,14 @@ static int footnote_shard_blocks(jq_ctx* ctx, const double* a, int64_t a_rows, i
     int64_t first_d = 0;
     const int64_t cnt = block_stack_layout(L.count, L.np, &first_d);
     if (cnt > L.count) JQ_CUDA(cudaMemsetAsync(L.leaves + L.count * nn, 0, (cnt - L.count) * nn * 8, ctx->stream));
-    sd[k] = BlockSide{sums[k], L.count, L.rows_per_leaf, ms[k], (int)ns[k], sqrt((double)mo[k]), L.leaves, first_d};
+    sd[k] = BlockSide{sums[k], L.count, L.rows_per_leaf, ms[k], (int)ns[k], sqrt((double)mo[k]), L.leaves, first_d,
+                     L.np};
   }
   // the shard's rows (uses the leaf counts before the layout change), then the blocks'
   shard_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], a_prefix, a_row0, sd[1], b_prefix,
                                                                     b_row0, rows + (include_head ? n : 0));
   JQ_CHECK_LAUNCH(ctx);
-  block_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], la.np, rh);  // rh: scratch head
+  block_rows_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], rh);  // rh: scratch head
   JQ_CHECK_LAUNCH(ctx);
   if (sums_out) {
     block_total_kernel<<<(unsigned)cdiv(n, 128), 128, 0, ctx->stream>>>(sd[0], sd[1], sums_out);

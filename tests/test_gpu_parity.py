@@ -181,7 +181,9 @@ def variant(request, P):
     # Cartesian footnote, carry-free leaves: many between-block row elements (NP = 16,
     # sides with different leaf counts: separate trees), an odd leaf count (147 leaves,
     # three dense elements, both trees in shared launches), a partial last block
-    (200000, 8, 150000, 12, None), (150001, 64, 150001, 64, None)])
+    (200000, 8, 150000, 12, None), (150001, 64, 150001, 64, None),
+    # sides of different leaf widths (NP 64 ws2 leaves / NP 128 CTA-wide leaves)
+    (200000, 40, 150000, 100, None)])
 def test_figaro_r_matches_oracle(P, variant, m1, n1, m2, n2, groups):
     rng = np.random.default_rng(m1 + 3 * m2 + n1 + (groups or 0))
     a, b = rand_tables(rng, m1, n1, m2, n2, groups)
