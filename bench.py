@@ -358,7 +358,9 @@ def main():
 
     # ---- end-to-end through the public API with host buffers (N=1)
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if sharded_path and not args.no_e2e:
+        e2e = run_e2e_sharded(args, A, B, m, a0, jrows, world, device)
+    elif world == 1 and not args.no_e2e:
         host = to_host(A, B, ka, kb)
         del A, B
         A = B = None
@@ -437,6 +439,61 @@ def run_e2e(args, host, jrows):
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(r.nbytes),
                 "pinned": bool(host["A"][1] and host["B"][1]),
                 "api": "paper_2503_23385_b200.figaro_r(Table(numpy), Table(numpy)) -> jq_figaro_r"}
+    finally:
+        for key in ("A", "B"):
+            h, pinned = host[key]
+            if pinned:
+                cudart.cudaHostUnregister(h.ctypes.data)
+
+
+def run_e2e_sharded(args, A, B, m, a0, jrows, world, device):
+    """Multi-GPU end to end through the public sharded API (paper_2503_23385_b200.sharded):
+    every rank copies its own row shards of A and B from page-locked host memory into
+    HBM, runs figaro_r_sharded_local (local carry-free leaves, one NCCL all-gather, the
+    fixed tree) and reads R back to the host -- all inside the timed region.  Timed with
+    CUDA events on the launching stream around the whole step (the D2H of R synchronises),
+    max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_23385_b200 import sharded
+    from paper_2503_23385_b200 import _native as N
+    host = to_host(A, B, None, None)
+    cudart = torch.cuda.cudart()
+    try:
+        ha, hb = torch.from_numpy(host["A"][0]), torch.from_numpy(host["B"][0])
+        stream = torch.cuda.current_stream()
+
+        def step():
+            A.copy_(ha, non_blocking=True)
+            B.copy_(hb, non_blocking=True)
+            N.use_torch_stream(A)
+            if N.get_variant() == "footnote":
+                r = sharded.figaro_r_sharded_local(A, B, m, m, a0, a0)
+            else:
+                r = sharded.figaro_r_sharded(A, B, m, m, a0, a0)
+            return r.cpu()
+
+        step()                                   # warm-up
+        torch.cuda.synchronize()
+        dist.barrier()
+        nsteps = max(1, min(args.steps, 3))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(nsteps):
+            r = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / nsteps], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        return {"value": jrows / (ms / 1e3), "unit": "join rows/s", "ms_per_step": ms, "steps": nsteps,
+                "h2d_bytes_per_step": int(host["A"][0].nbytes + host["B"][0].nbytes),
+                "d2h_bytes_per_step": int(r.numpy().nbytes),
+                "per_rank": True, "pinned": bool(host["A"][1] and host["B"][1]),
+                "note": "per rank: its own shards' H2D and R's D2H (bytes above are one rank's); "
+                        "time = max over ranks; H2D not overlapped with the leaves on this path",
+                "api": "paper_2503_23385_b200.sharded.figaro_r_sharded_local (torch.distributed NCCL)"}
     finally:
         for key in ("A", "B"):
             h, pinned = host[key]
