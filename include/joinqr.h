@@ -62,6 +62,8 @@ typedef struct jq_timing {
   double total_ms;   /* first event to last event                            */
   int64_t tsqr_ctas; /* leaves of the TSQR tree                              */
   int64_t reduced_rows; /* rows streamed into the TSQR (incl. zero padding)  */
+  double scan_tile_ms;    /* the head/tail tile-pass kernel(s) alone (<= 4 launches) */
+  double scan_tile_bytes; /* their algorithmic bytes (rows read once + segment ids)  */
 } jq_timing;
 
 /* ---- library / context ------------------------------------------------- */

@@ -58,7 +58,8 @@ _RESTYPE = {"jq_last_error": C.c_char_p, "jq_kernel_launches": C.c_int64}
 class JqTiming(C.Structure):
     _fields_ = [("group_ms", C.c_double), ("scan_ms", C.c_double), ("tsqr_ms", C.c_double),
                 ("tree_ms", C.c_double), ("svd_ms", C.c_double), ("total_ms", C.c_double),
-                ("tsqr_ctas", C.c_int64), ("reduced_rows", C.c_int64)]
+                ("tsqr_ctas", C.c_int64), ("reduced_rows", C.c_int64),
+                ("scan_tile_ms", C.c_double), ("scan_tile_bytes", C.c_double)]
 
 
 _lib = None

@@ -60,6 +60,8 @@ int ws_reserve(jq_ctx* ctx, size_t bytes) {
 int begin_call(jq_ctx* ctx) {
   JQ_CUDA(cudaSetDevice(ctx->device));
   ws_reset(ctx);
+  ctx->tile_launches = 0;
+  ctx->tile_bytes = 0.0;
   JQ_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), ctx->stream));
   return JQ_OK;
 }
@@ -787,6 +789,16 @@ static void record_timing(jq_ctx* ctx, bool svd) {
   t.tree_ms = ev_ms(ctx, 4, 5);
   t.svd_ms = svd ? ev_ms(ctx, 5, 6) : 0.0;
   t.total_ms = ev_ms(ctx, 0, svd ? 6 : 5);
+  t.scan_tile_ms = 0.0;
+  for (int k = 0; k < ctx->tile_launches; ++k) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->tev[2 * k], ctx->tev[2 * k + 1]) != cudaSuccess) {
+      cudaGetLastError();
+      ms = 0.f;
+    }
+    t.scan_tile_ms += ms;
+  }
+  t.scan_tile_bytes = ctx->tile_launches ? ctx->tile_bytes : 0.0;
 }
 
 static int check_tables(int64_t m1, int64_t n1, const int64_t* ka, int64_t m2, int64_t n2, const int64_t* kb) {
@@ -828,6 +840,7 @@ int jq_ctx_create(int device, jq_ctx** out) {
   JQ_CUDA(cudaMalloc(&ctx->d_flags, sizeof(int)));
   JQ_CUDA(cudaMallocHost(&ctx->h_flags, sizeof(int)));
   for (auto& e : ctx->ev) JQ_CUDA(cudaEventCreate(&e));
+  for (auto& e : ctx->tev) JQ_CUDA(cudaEventCreate(&e));
   *out = ctx;
   return JQ_OK;
 }
@@ -840,6 +853,7 @@ int jq_ctx_destroy(jq_ctx* ctx) {
   if (ctx->d_flags) cudaFree(ctx->d_flags);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->tev) if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);

@@ -33,6 +33,25 @@ __global__ void __launch_bounds__(256) segscan_tile_kernel(
   segscan_tile(x, rows, cols, gid, t, agg, flag, totals, lane);
 }
 
+// <= 64 columns: the narrow tile pass (fewer registers -> more warps, 16 rows in flight)
+template <int SL>
+__global__ void __launch_bounds__(256, 4) segscan_tile_narrow_kernel(
+    const double* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ gid,
+    int64_t ntiles, double* __restrict__ agg, int* __restrict__ flag, double* __restrict__ totals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= ntiles) return;
+  segscan_tile_narrow<SL == 1 ? 16 : 8, SL>(x, rows, cols, gid, t, agg, flag, totals, lane);  // 4 KB per warp in flight
+}
+
+static bool narrow_tiles() {
+  static const bool on = [] {
+    const char* e = getenv("JQ_SEGSCAN_GENERIC");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 // Segmented carry over tiles, two-level with FIXED association (deterministic):
 //   carry[0] = 0; carry[t+1] = flag[t] ? agg[t] : carry[t] + agg[t]
 // Level 1: thread (column, block of CB tiles) folds its block into (flag, sum);
@@ -162,9 +181,24 @@ int segscan_begin(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, cons
 int segscan_tiles(jq_ctx* ctx, const SideScan& side) {
   if (!side.x || side.ntiles == 0) return JQ_OK;
   const int wpb = 8;
-  segscan_tile_kernel<<<(unsigned)cdiv(side.ntiles, wpb), 32 * wpb, 0, ctx->stream>>>(
-      side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
+  const int k = ctx->tile_launches < 4 && ctx->tev[0] ? ctx->tile_launches : -1;
+  if (k >= 0) cudaEventRecord(ctx->tev[2 * k], ctx->stream);
+  const unsigned grid = (unsigned)cdiv(side.ntiles, wpb);
+  if (narrow_tiles() && side.cols <= 32)
+    segscan_tile_narrow_kernel<1><<<grid, 32 * wpb, 0, ctx->stream>>>(
+        side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
+  else if (narrow_tiles() && side.cols <= 64)
+    segscan_tile_narrow_kernel<2><<<grid, 32 * wpb, 0, ctx->stream>>>(
+        side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
+  else
+    segscan_tile_kernel<<<grid, 32 * wpb, 0, ctx->stream>>>(
+        side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
   JQ_CHECK_LAUNCH(ctx);
+  if (k >= 0) {  // algorithmic bytes: the rows read once (+ their segment ids)
+    cudaEventRecord(ctx->tev[2 * k + 1], ctx->stream);
+    ctx->tile_bytes += 8.0 * side.rows * side.cols + (side.gid ? 4.0 * side.rows : 0.0);
+    ctx->tile_launches = k + 1;
+  }
   return JQ_OK;
 }
 

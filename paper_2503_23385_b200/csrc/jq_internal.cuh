@@ -69,6 +69,10 @@ struct jq_ctx {
   cudaEvent_t pev[4]{};                 // piece copied / consumed events
   cudaStream_t aux_stream = nullptr;    // V replay beside the Jacobi sweeps (jq_svd.cu)
   cudaEvent_t aev[2]{};
+  // the head/tail tile pass timed on its own (up to 4 launches per call; bench roofline)
+  cudaEvent_t tev[8]{};
+  int tile_launches = 0;
+  double tile_bytes = 0.0;
 };
 
 namespace jq {

@@ -152,4 +152,104 @@ __device__ __forceinline__ void segscan_tile(const double* __restrict__ x, int64
   if (lane == 0) flag[t] = any_start;
 }
 
+// The same tile pass for <= 32 * SL columns with fewer registers and more rows in flight
+// (the standalone segscan_tile_kernel; the generic path above stays for wider tables and
+// for the TSQR leaf's spare warps).  Identical additions in identical order: keyed rows
+// run the same sequential segment logic; Cartesian row r goes to accumulator r % 4 and
+// the last r1 % 4 rows of the tile to accumulator 0, as in segscan_tile.
+template <int BATCH, int SL>
+__device__ __forceinline__ void segscan_tile_narrow(const double* __restrict__ x, int64_t rows, int cols,
+                                                    const int32_t* __restrict__ gid, int64_t t,
+                                                    double* __restrict__ agg, int* __restrict__ flag,
+                                                    double* __restrict__ totals, int lane) {
+  static_assert(BATCH % 4 == 0 && (SL == 1 || SL == 2), "narrow tile pass shape");
+  const int64_t r0 = t * TILE_ROWS, r1 = min(rows, r0 + TILE_ROWS);
+  bool h[SL];
+#pragma unroll
+  for (int k = 0; k < SL; ++k) h[k] = lane + 32 * k < cols;
+  if (!gid) {
+    double a[SL][4];
+#pragma unroll
+    for (int k = 0; k < SL; ++k)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[k][u] = 0.0;
+    int64_t r = r0;
+    for (; r + BATCH <= r1; r += BATCH) {
+      double v[SL][BATCH];
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+        for (int k = 0; k < SL; ++k) v[k][u] = h[k] ? __ldg(x + (r + u) * cols + lane + 32 * k) : 0.0;
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+        for (int k = 0; k < SL; ++k) a[k][u & 3] += v[k][u];
+    }
+    for (; r + 4 <= r1; r += 4)
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < SL; ++k) a[k][u] += h[k] ? __ldg(x + (r + u) * cols + lane + 32 * k) : 0.0;
+    for (; r < r1; ++r)
+#pragma unroll
+      for (int k = 0; k < SL; ++k)
+        if (h[k]) a[k][0] += __ldg(x + r * cols + lane + 32 * k);
+#pragma unroll
+    for (int k = 0; k < SL; ++k) {
+      const double sk = (a[k][0] + a[k][1]) + (a[k][2] + a[k][3]);
+      if (h[k]) {
+        if (r1 == rows) totals[lane + 32 * k] = sk;
+        agg[t * cols + lane + 32 * k] = sk;
+      }
+    }
+    if (lane == 0) flag[t] = r0 == 0;
+    return;
+  }
+  int seg = gid[r0];
+  int any_start = (r0 == 0) || (gid[r0 - 1] != seg);
+  double s[SL];
+#pragma unroll
+  for (int k = 0; k < SL; ++k) s[k] = 0.0;
+  auto row_step = [&](int64_t rr, int sr, const double* v) {
+    const bool start = (rr == 0) || (rr > r0 && sr != seg);
+    if (start && rr > r0) {
+      if (seg >= 0)
+#pragma unroll
+        for (int k = 0; k < SL; ++k)
+          if (h[k]) totals[(int64_t)seg * cols + lane + 32 * k] = s[k];
+      any_start = 1;
+    }
+    seg = sr;
+#pragma unroll
+    for (int k = 0; k < SL; ++k) s[k] = start ? v[k] : s[k] + v[k];
+  };
+  int64_t r = r0;
+  for (; r + BATCH <= r1; r += BATCH) {
+    int g[BATCH];
+    double v[BATCH][SL];
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      g[u] = gid[r + u];
+#pragma unroll
+      for (int k = 0; k < SL; ++k) v[u][k] = h[k] ? __ldg(x + (r + u) * cols + lane + 32 * k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) row_step(r + u, g[u], v[u]);
+  }
+  for (; r < r1; ++r) {
+    double v[SL];
+#pragma unroll
+    for (int k = 0; k < SL; ++k) v[k] = h[k] ? __ldg(x + r * cols + lane + 32 * k) : 0.0;
+    row_step(r, gid[r], v);
+  }
+  const bool ends_here = (r1 == rows) || (gid[r1] != seg);
+#pragma unroll
+  for (int k = 0; k < SL; ++k)
+    if (h[k]) {
+      if (ends_here && seg >= 0) totals[(int64_t)seg * cols + lane + 32 * k] = s[k];
+      agg[t * cols + lane + 32 * k] = s[k];
+    }
+  if (lane == 0) flag[t] = any_start;
+}
+
 }  // namespace jq

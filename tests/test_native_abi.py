@@ -73,3 +73,13 @@ def test_host_validation_errors_before_any_gpu_work():
         P.head_tail(np.zeros((0, 3)))
     with pytest.raises(ValueError):
         P.householder_r(np.zeros((3, 0)))
+
+
+def test_timing_struct_matches_header():
+    """jq_timing (include/joinqr.h) and the ctypes mirror list the same fields in order."""
+    import re
+    from paper_2503_23385_b200._native import JqTiming
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "joinqr.h")).read()
+    body = re.search(r"typedef struct jq_timing \{(.*?)\} jq_timing;", hdr, re.S).group(1)
+    names = re.findall(r"^\s*(?:double|int64_t)\s+(\w+);", body, re.M)
+    assert names == [f for f, _ in JqTiming._fields_]
