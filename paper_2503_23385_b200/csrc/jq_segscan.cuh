@@ -233,8 +233,18 @@ __device__ __forceinline__ void segscan_tile_narrow(const double* __restrict__ x
 #pragma unroll
       for (int k = 0; k < SL; ++k) v[u][k] = h[k] ? __ldg(x + (r + u) * cols + lane + 32 * k) : 0.0;
     }
+    bool uniform = r != 0;  // every row continues the open segment: plain sequential sums
 #pragma unroll
-    for (int u = 0; u < BATCH; ++u) row_step(r + u, g[u], v[u]);
+    for (int u = 0; u < BATCH; ++u) uniform = uniform && g[u] == seg;
+    if (uniform) {
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+        for (int k = 0; k < SL; ++k) s[k] = s[k] + v[u][k];
+    } else {
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) row_step(r + u, g[u], v[u]);
+    }
   }
   for (; r < r1; ++r) {
     double v[SL];
