@@ -105,6 +105,17 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, cfg_id: int):
     """The reference's CPU path: the oracle port of SPEC.md (numpy / LAPACK, all host
@@ -135,6 +146,8 @@ def run_reference(args, cfg_id: int):
     value = join_full / t_full
     cores = len(os.sched_getaffinity(0))
     return {"value": value, "unit": "join rows/s", "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(), "extrapolated": m_s < m_full, "sample_rows_per_side": m_s,
+            "sample_join_rows": (float(m_s) ** 2 if cfg["keys"] is None else None),
             "sample": f"{cfg['name']} with m1=m2={m_s} rows (same SplitMix64 recipe), full SPEC "
                       f"pipeline reduce->LAPACK Householder QR->canonicalize, mean of {args.steps} after "
                       f"{args.warmup} warm-up = {t_sample:.3f} s, extrapolated x{m_full / m_s:.0f} linearly "
@@ -202,6 +215,7 @@ def main():
                          "reported under 'variants')")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-memory e2e step")
     ap.add_argument("--force-sharded", action="store_true",
                     help="(testing) run the multi-GPU code path even with one rank (torchrun, 1 process)")
     args = ap.parse_args()
@@ -225,7 +239,8 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "impl": "reference",
                 "config": {"workload": cfg["name"], "sample_rows_per_side": min(cfg["m"], args.ref_rows)},
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                    "extrapolated", "ms_per_step_sample")},
                 "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -376,11 +391,13 @@ def main():
     if sharded_path and not args.no_e2e:
         e2e = run_e2e_sharded(args, A, B, m, a0, jrows, world, device)
     elif world == 1 and not args.no_e2e:
+        N.set_variant(args.variant)
+        r_ref = np.asarray(P.figaro_r(P.Table(A, ka), P.Table(B, kb)).cpu())
         host = to_host(A, B, ka, kb)
         del A, B
         A = B = None
         torch.cuda.empty_cache()
-        e2e = run_e2e(args, host, jrows)
+        e2e = run_e2e(args, host, jrows, r_ref)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -390,7 +407,12 @@ def main():
             ra = argparse.Namespace(**vars(args))
             ra.steps, ra.warmup = 2, 1
             cb = run_reference(ra, args.config)
-            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "extrapolated",
+                                      "ms_per_step_sample")}
+            # the measured same-config pair: our GPU path on the CPU sample's exact inputs
+            cpu["gpu_same_sample"] = gpu_on_sample(args, cb["sample_rows_per_side"])
+            cpu["gpu_same_sample"]["ratio_vs_cpu_sample"] = (cb["ms_per_step_sample"] /
+                                                             cpu["gpu_same_sample"]["ms_per_step"])
         except Exception as exc:  # reported, never fatal for the GPU line
             cpu = {"value": None, "unit": "join rows/s", "cores": None, "kind": "port", "sample": f"failed: {exc}"}
 
@@ -413,6 +435,45 @@ def main():
         dist.destroy_process_group()
 
 
+def gpu_on_sample(args, rows):
+    """Device time of our path on the CPU baseline's sample (identical inputs: the same
+    recipe and seeds at `rows` rows per side), so one GPU/CPU ratio is measured on the
+    same config rather than extrapolated."""
+    import torch
+    import oracle as O      # the sample's generator (cpu_baseline leg only)
+    import paper_2503_23385_b200 as P
+    from paper_2503_23385_b200 import _native as N
+    cfg = CONFIGS[args.config]
+    a, b = O.config_tables(args.config, rows=rows)
+    dev = lambda x: None if x is None else torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    ta, tb = P.Table(dev(a.data), dev(a.keys)), P.Table(dev(b.data), dev(b.keys))
+    N.set_variant(args.variant)
+
+    def run():
+        if cfg.get("want_v"):
+            return P.figaro_svd(ta, tb, want_vectors=True).values
+        return P.figaro_r(ta, tb)
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    reps = 10
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    e0.record(stream)
+    for _ in range(reps):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"ms_per_step": ms, "rows_per_side": rows, "variant": args.variant,
+            "note": "device-resident inputs, CUDA events, mean of 10 after 3 warm-up"}
+
+
+def rel_err_abs(r, r_ref) -> float:
+    r, r_ref = np.abs(np.asarray(r)), np.abs(np.asarray(r_ref))
+    return float(np.linalg.norm(r - r_ref) / max(np.linalg.norm(r_ref), 1e-300))
+
+
 def to_host(A, B, ka, kb):
     """Copy the device tables into page-locked host memory (outside any timing)."""
     import torch
@@ -430,9 +491,12 @@ def to_host(A, B, ka, kb):
     return host
 
 
-def run_e2e(args, host, jrows):
+def run_e2e(args, host, jrows, r_ref):
     """figaro_r(Table(host), Table(host)) through the public API: the H2D copy of both
-    tables (page-locked host memory) and the D2H of R are inside the timed region."""
+    tables (page-locked host memory) and the D2H of R are inside the timed region.
+    Every timed R is compared with the device-resident path's R on the same inputs
+    (`parity`: max relative Frobenius error of |R|, bar 1e-12).  A pageable-memory step
+    (the plain-numpy drop-in caller) is timed after the pinned ones."""
     import torch
     import paper_2503_23385_b200 as P
     cudart = torch.cuda.cudart()
@@ -441,18 +505,31 @@ def run_e2e(args, host, jrows):
         tb = P.Table(host["B"][0], host["kb"])
         nsteps = max(1, min(args.steps, 3))
         P.figaro_r(ta, tb)                     # warm-up (workspace sizing)
-        times = []
+        times, errs = [], []
         for _ in range(nsteps):
             t0 = time.perf_counter()
             r = P.figaro_r(ta, tb)              # returns after the D2H of R
             times.append(time.perf_counter() - t0)
+            errs.append(rel_err_abs(r, r_ref))
         t = float(np.mean(times))
+        pageable = None
+        if all(host[k][1] for k in ("A", "B")) and not args.no_pageable:
+            for key in ("A", "B"):
+                cudart.cudaHostUnregister(host[key][0].ctypes.data)
+                host[key] = (host[key][0], False)
+            t0 = time.perf_counter()
+            rp = P.figaro_r(ta, tb)
+            tp = time.perf_counter() - t0
+            pageable = {"value": jrows / tp, "ms_per_step": tp * 1e3, "steps": 1,
+                        "parity": rel_err_abs(rp, r_ref)}
         h2d = host["A"][0].nbytes + host["B"][0].nbytes
         if host["ka"] is not None:
             h2d += host["ka"].nbytes + host["kb"].nbytes
         return {"value": jrows / t, "unit": "join rows/s", "ms_per_step": t * 1e3, "steps": nsteps,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(r.nbytes),
-                "pinned": bool(host["A"][1] and host["B"][1]),
+                "pinned": True if pageable else bool(host["A"][1] and host["B"][1]),
+                "parity": {"max_rel_err_vs_device_path": max(errs), "bar": 1e-12, "ok": max(errs) <= 1e-12},
+                "pageable": pageable,
                 "api": "paper_2503_23385_b200.figaro_r(Table(numpy), Table(numpy)) -> jq_figaro_r"}
     finally:
         for key in ("A", "B"):
@@ -472,6 +549,11 @@ def run_e2e_sharded(args, A, B, m, a0, jrows, world, device):
     import torch.distributed as dist
     from paper_2503_23385_b200 import sharded
     from paper_2503_23385_b200 import _native as N
+    N.use_torch_stream(A)
+    if N.get_variant() == "footnote":
+        r_ref = sharded.figaro_r_sharded_local(A, B, m, m, a0, a0).cpu().numpy()
+    else:
+        r_ref = sharded.figaro_r_sharded(A, B, m, m, a0, a0).cpu().numpy()
     host = to_host(A, B, None, None)
     cudart = torch.cuda.cudart()
     try:
@@ -494,11 +576,14 @@ def run_e2e_sharded(args, A, B, m, a0, jrows, world, device):
         nsteps = max(1, min(args.steps, 3))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        rs = []
         for _ in range(nsteps):
             r = step()
+            rs.append(r)
         e1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
+        err = max(rel_err_abs(x.numpy(), r_ref) for x in rs)
         t = torch.tensor([e0.elapsed_time(e1) / nsteps], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -506,6 +591,8 @@ def run_e2e_sharded(args, A, B, m, a0, jrows, world, device):
                 "h2d_bytes_per_step": int(host["A"][0].nbytes + host["B"][0].nbytes),
                 "d2h_bytes_per_step": int(r.numpy().nbytes),
                 "per_rank": True, "pinned": bool(host["A"][1] and host["B"][1]),
+                "parity": {"max_rel_err_vs_device_path": err, "bar": 1e-12, "ok": err <= 1e-12,
+                           "rank": int(os.environ.get("RANK", "0"))},
                 "note": "per rank: its own shards' H2D and R's D2H (bytes above are one rank's); "
                         "time = max over ranks; H2D not overlapped with the leaves on this path",
                 "api": "paper_2503_23385_b200.sharded.figaro_r_sharded_local (torch.distributed NCCL)"}

@@ -72,7 +72,9 @@ JQ_API const char* jq_last_error(void);
 JQ_API int jq_ctx_create(int device, jq_ctx** out);
 JQ_API int jq_ctx_destroy(jq_ctx* ctx);
 /* Use a caller stream (e.g. torch.cuda.current_stream().cuda_stream); NULL
- * restores the context's own stream. */
+ * restores the context's own (non-blocking) stream.  The legacy default stream
+ * must be passed as cudaStreamLegacy ((void*)0x1), not as NULL: the own stream
+ * does not wait for work queued on the legacy stream. */
 JQ_API int jq_ctx_set_stream(jq_ctx* ctx, void* cuda_stream);
 JQ_API int jq_ctx_sync(jq_ctx* ctx);
 /* Internal variant switch: 0 = dense Claim-1 reduced matrix (north star),

@@ -161,11 +161,25 @@ def ptr(x):
     raise TypeError(f"unsupported array type {type(x)!r}")
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the handle of the legacy default stream
+
+
+def torch_stream_handle() -> int:
+    """torch's current stream as a CUDA handle the library can order against.  torch
+    reports its default stream as 0 (NULL), which the library would read as "use your
+    own non-blocking stream" -- and a non-blocking stream does NOT wait for the legacy
+    default stream, so the library could read a tensor before torch's producer kernel
+    or non_blocking H2D copy has landed.  0 is therefore passed as cudaStreamLegacy."""
+    import torch
+    h = int(torch.cuda.current_stream().cuda_stream)
+    return h if h != 0 else CUDA_STREAM_LEGACY
+
+
 def use_torch_stream(*arrays) -> None:
-    """Order library work after torch's producer kernels when device tensors flow in."""
+    """Order library work after torch's producer kernels when device tensors flow in
+    (the library then runs on torch's current stream, see torch_stream_handle)."""
     if any(is_torch_cuda(a) for a in arrays if a is not None):
-        import torch
-        check(lib().jq_ctx_set_stream(ctx(), _P(torch.cuda.current_stream().cuda_stream)))
+        check(lib().jq_ctx_set_stream(ctx(), _P(torch_stream_handle())))
     else:
         check(lib().jq_ctx_set_stream(ctx(), None))
 

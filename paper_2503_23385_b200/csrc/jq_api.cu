@@ -666,18 +666,27 @@ __global__ void pack2_kernel(const double* __restrict__ r0, const double* __rest
     out[i] = i < n * n ? r0[i] : r1[i - n * n];
 }
 
+// Environment overrides (read per call, for the piece-count parity sweep):
+// JQ_STREAM_MIN_BYTES (default 1 GiB of host input) and JQ_PIECE_BYTES (default 512 MiB).
+static int64_t env_bytes(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  if (!e || !*e) return dflt;
+  const long long v = atoll(e);
+  return v > 0 ? (int64_t)v : dflt;
+}
+
 static bool use_streamed(const double* a, int64_t m1, int64_t n1, const double* b, int64_t m2, int64_t n2,
                          const int64_t* ka) {
   if (ka) return false;
   if (is_device_ptr(a) || is_device_ptr(b)) return false;
-  return (m1 * n1 + m2 * n2) * 8 >= (int64_t(1) << 30);  // >= 1 GiB of input
+  return (m1 * n1 + m2 * n2) * 8 >= env_bytes("JQ_STREAM_MIN_BYTES", int64_t(1) << 30);
 }
 
 static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const double* b, int64_t m2,
                              int64_t n2, double* dr /* device, n x n canonical */) {
   const int64_t n = n1 + n2;
   const bool foot = use_footnote(ctx, m1 + m2, n);
-  const int64_t piece_bytes = int64_t(512) << 20;
+  const int64_t piece_bytes = env_bytes("JQ_PIECE_BYTES", int64_t(512) << 20);
   auto prows = [&](int64_t cols) {
     int64_t pr = piece_bytes / (8 * std::max<int64_t>(cols, 1));
     return std::max<int64_t>(TILE_ROWS, pr / TILE_ROWS * TILE_ROWS);

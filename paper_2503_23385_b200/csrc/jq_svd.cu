@@ -432,7 +432,8 @@ jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_
 // Row i of V (one warp per row): replay the logged rotations of jacobi_cluster_kernel
 // on V[i, :] (V = I at the start), rounds in order, lane l doing pairs l, l + 32, ...
 // (the same element arithmetic as a carried V); then vout[i][rank(j)] = V[i][j] for the
-// n_out largest sigma.  Runs on a second stream WHILE the sweeps go on: a sweep is
+// n_out largest sigma.  By default it runs after the cluster kernel on the same stream;
+// with JQ_SVD_V_OVERLAP=1 it runs on a second stream WHILE the sweeps go on: a sweep is
 // replayed once progress[0] says its log is out, and the kernel ends when progress[1]
 // (done) is set and nsweeps sweeps are replayed (the final, clean sweep is skipped).
 constexpr int SVDV_WARPS = 4, SVDV_BATCH = 4;
@@ -591,21 +592,32 @@ int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values,
     JQ_CHECK_LAUNCH(ctx);
     // nsw = {nsweeps, sweeps whose log is out, done}
     JQ_CUDA(cudaMemsetAsync(nsw, 0, 4 * sizeof(int), ctx->stream));
-    if (want_v && !ctx->aux_stream) {
+    // V replay: by default on the same stream AFTER the sweeps (it then finds every
+    // sweep published and never waits).  JQ_SVD_V_OVERLAP=1 runs it on a second stream
+    // concurrently with the sweeps (it spins on the cluster kernel's progress flags:
+    // ~0.5 ms faster at n = 256, but it relies on both kernels being co-scheduled, which
+    // CUDA does not guarantee -- MPS partitions, serialising tools -- so it is opt-in).
+    static const bool overlap_v = [] {
+      const char* e = getenv("JQ_SVD_V_OVERLAP");
+      return e && strcmp(e, "1") == 0;
+    }();
+    if (want_v && overlap_v && !ctx->aux_stream) {
       JQ_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
       for (auto& e : ctx->aev) JQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    if (want_v) JQ_CUDA(cudaEventRecord(ctx->aev[0], ctx->stream));
+    if (want_v && overlap_v) JQ_CUDA(cudaEventRecord(ctx->aev[0], ctx->stream));
     JQ_TRY(launch_jacobi_cluster(ctx, A, npc, sig, rlog, nsw, values, (int)n));
-    if (want_v) {
-      // V replays each sweep's log on a second stream while the next sweeps run (launched
-      // only once the cluster kernel is queued: it waits on that kernel's progress flags)
+    if (want_v && overlap_v) {
       JQ_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aev[0], 0));
       jacobi_v_kernel<<<(unsigned)cdiv(n, SVDV_WARPS), SVDV_WARPS * 32, 0, ctx->aux_stream>>>(rlog, nsw, nsw + 1,
                                                                                            npc, sig, v, (int)n);
       JQ_CHECK_LAUNCH(ctx);
       JQ_CUDA(cudaEventRecord(ctx->aev[1], ctx->aux_stream));
       JQ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aev[1], 0));
+    } else if (want_v) {
+      jacobi_v_kernel<<<(unsigned)cdiv(n, SVDV_WARPS), SVDV_WARPS * 32, 0, ctx->stream>>>(rlog, nsw, nsw + 1, npc,
+                                                                                        sig, v, (int)n);
+      JQ_CHECK_LAUNCH(ctx);
     }
     return JQ_OK;
   }

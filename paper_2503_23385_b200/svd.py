@@ -25,6 +25,8 @@ class SvdResult:
 
 def svd_of_r(r, want_vectors: bool = False) -> SvdResult:
     r = as_matrix(r)
+    if r.shape[0] != r.shape[1]:
+        raise ValueError(f"svd_of_r needs a square upper-triangular R, got {r.shape[0]}x{r.shape[1]}")
     n = r.shape[1]
     vals = like((n,), r)
     v = like((n, n), r) if want_vectors else None

@@ -407,6 +407,56 @@ def test_streamed_host_path_matches_device_path(P, variant):
     check_r(r_host, r_dev, 1e-12)
 
 
+@pytest.mark.parametrize("variant", ["dense", "footnote"])
+@pytest.mark.parametrize("pieces", [(1, 1), (2, 3), (3, 2), (4, 7), (5, 5), (7, 1)], ids=lambda p: f"{p[0]}x{p[1]}")
+def test_streamed_host_path_piece_sweep(P, variant, pieces, monkeypatch):
+    """The streamed host path (the one bench.py's e2e times) with 1-7 pieces per table,
+    odd counts and unequal sides: JQ_STREAM_MIN_BYTES forces the path at small sizes,
+    JQ_PIECE_BYTES sets 1024-row pieces.  R must match LAPACK on the reduced matrix and
+    the device-resident path."""
+    import torch
+    n1, n2 = 12, 20
+    pa, pb = pieces
+    m1, m2 = 1024 * (pa - 1) + 517, 1024 * (pb - 1) + 1000    # last piece partial
+    rng = np.random.default_rng(100 * pa + pb)
+    A, B = rng.random((m1, n1)), rng.random((m2, n2))
+    # pieces of exactly 1024 rows on both sides: piece_bytes / (8 * cols) rounded to 1024
+    monkeypatch.setenv("JQ_STREAM_MIN_BYTES", "1")
+    monkeypatch.setenv("JQ_PIECE_BYTES", str(8 * max(n1, n2) * 1024 + 8 * 1023))
+    P.set_variant(variant)
+    try:
+        r_host = np.asarray(P.figaro_r(P.Table(A), P.Table(B)))
+        monkeypatch.delenv("JQ_STREAM_MIN_BYTES")
+        r_dev = P.figaro_r(P.Table(torch.from_numpy(A).cuda()), P.Table(torch.from_numpy(B).cuda())).cpu().numpy()
+    finally:
+        P.set_variant("dense")
+    red = O.reduce_cartesian(A, B).matrix
+    check_r(r_host, O.canonicalize(O.householder_r_lapack(red)))
+    check_r(r_host, r_dev, 1e-12)
+
+
+def test_async_torch_producer_is_ordered(P):
+    """a tensor produced by a non_blocking H2D copy and a large torch
+    kernel on torch's default stream, handed to the library with no sync in between,
+    must be read after it lands (the library runs on cudaStreamLegacy, not its own
+    non-blocking stream)."""
+    import torch
+    rng = np.random.default_rng(5)
+    m, n = 2_000_000, 16
+    ha = torch.from_numpy(rng.random((m, n))).pin_memory()
+    hb = torch.from_numpy(rng.random((m, n))).pin_memory()
+    ref = np.asarray(P.figaro_r(P.Table(ha.numpy()), P.Table(hb.numpy())))
+    for _ in range(3):
+        A = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        B = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        A.copy_(ha, non_blocking=True)
+        B.copy_(hb, non_blocking=True)
+        B.mul_(1.0).add_(0.0)                   # producer kernels queued behind the copies
+        r = P.figaro_r(P.Table(A), P.Table(B)).cpu().numpy()
+        check_r(r, ref, 1e-12)
+
+
 @pytest.mark.gpu
 def test_auto_variant_large_join_matches_oracle_gram(P):
     """Default variant ("auto") above its 1e8-element threshold takes the footnote

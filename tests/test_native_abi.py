@@ -73,6 +73,17 @@ def test_host_validation_errors_before_any_gpu_work():
         P.head_tail(np.zeros((0, 3)))
     with pytest.raises(ValueError):
         P.householder_r(np.zeros((3, 0)))
+    with pytest.raises(ValueError, match="square"):
+        P.svd_of_r(np.ones((3, 4)))                        # R is n x n
+    with pytest.raises(ValueError, match="square"):
+        P.svd_of_r(np.ones((4, 3)), True)
+
+
+def test_default_stream_maps_to_legacy_handle():
+    """torch's default stream (handle 0) must reach the library as cudaStreamLegacy:
+    NULL would select the library's own non-blocking stream (no ordering with torch)."""
+    from paper_2503_23385_b200 import _native as N
+    assert N.CUDA_STREAM_LEGACY == 1
 
 
 def test_timing_struct_matches_header():
