@@ -171,10 +171,43 @@ def make_inputs(cfg_id, rank, world, device):
         ka = torch.from_numpy(datagen.near_equal_keys(m, cfg["key_groups"])).to(device)
         kb = ka.clone()
     elif cfg["keys"] == "zipf":
-        ka = torch.from_numpy(datagen.zipf_sorted_keys(1000 * cfg_id + 3, m)).to(device)
-        kb = torch.from_numpy(datagen.zipf_sorted_keys(1000 * cfg_id + 4, m)).to(device)
+        # SURVEY.md §8d C3 recipe: per-row keys, then the stable (key, row) sort permutes
+        # the data rows (GPU radix sort + gather; input preparation, outside the step)
+        del A, B
+        ta = datagen.zipf_table(1000 * cfg_id + 3, 1000 * cfg_id + 1, m, n, device=device)
+        tb = datagen.zipf_table(1000 * cfg_id + 4, 1000 * cfg_id + 2, m, n, device=device)
+        A, ka, B, kb = ta.data, ta.keys, tb.data, tb.keys
     torch.cuda.synchronize()
     return A, B, ka, kb, a0
+
+
+def time_radix_sort(cfg_id, device):
+    """Device time of the opt-in key sort of one unsorted C3 table (radix sort of the
+    keys + gather of the data rows), CUDA events, mean of 3."""
+    import torch
+    from paper_2503_23385_b200 import datagen, argsort_keys, gather_rows
+    cfg = CONFIGS[cfg_id]
+    m, n = cfg["m"], cfg["n"]
+    ku = datagen.zipf_keys(1000 * cfg_id + 3, m, out=torch.empty(m, dtype=torch.int64, device=device))
+    x = datagen.uniform(1000 * cfg_id + 1, m, n, out=torch.empty((m, n), dtype=torch.float64, device=device))
+    argsort_keys(ku)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    s = torch.cuda.current_stream()
+    t_sort = t_gather = 0.0
+    for _ in range(3):
+        e[0].record(s)
+        _, perm = argsort_keys(ku)
+        e[1].record(s)
+        gather_rows(x, perm)
+        e[2].record(s)
+        torch.cuda.synchronize()
+        t_sort += e[0].elapsed_time(e[1]) / 3
+        t_gather += e[1].elapsed_time(e[2]) / 3
+    return {"keys": m, "sort_ms": t_sort, "gather_ms": t_gather, "keys_per_s": m / (t_sort / 1e3),
+            "gather_gbs": 2 * 8 * m * n / (t_gather / 1e3) / 1e9,
+            "note": "stable LSD radix sort (jq_sort.cu, digit passes whose digit is constant skipped) of one "
+                    "side's unsorted Zipf keys + row gather; input preparation, not in the timed step"}
 
 
 def tsqr_flops(variant, cfg, m, n, st):
@@ -416,6 +449,12 @@ def main():
         except Exception as exc:  # reported, never fatal for the GPU line
             cpu = {"value": None, "unit": "join rows/s", "cores": None, "kind": "port", "sample": f"failed: {exc}"}
 
+    sort_info = None
+    if world == 1 and cfg["keys"] == "zipf":
+        A = B = None
+        torch.cuda.empty_cache()
+        sort_info = time_radix_sort(args.config, device)
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "join rows/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -427,7 +466,7 @@ def main():
                            "l2": "inputs 16*m*n bytes >> 126 MB L2 (no flush needed)" if m * n * 16 > 2**28 else "small config: L2-resident"},
                 "gpu_launches": launches, "clocks": clk, "roofline": roof, "roofline_hbm": roof_hbm,
                 "stages_ms": stage_avg, "step_ms_all": step_ms, "e2e": e2e, "cpu_baseline": cpu,
-                "variant": args.variant,
+                "variant": args.variant, "radix_sort": sort_info,
                 "variants": {args.variant: {"ms_per_step": ms, "value": value},
                              other: ({"ms_per_step": ms_o, "value": jrows / (ms_o / 1e3)} if ms_o else None)}}
         print(json.dumps(line), flush=True)

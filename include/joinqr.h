@@ -137,6 +137,21 @@ JQ_API int jq_gen_uniform(jq_ctx* ctx, uint64_t seed, int64_t rows, int64_t cols
  * multiset of searchsorted(cdf, u_row, 'right') (cdf given, universe entries). */
 JQ_API int jq_gen_zipf_sorted_keys(jq_ctx* ctx, uint64_t seed, int64_t rows, const double* cdf,
                             int64_t universe, int64_t* keys_out);
+/* Unsorted Zipf keys, one per row in generation order: keys_out[i] =
+ * searchsorted(cdf, u_i, 'right') (SURVEY.md §8d C3 recipe, before the stable sort). */
+JQ_API int jq_gen_zipf_keys(jq_ctx* ctx, uint64_t seed, int64_t rows, const double* cdf, int64_t universe,
+                            int64_t* keys_out);
+
+/* ---- key sort for unsorted tables (opt-in; SPEC.md:204-206 raises by default) ---- */
+/* Stable LSD radix sort of m int64 keys: perm_out[i] = the original row of sorted
+ * position i, equal to np.argsort(keys, kind="stable") bit for bit; keys_out
+ * (optional) = keys[perm_out].  Replaces the caller-side sort the reference
+ * requires before reduce_natural_join / figaro_r. */
+JQ_API int jq_sort_keys(jq_ctx* ctx, const int64_t* keys, int64_t m, int64_t* keys_out, int64_t* perm_out);
+/* out[i, :] = x[perm[i], :] for a row-major rows x cols table (perm entries must lie
+ * in [0, rows)): applies jq_sort_keys' permutation to the data rows. */
+JQ_API int jq_gather_rows(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int64_t* perm,
+                          double* out);
 
 /* ---- row-sharded multi-GPU building blocks -------------- */
 /* Column sums of a row block (fixed-order, deterministic): sums[cols]. */

@@ -30,7 +30,12 @@ static inline double unif(uint64_t seed, uint64_t k) {
 #define BLK 256
 
 /* G[0:n,0:n] += sum_i w_i x_i x_i^T over rows of a SplitMix table (upper triangle). */
-static void weighted_gram(uint64_t seed, int64_t m, int n, const double* w, double* G, int ld, int off) {
+/* Row r of the table as held by the caller is generated row perm[r] (perm == NULL:
+ * identity) -- tables whose rows were permuted by a stable key sort (C3 recipe). */
+static inline uint64_t grow(const int64_t* perm, int64_t r) { return perm ? (uint64_t)perm[r] : (uint64_t)r; }
+
+static void weighted_gram(uint64_t seed, int64_t m, int n, const double* w, double* G, int ld, int off,
+                          const int64_t* perm) {
   int nt = omp_get_max_threads();
   double* priv = (double*)calloc((size_t)nt * n * n, sizeof(double));
   int64_t nblk = (m + BLK - 1) / BLK;
@@ -45,7 +50,7 @@ static void weighted_gram(uint64_t seed, int64_t m, int n, const double* w, doub
       int rows = (int)(r1 - r0);
       for (int i = 0; i < rows; ++i) {
         double sw = w ? w[r0 + i] : 1.0;
-        for (int c = 0; c < n; ++c) x[i * n + c] = unif(seed, (uint64_t)(r0 + i) * n + c);
+        for (int c = 0; c < n; ++c) x[i * n + c] = unif(seed, grow(perm, r0 + i) * n + c);
         (void)sw;
       }
       int i = 0;
@@ -79,8 +84,8 @@ static void weighted_gram(uint64_t seed, int64_t m, int n, const double* w, doub
 
 /* Per-row weights (count of the other side's rows with the same key) and the
  * cross term sum_g colsum(A_g)^T colsum(B_g). */
-int jq_oracle_gram(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, uint64_t seed_b, int64_t m2,
-                   int n2, const int64_t* kb, double* G) {
+int jq_oracle_gram_perm(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, const int64_t* pa,
+                        uint64_t seed_b, int64_t m2, int n2, const int64_t* kb, const int64_t* pb, double* G) {
   const int n = n1 + n2;
   memset(G, 0, sizeof(double) * n * n);
   double* wa = NULL;
@@ -103,9 +108,9 @@ int jq_oracle_gram(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, uint6
       memset(sa, 0, sizeof(double) * n1);
       memset(sb, 0, sizeof(double) * n2);
       for (int64_t r = i; r < i1; ++r)
-        for (int c = 0; c < n1; ++c) sa[c] += unif(seed_a, (uint64_t)r * n1 + c);
+        for (int c = 0; c < n1; ++c) sa[c] += unif(seed_a, grow(pa, r) * n1 + c);
       for (int64_t r = j; r < j1; ++r)
-        for (int c = 0; c < n2; ++c) sb[c] += unif(seed_b, (uint64_t)r * n2 + c);
+        for (int c = 0; c < n2; ++c) sb[c] += unif(seed_b, grow(pb, r) * n2 + c);
       for (int p = 0; p < n1; ++p)
         for (int q = 0; q < n2; ++q) G[p * n + n1 + q] += sa[p] * sb[q];
       i = i1;
@@ -120,10 +125,10 @@ int jq_oracle_gram(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, uint6
       double* p = pa + (size_t)omp_get_thread_num() * (n1 + n2 + 1);
 #pragma omp for schedule(static)
       for (int64_t r = 0; r < m1; ++r)
-        for (int c = 0; c < n1; ++c) p[c] += unif(seed_a, (uint64_t)r * n1 + c);
+        for (int c = 0; c < n1; ++c) p[c] += unif(seed_a, grow(pa, r) * n1 + c);
 #pragma omp for schedule(static)
       for (int64_t r = 0; r < m2; ++r)
-        for (int c = 0; c < n2; ++c) p[n1 + c] += unif(seed_b, (uint64_t)r * n2 + c);
+        for (int c = 0; c < n2; ++c) p[n1 + c] += unif(seed_b, grow(pb, r) * n2 + c);
     }
     for (int t = 0; t < nt; ++t) {
       for (int c = 0; c < n1; ++c) sa[c] += pa[(size_t)t * (n1 + n2 + 1) + c];
@@ -136,11 +141,11 @@ int jq_oracle_gram(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, uint6
   /* weighted diagonal blocks: A rows weighted by m2g, B rows by m1g */
   double* G1 = (double*)calloc((size_t)n * n, sizeof(double));
   if (ka) {
-    weighted_gram(seed_a, m1, n1, wa, G1, n, 0);
-    weighted_gram(seed_b, m2, n2, wb, G1, n, n1);
+    weighted_gram(seed_a, m1, n1, wa, G1, n, 0, pa);
+    weighted_gram(seed_b, m2, n2, wb, G1, n, n1, pb);
   } else {
-    weighted_gram(seed_a, m1, n1, NULL, G1, n, 0);
-    weighted_gram(seed_b, m2, n2, NULL, G1, n, n1);
+    weighted_gram(seed_a, m1, n1, NULL, G1, n, 0, pa);
+    weighted_gram(seed_b, m2, n2, NULL, G1, n, n1, pb);
     for (int p = 0; p < n1; ++p) for (int q = p; q < n1; ++q) G1[p * n + q] *= (double)m2;
     for (int p = n1; p < n; ++p) for (int q = p; q < n; ++q) G1[p * n + q] *= (double)m1;
   }
@@ -150,4 +155,9 @@ int jq_oracle_gram(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, uint6
     for (int q = 0; q < p; ++q) G[p * n + q] = G[q * n + p];
   free(G1); free(sa); free(sb); free(wa); free(wb);
   return 0;
+}
+
+int jq_oracle_gram(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, uint64_t seed_b, int64_t m2,
+                   int n2, const int64_t* kb, double* G) {
+  return jq_oracle_gram_perm(seed_a, m1, n1, ka, NULL, seed_b, m2, n2, kb, NULL, G);
 }

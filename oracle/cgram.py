@@ -12,15 +12,16 @@ def available() -> bool:
     return os.path.exists(_LIB)
 
 
-def join_gram(seed_a, m1, n1, seed_b, m2, n2, keys_a=None, keys_b=None) -> np.ndarray:
+def join_gram(seed_a, m1, n1, seed_b, m2, n2, keys_a=None, keys_b=None, perm_a=None, perm_b=None) -> np.ndarray:
+    """perm_x[r] = the generation row of row r (tables permuted by a stable key sort)."""
     lib = C.CDLL(_LIB)
-    f = lib.jq_oracle_gram
-    f.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_void_p, C.c_uint64, C.c_int64, C.c_int, C.c_void_p,
-                  C.c_void_p]
+    f = lib.jq_oracle_gram_perm
+    f.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int64, C.c_int,
+                  C.c_void_p, C.c_void_p, C.c_void_p]
     n = n1 + n2
     g = np.zeros((n, n))
-    ka = None if keys_a is None else np.ascontiguousarray(keys_a, dtype=np.int64)
-    kb = None if keys_b is None else np.ascontiguousarray(keys_b, dtype=np.int64)
-    f(seed_a, m1, n1, None if ka is None else ka.ctypes.data, seed_b, m2, n2,
-      None if kb is None else kb.ctypes.data, g.ctypes.data)
+    conv = lambda x: None if x is None else np.ascontiguousarray(x, dtype=np.int64)
+    ka, kb, pa, pb = conv(keys_a), conv(keys_b), conv(perm_a), conv(perm_b)
+    ptr = lambda x: None if x is None else x.ctypes.data
+    f(seed_a, m1, n1, ptr(ka), ptr(pa), seed_b, m2, n2, ptr(kb), ptr(pb), g.ctypes.data)
     return g

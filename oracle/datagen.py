@@ -110,10 +110,25 @@ def config_keys(c: int, side: int, rows: Optional[int] = None) -> Optional[np.nd
     return None
 
 
+def zipf_sorted_table(seed_keys: int, seed_data: int, rows: int, cols: int, s: float = 1.1,
+                      universe: int = 1_000_000):
+    """C3 recipe: keys and data rows in generation order, then a stable
+    sort of (key, row) permutes the rows.  Returns (Table, perm), perm[r] = generation
+    row of row r (np.argsort(kind="stable"), the GPU radix sort's parity target)."""
+    k = zipf_keys(seed_keys, rows, s, universe)
+    perm = np.argsort(k, kind="stable")
+    return Table(uniform_matrix(seed_data, rows, cols)[perm], k[perm]), perm
+
+
 def config_tables(c: int, rows: Optional[int] = None):
-    """(A, B) Tables of config c; ``rows`` overrides m (a bounded sample, same recipe)."""
+    """(A, B) Tables of config c; ``rows`` overrides m (a bounded sample, same recipe).
+    C3: data rows permuted by the stable key sort (zipf_sorted_table)."""
     cfg = CONFIGS[c]
     m = cfg["m"] if rows is None else rows
+    if cfg["keys"] == "zipf":
+        a, _ = zipf_sorted_table(1000 * c + 3, 1000 * c + 1, m, cfg["n"], cfg["s"], cfg["universe"])
+        b, _ = zipf_sorted_table(1000 * c + 4, 1000 * c + 2, m, cfg["n"], cfg["s"], cfg["universe"])
+        return a, b
     a = Table(uniform_matrix(1000 * c + 1, m, cfg["n"]), config_keys(c, 1, m))
     b = Table(uniform_matrix(1000 * c + 2, m, cfg["n"]), config_keys(c, 2, m))
     return a, b

@@ -35,6 +35,9 @@ _EXPORTS = {
     "reduce_natural_join": ".joins",
     "reduce_join": ".joins",
     "group_keys": ".joins",
+    "argsort_keys": ".joins",
+    "gather_rows": ".joins",
+    "sort_by_key": ".joins",
     "householder_r": ".qr",
     "canonicalize": ".qr",
     "figaro_r": ".qr",

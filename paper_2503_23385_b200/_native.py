@@ -45,6 +45,9 @@ SIGNATURES = {
     "jq_figaro_svd": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, C.c_int, _P, _P, _P],
     "jq_gen_uniform": [_P, C.c_uint64, _I64, _I64, _I64, _P],
     "jq_gen_zipf_sorted_keys": [_P, C.c_uint64, _I64, _P, _I64, _P],
+    "jq_gen_zipf_keys": [_P, C.c_uint64, _I64, _P, _I64, _P],
+    "jq_sort_keys": [_P, _P, _I64, _P, _P],
+    "jq_gather_rows": [_P, _P, _I64, _I64, _P, _P],
     "jq_colsums": [_P, _P, _I64, _I64, _P],
     "jq_figaro_r_shard": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, C.c_int, _P],
     "jq_figaro_r_shard_local": [_P, _P, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P, _P],

@@ -45,6 +45,20 @@ __global__ void zipf_hist_kernel(uint64_t seed, int64_t rows, const double* __re
   }
 }
 
+// unsorted Zipf keys, one per row: key_i = searchsorted(cdf, u_i, 'right') (oracle zipf_keys)
+__global__ void zipf_keys_kernel(uint64_t seed, int64_t rows, const double* __restrict__ cdf, int64_t universe,
+                                 int64_t* __restrict__ keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    const double u = splitmix_uniform(seed, (uint64_t)i);
+    int64_t lo = 0, hi = universe;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(cdf + mid) <= u) lo = mid + 1; else hi = mid;
+    }
+    keys[i] = lo;
+  }
+}
+
 __global__ void zipf_fill_kernel(const int64_t* __restrict__ off, int64_t universe, int64_t rows,
                                  int64_t* __restrict__ keys) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < rows; p += (int64_t)gridDim.x * blockDim.x) {
@@ -98,6 +112,24 @@ extern "C" int jq_gen_zipf_sorted_keys(jq_ctx* ctx, uint64_t seed, int64_t rows,
   JQ_CHECK_LAUNCH(ctx);
   JQ_TRY(scan_i64_dev(ctx, hist, universe, nullptr, off));
   zipf_fill_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(off, universe, rows, dkeys);
+  JQ_CHECK_LAUNCH(ctx);
+  JQ_TRY(copy_out(ctx, keys_out, (const int64_t*)dkeys, rows));
+  return sync_and_check_flags(ctx);
+}
+
+extern "C" int jq_gen_zipf_keys(jq_ctx* ctx, uint64_t seed, int64_t rows, const double* cdf, int64_t universe,
+                                int64_t* keys_out) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (rows < 0 || universe <= 0) return fail(JQ_E_INVALID, "bad Zipf geometry");
+  if (rows == 0) return JQ_OK;
+  JQ_TRY(begin_call(ctx));
+  JQ_TRY(ws_reserve(ctx, stage_bytes(cdf, universe) + stage_bytes((const int64_t*)keys_out, rows)));
+  const double* dcdf;
+  int64_t* dkeys;
+  JQ_TRY(stage_in(ctx, cdf, universe, &dcdf));
+  JQ_TRY(stage_out(ctx, keys_out, rows, &dkeys));
+  const int64_t blocks = std::min<int64_t>(cdiv(rows, 256), int64_t(ctx->sms) * 16);
+  zipf_keys_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(seed, rows, dcdf, universe, dkeys);
   JQ_CHECK_LAUNCH(ctx);
   JQ_TRY(copy_out(ctx, keys_out, (const int64_t*)dkeys, rows));
   return sync_and_check_flags(ctx);

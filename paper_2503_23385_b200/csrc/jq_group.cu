@@ -9,8 +9,9 @@
 //   run tables (start, key) -> binary-search match of A runs in B runs ->
 //   scan of match flags = group ids in ascending key order -> group tables,
 //   red_off = exclusive scan of (a_count + b_count - 1) -> per-row group ids.
-// The GPU stable LSD radix sort (for tables that arrive unsorted) lives with the
-// generator, jq_gen.cu.
+// Tables that arrive unsorted are sorted first, opt-in, by the GPU stable LSD radix
+// sort of jq_sort.cu (bit-exact with np.argsort(kind="stable")); the default keeps the
+// SPEC's ValueError for unsorted keys.
 #include <algorithm>
 
 #include "jq_internal.cuh"

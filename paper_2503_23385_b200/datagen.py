@@ -58,6 +58,34 @@ def zipf_sorted_keys(seed: int, rows: int, s: float = 1.1, universe: int = 1_000
     return out
 
 
+def zipf_keys(seed: int, rows: int, s: float = 1.1, universe: int = 1_000_000, out=None):
+    """Unsorted Zipf(s) keys, one per row: searchsorted(cdf, u_row, 'right')."""
+    cdf = zipf_cdf(s, universe)
+    if out is None:
+        out = np.empty(rows, dtype=np.int64)
+    N.use_torch_stream(out)
+    N.check(N.lib().jq_gen_zipf_keys(N.ctx(), seed & 0xFFFFFFFFFFFFFFFF, rows, cdf.ctypes.data, universe,
+                                     N.ptr(out)))
+    return out
+
+
+def zipf_table(seed_keys: int, seed_data: int, rows: int, cols: int, device=None, s: float = 1.1,
+               universe: int = 1_000_000) -> Table:
+    """C3 recipe: per-row Zipf keys and uniform rows in generation
+    order, then a stable sort of (key, row) permutes the data rows (GPU radix sort +
+    row gather).  device=None: numpy tables; else torch tensors on that device."""
+    from .joins import argsort_keys, gather_rows
+    if device is None:
+        keys, data = zipf_keys(seed_keys, rows, s, universe), uniform(seed_data, rows, cols)
+    else:
+        import torch
+        keys = zipf_keys(seed_keys, rows, s, universe,
+                         out=torch.empty(rows, dtype=torch.int64, device=device))
+        data = uniform(seed_data, rows, cols, out=torch.empty((rows, cols), dtype=torch.float64, device=device))
+    sk, perm = argsort_keys(keys)
+    return Table(gather_rows(data, perm), sk)
+
+
 def gen_uniform(spec: GenSpec) -> Table:
     """rows x cols uniform(0,1), same spec -> bit-identical table."""
     if spec.rows < 1 or spec.cols < 1:

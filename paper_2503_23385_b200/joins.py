@@ -70,20 +70,59 @@ def reduce_cartesian(a, b) -> ReducedMatrix:
     return _reduce(a, None, b, None)
 
 
-def reduce_natural_join(a: Table, b: Table) -> ReducedMatrix:
-    """missing keys / unsorted keys -> ValueError."""
+def reduce_natural_join(a: Table, b: Table, sort: bool = False) -> ReducedMatrix:
+    """missing keys / unsorted keys -> ValueError.  ``sort=True``
+    (opt-in, not in the reference) first sorts both tables by key on the GPU
+    (sort_by_key); group_boundaries then refer to the sorted tables."""
     if a.keys is None or b.keys is None:
         raise ValueError("reduce_natural_join needs keys on both tables")
+    if sort:
+        a, b = sort_by_key(a), sort_by_key(b)
     return _reduce(a.data, a.keys, b.data, b.keys)
 
 
-def reduce_join(a: Table, b: Table) -> ReducedMatrix:
+def reduce_join(a: Table, b: Table, sort: bool = False) -> ReducedMatrix:
     """Dispatcher exported by the reference (pkg/src/joinqr/__init__.py:38)."""
     if (a.keys is None) != (b.keys is None):
         raise ValueError("both tables must carry keys, or neither")
     if a.keys is None:
         return reduce_cartesian(a.data, b.data)
-    return reduce_natural_join(a, b)
+    return reduce_natural_join(a, b, sort=sort)
+
+
+def argsort_keys(keys):
+    """(sorted keys, permutation) of an int64 key column by the GPU stable LSD radix
+    sort (jq_sort.cu): perm equals np.argsort(keys, kind="stable") bit for bit and
+    sorted = keys[perm].  numpy in -> numpy out, torch CUDA in -> torch CUDA out."""
+    k = as_keys(keys, len(keys))
+    out_k = like((len(k),), k, dtype="i8")
+    perm = like((len(k),), k, dtype="i8")
+    N.use_torch_stream(k)
+    N.check(N.lib().jq_sort_keys(N.ctx(), N.ptr(k), len(k), N.ptr(out_k), N.ptr(perm)))
+    return out_k, perm
+
+
+def gather_rows(x, perm):
+    """x[perm] for a row-major table on the GPU (jq_gather_rows)."""
+    x = as_matrix(x)
+    perm = as_keys(perm, len(perm))
+    rows, cols = x.shape
+    if len(perm) != rows:
+        raise ValueError("permutation length does not match the row count")
+    out = like((rows, cols), x)
+    N.use_torch_stream(x, perm)
+    N.check(N.lib().jq_gather_rows(N.ctx(), N.ptr(x), rows, cols, N.ptr(perm), N.ptr(out)))
+    return out
+
+
+def sort_by_key(t: Table) -> Table:
+    """The table with its rows stably sorted by key (GPU radix sort + row gather).
+    The reference requires sorted keys and raises otherwise; this is
+    the opt-in way to feed it unsorted tables.  Keyless tables are returned as is."""
+    if t.keys is None:
+        return t
+    keys, perm = argsort_keys(t.keys)
+    return Table(gather_rows(t.data, perm), keys)
 
 
 def group_keys(keys_a, keys_b):

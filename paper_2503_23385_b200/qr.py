@@ -38,19 +38,24 @@ def canonicalize(r):
     return out
 
 
-def _tables(a: Table, b: Table):
+def _tables(a: Table, b: Table, sort: bool = False):
     if not isinstance(a, Table):
         a = Table(a)
     if not isinstance(b, Table):
         b = Table(b)
     if (a.keys is None) != (b.keys is None):
         raise ValueError("both tables must carry keys, or neither")
+    if sort and a.keys is not None:
+        from .joins import sort_by_key
+        a, b = sort_by_key(a), sort_by_key(b)
     return a, b
 
 
-def figaro_r(a: Table, b: Table):
-    """Canonical R of the join matrix, join never materialised."""
-    a, b = _tables(a, b)
+def figaro_r(a: Table, b: Table, sort: bool = False):
+    """Canonical R of the join matrix, join never materialised.
+    ``sort=True`` (opt-in) sorts unsorted keyed tables on the GPU first (sort_by_key);
+    by default unsorted keys raise ValueError as in the reference."""
+    a, b = _tables(a, b, sort)
     m1, n1 = a.data.shape
     m2, n2 = b.data.shape
     out = like((n1 + n2, n1 + n2), a.data, b.data)

@@ -35,9 +35,10 @@ def svd_of_r(r, want_vectors: bool = False) -> SvdResult:
     return SvdResult(vals, v)
 
 
-def figaro_svd(a, b, want_vectors: bool = False) -> SvdResult:
-    """figaro_r followed by svd_of_r, in one device pipeline."""
-    a, b = _tables(a, b)
+def figaro_svd(a, b, want_vectors: bool = False, sort: bool = False) -> SvdResult:
+    """figaro_r followed by svd_of_r, in one device pipeline (SPEC.md:340-347);
+    ``sort`` as in figaro_r."""
+    a, b = _tables(a, b, sort)
     m1, n1 = a.data.shape
     m2, n2 = b.data.shape
     n = n1 + n2

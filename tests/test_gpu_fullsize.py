@@ -101,6 +101,33 @@ def test_c3_zipf_join_full(P, c3_keys, variant):
     check_against_gram(r, g)
 
 
+def test_c3_recipe_radix_sort_full(P):
+    """C3 as SURVEY.md §8d specifies it: per-row Zipf keys and data rows in generation
+    order, the GPU stable radix sort permutes the rows (1e7 per side).  Keys and the
+    permutation are bit-exact with np.argsort(kind="stable"); R matches the Gram oracle
+    of the permuted tables."""
+    import torch
+    from paper_2503_23385_b200 import datagen
+    m, n = 10_000_000, 32
+    ta = datagen.zipf_table(3003, SEEDS[3][0], m, n, device="cuda")
+    tb = datagen.zipf_table(3004, SEEDS[3][1], m, n, device="cuda")
+    ku_a, ku_b = O.zipf_keys(3003, m), O.zipf_keys(3004, m)
+    pa, pb = np.argsort(ku_a, kind="stable"), np.argsort(ku_b, kind="stable")
+    assert np.array_equal(ta.keys.cpu().numpy(), ku_a[pa])
+    assert np.array_equal(tb.keys.cpu().numpy(), ku_b[pb])
+    _, perm_a = P.argsort_keys(torch.from_numpy(ku_a).cuda())
+    assert np.array_equal(perm_a.cpu().numpy(), pa)
+    P.set_variant("footnote")
+    try:
+        r = P.figaro_r(ta, tb).cpu().numpy()
+    finally:
+        P.set_variant("dense")
+        del ta, tb
+        torch.cuda.empty_cache()
+    g = cgram.join_gram(SEEDS[3][0], m, n, SEEDS[3][1], m, n, ku_a[pa], ku_b[pb], pa, pb)
+    check_against_gram(r, g)
+
+
 @pytest.mark.parametrize("variant", ["footnote", "dense"])
 def test_c5_full_svd(P, variant):
     """C5: 1e6 x 128 |x| 1e6 x 128, singular values and right vectors."""

@@ -210,3 +210,17 @@ def test_factorised_gram_oracle():
     g = O.factorised_gram(a, b)
     r = O.figaro_r(a, b, lapack=True)
     assert np.abs(O.gram_r(g) - r).max() <= 1e-10 * np.abs(r).max()
+
+
+def test_c_gram_oracle_with_permuted_rows():
+    """oracle/c gram with row permutations (the C3 recipe's stable key sort) equals
+    the numpy factorised Gram of the permuted tables."""
+    from oracle import cgram
+    if not cgram.available():
+        pytest.skip("oracle/c not built")
+    t_a, pa = O.datagen.zipf_sorted_table(77, 78, 3000, 3, universe=50)
+    t_b, pb = O.datagen.zipf_sorted_table(79, 80, 2000, 4, universe=50)
+    assert np.array_equal(pa, np.argsort(O.zipf_keys(77, 3000, universe=50), kind="stable"))
+    g = cgram.join_gram(78, 3000, 3, 80, 2000, 4, t_a.keys, t_b.keys, pa, pb)
+    g_ref = O.factorised_gram(t_a, t_b)
+    assert np.abs(g - g_ref).max() <= 1e-12 * np.abs(g_ref).max()
