@@ -180,6 +180,19 @@ JQ_API int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64
 JQ_API int jq_figaro_r_shard_local(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1,
                                    const double* b, int64_t b_rows, int64_t n2, int64_t m2, double* r_local,
                                    double* sums);
+/* Rows completing the join Gram of key groups split by rows across shards
+ * (SURVEY.md §8e co-partition; a Cartesian product is one group split over every
+ * rank).  Part k (ordered by part_group[k], groups contiguous, parts of a group in
+ * shard order) holds part_rows[2k] A rows and part_rows[2k+1] B rows of its group and
+ * was factored by jq_figaro_r_shard_local with the group's m1g / m2g (the sums of the
+ * group's parts) -- part_sums[k] is that call's sums (n1 + n2).  Writes per group the
+ * head row [sqrt(m2g) hA | sqrt(m1g) hB] and one between-part row per side and part
+ * after the first (pairwise scatter update).  rows == NULL only reports *n_rows.
+ * part_rows / part_group are host arrays; part_sums and rows host or device.
+ * Replaces the host-side prefix / head arithmetic of the carry exchange. */
+JQ_API int jq_split_group_rows(jq_ctx* ctx, const double* part_sums, const int64_t* part_rows,
+                               const int64_t* part_group, int64_t nparts, int64_t n1, int64_t n2, double* rows,
+                               int64_t rows_capacity, int64_t* n_rows);
 /* Canonical R of the row stack [R_0; R_1; ...; R_{count-1}] (each n x n), by
  * the fixed binary TSQR tree — identical on every rank for the same input. */
 JQ_API int jq_tsqr_stack(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, double* r);

@@ -52,6 +52,7 @@ SIGNATURES = {
     "jq_figaro_r_shard": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, C.c_int, _P],
     "jq_figaro_r_shard_local": [_P, _P, _I64, _I64, _I64, _P, _I64, _I64, _I64, _P, _P],
     "jq_tsqr_stack": [_P, _P, _I64, _I64, _P],
+    "jq_split_group_rows": [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I64, _P],
     "jq_materialize": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _P, _I64, _P],
     "jq_join_r_bruteforce": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _P],
 }

@@ -467,6 +467,45 @@ __global__ void shard_rows_kernel(BlockSide sa, const double* __restrict__ pre_a
   rows[(side_a ? n : 0) + c] = 0.0;
 }
 
+// Rows that complete the Gram of key groups split by rows across shards (multi-GPU
+// co-partition; the Cartesian product is one group split over every
+// rank).  Each shard factored its part of group g as a carry-free block: local tails
+// scaled by sqrt(m2g) / sqrt(m1g) (jq_figaro_r_shard_local).  What the parts' R's miss
+// is, per group, the head row [sqrt(m2g) SA / sqrt(m1g) | sqrt(m1g) SB / sqrt(m2g)] and
+// per side one between-part row per part k >= 1 (pairwise scatter update, as
+// block_rows_kernel):  v_k = scale sqrt(W m_k / (W + m_k)) (s_k / m_k - S / W).
+// One CTA per group, one thread per column, parts in order: deterministic.  Rows of a
+// group: head, A rows, B rows from row0[g]; the caller zero-fills `out`.
+__global__ void split_group_rows_kernel(const double* __restrict__ sums, const int64_t* __restrict__ prows,
+                                        const int64_t* __restrict__ first_part, const int64_t* __restrict__ row0,
+                                        const int64_t* __restrict__ na_rows, int n1, int n2,
+                                        double* __restrict__ out) {
+  const int64_t g = blockIdx.x;
+  const int n = n1 + n2;
+  const int64_t k0 = first_part[g], k1 = first_part[g + 1];
+  double m1g = 0.0, m2g = 0.0;
+  for (int64_t k = k0; k < k1; ++k) {
+    m1g += (double)prows[2 * k];
+    m2g += (double)prows[2 * k + 1];
+  }
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const bool side_a = c < n1;
+    const double scale = sqrt(side_a ? m2g : m1g);
+    int64_t r = row0[g] + 1 + (side_a ? 0 : na_rows[g]);
+    double W = 0.0, S = 0.0;
+    for (int64_t k = k0; k < k1; ++k) {
+      const double mk = (double)prows[2 * k + (side_a ? 0 : 1)];
+      if (mk <= 0.0) continue;
+      const double sk = sums[k * n + c];
+      if (W > 0.0) out[r++ * n + c] = scale * sqrt(W * mk / (W + mk)) * (sk / mk - S / W);
+      W += mk;
+      S += sk;
+    }
+    const double mx = side_a ? m1g : m2g;
+    out[row0[g] * n + c] = (mx > 0.0) ? scale * (S / sqrt(mx)) : 0.0;
+  }
+}
+
 // Column sums of the shard (A then B) from its leaves' block sums, in block order.
 __global__ void block_total_kernel(BlockSide sa, BlockSide sb, double* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1082,6 +1121,60 @@ int jq_figaro_r_shard_local(jq_ctx* ctx, const double* a, int64_t a_rows, int64_
   const int rc = sync_and_check_flags(ctx);
   record_timing(ctx, false);
   return rc;
+}
+
+int jq_split_group_rows(jq_ctx* ctx, const double* part_sums, const int64_t* part_rows,
+                        const int64_t* part_group, int64_t nparts, int64_t n1, int64_t n2, double* rows,
+                        int64_t rows_capacity, int64_t* n_rows) {
+  if (!ctx) return fail(JQ_E_INVALID, "null context");
+  if (nparts < 0 || n1 < 0 || n2 < 0 || n1 + n2 == 0 || n1 + n2 > 1024) return fail(JQ_E_INVALID, "bad geometry");
+  if (nparts > 0 && (!part_sums || !part_rows || !part_group)) return fail(JQ_E_INVALID, "null argument");
+  const int64_t n = n1 + n2;
+  // group layout on the host (part_rows / part_group are small host arrays)
+  std::vector<int64_t> first{0}, row0, na;
+  int64_t total = 0;
+  for (int64_t k = 0; k < nparts; ++k) {
+    if (part_rows[2 * k] < 0 || part_rows[2 * k + 1] < 0) return fail(JQ_E_INVALID, "negative part size");
+    if (k > 0 && part_group[k] < part_group[k - 1]) return fail(JQ_E_INVALID, "parts must be ordered by group");
+    if (k + 1 == nparts || part_group[k + 1] != part_group[k]) first.push_back(k + 1);
+  }
+  const int64_t ng = (int64_t)first.size() - 1;
+  for (int64_t g = 0; g < ng; ++g) {
+    int64_t ca = 0, cb = 0;
+    for (int64_t k = first[g]; k < first[g + 1]; ++k) {
+      ca += part_rows[2 * k] > 0;
+      cb += part_rows[2 * k + 1] > 0;
+    }
+    row0.push_back(total);
+    na.push_back(std::max<int64_t>(ca - 1, 0));
+    total += 1 + std::max<int64_t>(ca - 1, 0) + std::max<int64_t>(cb - 1, 0);
+  }
+  if (n_rows) *n_rows = total;
+  if (!rows) return JQ_OK;
+  if (total > rows_capacity) return fail(JQ_E_INVALID, "row output capacity too small");
+  if (total == 0) return JQ_OK;
+  JQ_TRY(begin_call(ctx));
+  JQ_TRY(ws_reserve(ctx, stage_bytes(part_sums, nparts * n) + stage_bytes((const double*)rows, total * n) +
+                             4 * ws_bytes(nparts * 2 + ng + 2, 8)));
+  const double* dsums;
+  double* dout;
+  JQ_TRY(stage_in(ctx, part_sums, nparts * n, &dsums));
+  JQ_TRY(stage_out(ctx, rows, total * n, &dout));
+  int64_t* meta = ws_alloc<int64_t>(ctx, 2 * nparts + (ng + 1) + 2 * ng);
+  if (!meta) return fail(JQ_E_OOM, "workspace exhausted (split group rows)");
+  std::vector<int64_t> hm(part_rows, part_rows + 2 * nparts);
+  hm.insert(hm.end(), first.begin(), first.end());
+  hm.insert(hm.end(), row0.begin(), row0.end());
+  hm.insert(hm.end(), na.begin(), na.end());
+  JQ_CUDA(cudaMemcpyAsync(meta, hm.data(), hm.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  JQ_CUDA(cudaMemsetAsync(dout, 0, total * n * 8, ctx->stream));
+  split_group_rows_kernel<<<(unsigned)ng, 256, 0, ctx->stream>>>(dsums, meta, meta + 2 * nparts,
+                                                                  meta + 2 * nparts + ng + 1,
+                                                                  meta + 2 * nparts + ng + 1 + ng, (int)n1, (int)n2,
+                                                                  dout);
+  JQ_CHECK_LAUNCH(ctx);
+  JQ_TRY(copy_out(ctx, rows, (const double*)dout, total * n));
+  return sync_and_check_flags(ctx);
 }
 
 int jq_tsqr_stack(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, double* r) {

@@ -126,23 +126,22 @@ __global__ void __launch_bounds__(RS_THREADS) scatter_kernel(const int64_t* __re
   }
 }
 
-// out[i, :] = x[perm[i], :] (row-major, cols columns); 16-byte accesses when aligned
-__global__ void gather_rows_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,
-                                   const int64_t* __restrict__ perm, double* __restrict__ out) {
-  const bool vec = (cols % 2 == 0) && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
-  if (vec) {
-    const int64_t half = cols / 2, total = rows * half;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t i = e / half, c = e - i * half;
-      const int64_t src = __ldg(perm + i);
-      reinterpret_cast<double2*>(out)[e] = __ldg(reinterpret_cast<const double2*>(x + src * cols) + c);
-    }
-  } else {
-    const int64_t total = rows * cols;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t i = e / cols, c = e - i * cols;
-      out[e] = __ldg(x + __ldg(perm + i) * cols + c);
-    }
+// out[i, :] = x[perm[i], :] (row-major).  L lanes per row (L = the row's 16-byte (or
+// 8-byte) items rounded up to a power of two, <= 32), 32 / L rows per warp: every row
+// is one contiguous read, no per-element integer division.
+template <class V>
+__global__ void gather_rows_kernel(const V* __restrict__ x, int64_t rows, int64_t items, int lshift,
+                                   const int64_t* __restrict__ perm, V* __restrict__ out) {
+  const int L = 1 << lshift;
+  const int lane = threadIdx.x & 31, sub = lane >> lshift, c0 = lane & (L - 1);
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int rpw = 32 >> lshift;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w * rpw < rows; w += warps) {
+    const int64_t i = w * rpw + sub;
+    if (i >= rows) continue;
+    const V* src = x + __ldg(perm + i) * items;
+    V* dst = out + i * items;
+    for (int64_t c = c0; c < items; c += L) dst[c] = __ldg(src + c);
   }
 }
 
@@ -207,9 +206,17 @@ int sort_keys_dev(jq_ctx* ctx, const int64_t* keys, int64_t m, int64_t* keys_out
 
 int gather_rows_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int64_t* perm, double* out) {
   if (rows == 0 || cols == 0) return JQ_OK;
-  const int64_t work = rows * cols / ((cols % 2) ? 1 : 2);
-  gather_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(work, 256), int64_t(ctx->sms) * 16), 256, 0,
-                       ctx->stream>>>(x, rows, cols, perm, out);
+  const bool vec = (cols % 2 == 0) && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const int64_t items = vec ? cols / 2 : cols;
+  int lshift = 0;
+  while ((1 << lshift) < items && lshift < 5) ++lshift;
+  const int64_t warps = cdiv(rows, 32 >> lshift);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(warps, 8), int64_t(ctx->sms) * 16);
+  if (vec)
+    gather_rows_kernel<double2><<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const double2*>(x), rows, items,
+                                                                 lshift, perm, reinterpret_cast<double2*>(out));
+  else
+    gather_rows_kernel<double><<<blocks, 256, 0, ctx->stream>>>(x, rows, items, lshift, perm, out);
   JQ_CHECK_LAUNCH(ctx);
   return JQ_OK;
 }
