@@ -119,10 +119,10 @@ int jq_oracle_gram_perm(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, 
   } else {
     /* one group: column sums in parallel blocks, fixed-order reduction */
     int nt = omp_get_max_threads();
-    double* pa = (double*)calloc((size_t)nt * (n1 + n2 + 1), sizeof(double));
+    double* part = (double*)calloc((size_t)nt * (n1 + n2 + 1), sizeof(double));
 #pragma omp parallel
     {
-      double* p = pa + (size_t)omp_get_thread_num() * (n1 + n2 + 1);
+      double* p = part + (size_t)omp_get_thread_num() * (n1 + n2 + 1);
 #pragma omp for schedule(static)
       for (int64_t r = 0; r < m1; ++r)
         for (int c = 0; c < n1; ++c) p[c] += unif(seed_a, grow(pa, r) * n1 + c);
@@ -131,10 +131,10 @@ int jq_oracle_gram_perm(uint64_t seed_a, int64_t m1, int n1, const int64_t* ka, 
         for (int c = 0; c < n2; ++c) p[n1 + c] += unif(seed_b, grow(pb, r) * n2 + c);
     }
     for (int t = 0; t < nt; ++t) {
-      for (int c = 0; c < n1; ++c) sa[c] += pa[(size_t)t * (n1 + n2 + 1) + c];
-      for (int c = 0; c < n2; ++c) sb[c] += pa[(size_t)t * (n1 + n2 + 1) + n1 + c];
+      for (int c = 0; c < n1; ++c) sa[c] += part[(size_t)t * (n1 + n2 + 1) + c];
+      for (int c = 0; c < n2; ++c) sb[c] += part[(size_t)t * (n1 + n2 + 1) + n1 + c];
     }
-    free(pa);
+    free(part);
     for (int p = 0; p < n1; ++p)
       for (int q = 0; q < n2; ++q) G[p * n + n1 + q] = sa[p] * sb[q];
   }

@@ -98,6 +98,7 @@ struct Cfg {
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(KW % 8 == 0, "whole row tiles per warp");
+  static_assert(OFF_S - OFF_U >= 16 * LDT + 16, "factor_panel_chol scratch (U .. P)");
 };
 
 // R element (r, c), c >= 8 * (r / 8), in the packed (smem) or dense (global) layout
@@ -929,6 +930,116 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
   return ok;
 }
 
+// ------------------------------------------------------------------ Cholesky panel
+// The same panel factorisation as factor_panel_gram (identical outputs: R rows, M', T,
+// the guard), derived in closed form from S = R_p^T R_p + G instead of the 8-step
+// reflector chain.  For the stacked panel [R_p; X] (R_p: the panel's 8 x 8 upper R
+// block, X: the chunk rows) the Householder QR with reflectors v = [e_j; y_j] is
+//   R_new = D chol(S)^T,  D_jj = -sign(R_p[j][j])   (beta = -sign(alpha) |.|: no
+//                                                   cancellation in W = R_p - R_new)
+//   Y = X W^{-1}  (M' = W^{-1}),    T = -W R_new^{-1}
+// (Q^T [R_p; X] = [R_new; 0] with Q = I - V T V^T, V = [I; Y], fixes Y and T given
+// R_new; T^{-1} + T^{-T} = I + Y^T Y follows from R_new^T R_new = R_p^T R_p + X^T X).
+// The critical path is the 8 Cholesky steps, each ONE reciprocal (MUFU + one cubic
+// correction) between two shuffles -- versus rsqrt then rcp plus the T column in the
+// reflector chain -- then W^{-1} and R_new^{-1} by back substitution (one lane per
+// column, operands in shared memory `scr`: >= 16 LDT + 16 doubles, the explicit path's
+// U / taus / scales / partials, idle while the chain runs) and one 8 x 8 DMMA product.  Guard: every pivot (= R_new[j][j]^2, the quantity the
+// reflector chain's guard tests) must be >= 1e-2 (S[j][j] + Pg_j): S[j][j] bounds the
+// rounding error of the Cholesky elimination, Pg that of the (derived) Gram.  Otherwise
+// the panel is redone by factor_panel_all, as with the reflector chain.
+template <class C>
+__device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (&Rb)[2], const double* Rs,
+                                                  const int j0, double* T, double* Mg, double* scr,
+                                                  const int lane, const double Pg) {
+  const int g = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
+  // R_p in accumulator layout, and the fragments R_p[2t+b][g] of R_p^T R_p
+  const double rp0 = (c0 >= g) ? Rs[rix<C>(j0 + g, j0 + c0)] : 0.0;
+  const double rp1 = (c1 >= g) ? Rs[rix<C>(j0 + g, j0 + c1)] : 0.0;
+  const double rt0 = (g >= c0) ? Rs[rix<C>(j0 + c0, j0 + g)] : 0.0;
+  const double rt1 = (g >= c1) ? Rs[rix<C>(j0 + c1, j0 + g)] : 0.0;
+  const double alpha = Rs[rix<C>(j0 + g, j0 + g)];
+  const double dsg = alpha >= 0.0 ? -1.0 : 1.0;  // D_gg
+  double S[2] = {G[0], G[1]};
+  dmma(S, rt0, rt0);
+  dmma(S, rt1, rt1);
+  const double sdiag = diag_of(S, lane);
+  // 8 Cholesky steps; lanes of quad j keep row j of S^{(j)} (R_new row j up to the
+  // 1 / sqrt(pivot) applied after the loop: no rsqrt on the critical path)
+  double piv_g = 1.0, sv0 = 0.0, sv1 = 0.0;
+  bool rng_ok = true;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double e = (j & 1) ? S[1] : S[0];
+    const double piv = __shfl_sync(FULL, e, 4 * j + (j >> 1));  // S[j][j]
+    const double sgj = __shfl_sync(FULL, e, 4 * g + (j >> 1));  // S[g][j]
+    const double sj0 = __shfl_sync(FULL, S[0], 4 * j + t);      // S[j][c0]
+    const double sj1 = __shfl_sync(FULL, S[1], 4 * j + t);      // S[j][c1]
+    const bool in = piv > 1e-280 && piv < 1e280;               // MUFU approximations' safe range
+    rng_ok = rng_ok && in;
+    const double f = sgj * rcp_nr(in ? piv : 1.0);  // S[g][c] -= S[g][j] S[j][c] / S[j][j]  (g, c > j)
+    if (g == j) {
+      piv_g = piv;
+      sv0 = c0 >= j ? sj0 : 0.0;
+      sv1 = c1 >= j ? sj1 : 0.0;
+    }
+    if (g > j && c0 > j) S[0] = fma(-f, sj0, S[0]);
+    if (g > j && c1 > j) S[1] = fma(-f, sj1, S[1]);
+  }
+  const double rs_g = rsqrt_nr(rng_ok ? piv_g : 1.0);
+  Rb[0] = dsg * sv0 * rs_g;  // R_new[g][:] = D_g S^{(g)}[g][:] / sqrt(pivot_g)
+  Rb[1] = dsg * sv1 * rs_g;
+  const double w0 = rp0 - Rb[0], w1 = rp1 - Rb[1];
+  // W and R_new in natural layout (scratch), their diagonals' reciprocals
+  double* Un = scr;                 // [2][8][LDT]: W, R_new
+  double* dg = scr + 16 * C::LDT;   // [2][8]: 1 / W[i][i], 1 / R_new[i][i]
+  *reinterpret_cast<double2*>(Un + g * C::LDT + c0) = make_double2(w0, w1);
+  *reinterpret_cast<double2*>(Un + (8 + g) * C::LDT + c0) = make_double2(Rb[0], Rb[1]);
+  if (t == 0) {
+    dg[g] = rcp_nr(alpha - dsg * piv_g * rs_g);  // W[g][g] = alpha - R_new[g][g]
+    dg[8 + g] = dsg * rs_g;                      // 1 / R_new[g][g]
+  }
+  __syncwarp();
+  // Inverses of the two upper-triangular matrices by back substitution, one lane per
+  // column (lanes 0..7: W^{-1} = M', lanes 8..15: R_new^{-1}), the same code on every
+  // lane (no divergence), right-looking: per step one multiply + one FMA on the path.
+  {
+    const int m = (lane >> 3) & 1, c = lane & 7;
+    const double* U = Un + m * 8 * C::LDT;
+    const double* d = dg + 8 * m;
+    double acc[8], x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int k = 7; k >= 0; --k) {
+      const double xk = -d[k] * acc[k];
+      x[k] = k > c ? 0.0 : (k == c ? d[k] : xk);
+#pragma unroll
+      for (int i = 0; i < k; ++i) acc[i] = fma(U[i * C::LDT + k], x[k], acc[i]);
+    }
+    __syncwarp();
+    if (lane < 16) {
+      double* out = m ? T : Mg;  // R_new^{-1} parks in T's buffer
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i * C::LDT + c] = x[i];
+    }
+  }
+  __syncwarp();
+  // T = -W R_new^{-1}  (B fragments R_new^{-1}[2t+b][g] from the parked copy)
+  const double b0 = T[c0 * C::LDT + g], b1 = T[c1 * C::LDT + g];
+  double P[2] = {0.0, 0.0};
+  dmma(P, w0, b0);
+  dmma(P, w1, b1);
+  __syncwarp();
+  *reinterpret_cast<double2*>(T + g * C::LDT + c0) = make_double2(-P[0], -P[1]);
+  const bool good = rng_ok && piv_g >= 1e-2 * (sdiag + Pg);
+  const bool ok = __all_sync(FULL, good);
+#ifdef JQ_KTIME
+  if (!ok && lane == 0) atomicAdd(&g_gram_fail[0], 1ull);
+#endif
+  return ok;
+}
+
 // ------------------------------------------------------------------ the kernel
 // Each CTA: R (init zero, or R_init[cta]) absorbs its rows [row_begin, row_end)
 // of `src`, then writes R (NP x NP, row-major, zeros below the diagonal) to
@@ -1126,7 +1237,10 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
           G[1] += gg.y;
         }
         double Rb[2];
-        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, T, Mg, lane, diag_of(G, lane)) && !(use_tma & 2);
+        const double pg = diag_of(G, lane);
+        bool ok = !(use_tma & 16) && factor_panel_chol<C>(G, Rb, R, j0, T, Mg, U, lane, pg);
+        if (!ok) ok = factor_panel_gram<C>(G, Rb, R, j0, T, Mg, lane, pg);  // looser guard
+        ok = ok && !(use_tma & 2);
         if (ok) {  // commit the panel's R rows
           if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
           if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];
@@ -1269,6 +1383,28 @@ static int ctas_per_sm() {
   return std::max(1, n);
 }
 
+// JQ_TSQR_CHAIN=householder: the reflector chain (factor_panel_gram) instead of the
+// Cholesky panel (factor_panel_chol, the default); kernel flag 16.  A/B and parity only.
+static int chain_flag() {
+  static const int f = [] {
+    const char* e = getenv("JQ_TSQR_CHAIN");
+    return (e && strcmp(e, "householder") == 0) ? 16 : 0;
+  }();
+  return f;
+}
+
+// Kernel flag 32 (opt-in, JQ_TSQR_REDUCERS=1): the ws2 leaf's spare warps reduce the
+// trailing tiles (reducer warps) when they have no side scan to run.  Measured slower at
+// C4 (175.1 vs 169.5 ms): the reducers sit on SM sub-partition 0 with the chain, whose
+// lookahead then publishes V later, and the data warps wait on two V barriers per panel.
+static int reducer_flag(int nspare, const SideScan& side) {
+  static const bool on = [] {
+    const char* e = getenv("JQ_TSQR_REDUCERS");
+    return e && e[0] == '1';
+  }();
+  return (on && nspare > 0 && side.x == nullptr) ? 32 : 0;
+}
+
 template <class C, class Src, bool COMBINE>
 static int launch_tsqr(jq_ctx* ctx, int grid, const Src& src, int64_t rows_per_cta,
                        int64_t total_rows, const double* r_init, int64_t init_count, double* r_out,
@@ -1281,6 +1417,7 @@ static int launch_tsqr(jq_ctx* ctx, int grid, const Src& src, int64_t rows_per_c
     return e && e[0] == '1';
   }();
   if (explicit_panels) use_tma |= 2;
+  use_tma |= chain_flag();
   kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, rows_per_cta, total_rows, r_init,
                                                    init_count, r_out, use_tma);
   JQ_CHECK_LAUNCH(ctx);
@@ -1441,7 +1578,8 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t 
   auto kern = tsqr_ws2_kernel<CS, Src>;
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM));
   kern<<<(int)ctas, CS::THREADS, CS::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a,
-                                                          (use_tma ? 1 : 0) | (explicit_panels ? 2 : 0) | debug_flags);
+                                                          (use_tma ? 1 : 0) | (explicit_panels ? 2 : 0) | debug_flags |
+                                                              chain_flag() | reducer_flag(CS::NSPARE, src.side_job()));
   JQ_CHECK_LAUNCH(ctx);
   if (defer) {
     *defer = LeafSet{a, b, ctas, C::NP, n, rows_per_cta};

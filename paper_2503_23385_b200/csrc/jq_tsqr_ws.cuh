@@ -66,11 +66,12 @@ struct CfgS {
   static constexpr int NSPARE = WARPS - 1 - NLOAD - DW;  // spare warps: the side scan (FigaroSrc::side_scan)
   static constexpr int OFF_LSR = OFF_GD + DW * 64;        // [NLOAD][2][64] loader segment sums
   static constexpr int OFF_ROLE = OFF_LSR + NLOAD * 128;  // WARPS ints: SMSP of each warp
-  static constexpr int OFF_BAR = OFF_ROLE + WARPS / 2;    // mbarriers: TMA, READY, FREE, VREADY
-  static constexpr int TOTAL = OFF_BAR + 4;
+  static constexpr int OFF_BAR = OFF_ROLE + WARPS / 2;    // mbarriers: TMA, READY, FREE, VREADY, VREADY2
+  static constexpr int TOTAL = OFF_BAR + 5;
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
   static_assert(SMEM <= (MIN_CTAS == 1 ? 227 : 113) * 1024, "shared memory per CTA");
   static_assert(NP <= 128, "loader transform assumes <= 128 columns per side");
+  static_assert(OFF_LD - OFF_U >= 16 * LDT + 16, "factor_panel_chol scratch (U .. P)");
 };
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned count) {
@@ -93,6 +94,7 @@ __device__ long long g_trace[4096];
 constexpr int BAR_ALL = 1;   // chain + data warps
 constexpr int BAR_DATA = 2;  // data warps
 constexpr int BAR_LOAD = 3;  // loader warps
+constexpr int BAR_GD = 4;    // chain + data warps: direct Gram after an explicit panel
 
 // ------------------------------------------------------------------ the kernel (ws2)
 // The chain warp also performs, right after B_p,
@@ -125,13 +127,19 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
   uint64_t* bar_ready = bar_tma + 1;
   uint64_t* bar_free = bar_tma + 2;
   uint64_t* bar_v = bar_tma + 3;
+  uint64_t* bar_v2 = bar_tma + 4;  // reducer warps -> data warps (tiles q > p + 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int64_t cta = blockIdx.x;
   const int64_t row_begin = cta * rows_per_cta;
   const int64_t row_end = min(total_rows, row_begin + rows_per_cta);
-  constexpr int NALL = (C::DW + 1) * 32;
+  constexpr int NALL = (C::DW + 1) * 32;  // chain + data warps
+  // REDUCER warps (flags & 32: the spare warps have no side scan to run): they reduce the
+  // tiles q > p + 1 of panel p (Z^T = R^T + S M', W^T = Z^T T, V^T = W^T M'^T) while the
+  // chain does the lookahead tile p + 1 and the next panel, so the data warps only apply
+  const bool use_red = C::NSPARE > 0 && (flags & 32);
+  const int NB = NALL + (use_red ? C::NSPARE * 32 : 0);  // BAR_ALL: chain + data (+ reducers)
   int tr_k = 0;
   (void)tr_k;
 
@@ -147,6 +155,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     mbar_init_n(bar_ready, 1);
     mbar_init_n(bar_free, C::DW);
     mbar_init_n(bar_v, 1);
+    mbar_init_n(bar_v2, C::NSPARE > 0 ? C::NSPARE : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -179,6 +188,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       ++k;
     }
   }
+  int red_i = -1;  // reducer index (spare warps when use_red)
   if (warp != chain_w && li < 0 && d < 0) {
     // spare warp: the tile pass of the other side's scan, if the host attached one
     int si = 0, zc = 0, dk = 0;
@@ -192,8 +202,11 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       }
       si += busy ? 0 : 1;
     }
-    src.side_scan(si, C::NSPARE, lane);
-    return;
+    if (!use_red) {
+      src.side_scan(si, C::NSPARE, lane);
+      return;
+    }
+    red_i = si;
   }
 
   auto chunk_end = [&](int64_t r0) -> int64_t {
@@ -222,6 +235,46 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     out[0] = v[0].x;
     out[1] = v[0].y;
   };
+
+  if (red_i >= 0) {
+    const int si = red_i;
+    // ================= reducer warp si: tiles q = p + 2 + si, p + 2 + si + NSPARE, ...
+    for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0)) {
+      named_bar(BAR_ALL, NB);  // direct Gram partials of tile 0
+#pragma unroll 1
+      for (int p = 0; p < C::NLT; ++p) {
+        const int par = p & 1, j0 = 8 * p;
+        named_bar(BAR_ALL, NB);  // B_p
+        if (flag[par] == 0) named_bar(BAR_ALL, NB);  // F_p: explicit T / M' of the panel
+        if (p + 1 < C::NLT) {
+          const double* Tc = smem_dyn + C::OFF_T + par * 8 * C::LDT;
+          const double* Mc = smem_dyn + C::OFF_M + par * 8 * C::LDT;
+          for (int q = p + 2 + si; q < C::NLT; q += C::NSPARE) {
+            const int l0 = 8 * q;
+            const int r0i = rix<C>(j0 + 2 * t, l0 + g), r1i = rix<C>(j0 + 2 * t + 1, l0 + g);
+            double st[2];
+            sum_partials(Zp + q * 64, C::NLT * 64, st);
+            double zt[2] = {R[r0i], R[r1i]};
+            dmma(zt, st[0], Mc[(2 * t) * C::LDT + g]);
+            dmma(zt, st[1], Mc[(2 * t + 1) * C::LDT + g]);
+            double wv[2] = {0.0, 0.0};
+            dmma(wv, zt[0], Tc[(2 * t) * C::LDT + g]);
+            dmma(wv, zt[1], Tc[(2 * t + 1) * C::LDT + g]);
+            R[r0i] -= wv[0];
+            R[r1i] -= wv[1];
+            double vt[2] = {0.0, 0.0};
+            dmma(vt, wv[0], Mc[g * C::LDT + 2 * t]);
+            dmma(vt, wv[1], Mc[g * C::LDT + 2 * t + 1]);
+            *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-vt[0], -vt[1]);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_v2);  // tiles q > p + 1 may be updated
+        }
+      }
+    }
+    named_bar(BAR_ALL, NB);  // R final
+    return;
+  }
 
   if (li >= 0) {
     // ================= loader warp(s): li == 0 fetches; all transform a row segment
@@ -274,7 +327,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
   if (warp == chain_w) {
     // ================= chain warp: the whole critical path
     for (int64_t r0 = row_begin; r0 < row_end; r0 = chunk_end(r0)) {
-      named_bar(BAR_ALL, NALL);  // direct Gram partials of tile 0
+      named_bar(BAR_ALL, NB);  // direct Gram partials of tile 0
       double G[2];
       sum_partials(Gd, 64, G);
       double Pg = diag_of(G, lane);
@@ -286,16 +339,20 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
         const double G0[2] = {G[0], G[1]};  // X^T X of panel p (before the chain)
         TR(0, 1);
         double Rb[2];
-        const bool ok = factor_panel_gram<C>(G, Rb, R, j0, Tc, Mc, lane, Pg) && !(flags & 2);
+        // Cholesky panel; where its guard rejects (pivot cancellation) the reflector chain,
+        // whose guard is looser (it never forms R_p^T R_p); then the explicit path
+        bool ok = !(flags & 16) && factor_panel_chol<C>(G, Rb, R, j0, Tc, Mc, smem_dyn + C::OFF_U, lane, Pg);
+        if (!ok) ok = factor_panel_gram<C>(G, Rb, R, j0, Tc, Mc, lane, Pg);
+        ok = ok && !(flags & 2);
         if (ok) {
           if (2 * t >= g) R[rix<C>(j0 + g, j0 + 2 * t)] = Rb[0];
           if (2 * t + 1 >= g) R[rix<C>(j0 + g, j0 + 2 * t + 1)] = Rb[1];
         }
         if (lane == 0) flag[par] = ok ? 1 : 0;
         TR(0, 2);
-        named_bar(BAR_ALL, NALL);  // B_p: chain results out, data partials in
+        named_bar(BAR_ALL, NB);  // B_p: chain results out, data partials in
         TR(0, 3);
-        if (!ok) named_bar(BAR_ALL, NALL);  // F_p: explicit panel done by the data warps
+        if (!ok) named_bar(BAR_ALL, NB);  // F_p: explicit panel done by the data warps
         if (p + 1 < C::NLT) {
           const int q = p + 1, l0 = 8 * q;
           double cc[2] = {0.0, 0.0};
@@ -337,14 +394,14 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
             Pg = dcc + de3;
             TR(0, 5);
           } else {
-            named_bar(BAR_ALL, NALL);  // D_q: direct Gram partials of the updated tile
+            named_bar(BAR_GD, NALL);  // D_q: direct Gram partials of the updated tile
             sum_partials(Gd, 64, G);
             Pg = diag_of(G, lane);
           }
         }
       }
     }
-    named_bar(BAR_ALL, NALL);  // R final
+    named_bar(BAR_ALL, NB);  // R final
   } else {
     // ================= data warps
     double* Ytw = smem_dyn + C::OFF_YT + d * C::SZ_YT;
@@ -353,7 +410,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     double* scs = smem_dyn + C::OFF_SC;
     double* P = smem_dyn + C::OFF_P;
     double c[C::NLT][C::KWT][2];
-    uint32_t ph_ready = 0, ph_v = 0;
+    uint32_t ph_ready = 0, ph_v = 0, ph_v2 = 0;
 
     // (single DMMA accumulation chains: a final DADD would queue behind the other warps'
     // DMMAs in this SM sub-partition's FP64 datapath)
@@ -392,7 +449,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_free);
       gram_partial(0, Gd);
-      named_bar(BAR_ALL, NALL);
+      named_bar(BAR_ALL, NB);
 
 #pragma unroll 1
       for (int p = 0; p < C::NLT; ++p) {
@@ -400,29 +457,31 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
         const double* Tp = smem_dyn + C::OFF_T + (par ^ 1) * 8 * C::LDT;
         const double* Mp = smem_dyn + C::OFF_M + (par ^ 1) * 8 * C::LDT;
         if (p > 0) {
-          // (3a) reduces of the tiles q > p with panel p-1 first: their inputs (partials,
-          // T, M') are ready since B_{p-1}, so they overlap the chain warp's update of tile p
-          for (int q = p + 1 + ((d - (p + 1)) % C::DW + C::DW) % C::DW; q < C::NLT; q += C::DW) {
-            const int l0 = 8 * q;
-            const int r0i = rix<C>(j0 - 8 + 2 * t, l0 + g), r1i = rix<C>(j0 - 8 + 2 * t + 1, l0 + g);
-            double st[2];
-            sum_partials(Zp + q * 64, C::NLT * 64, st);
-            double zt[2] = {R[r0i], R[r1i]};
-            dmma(zt, st[0], Mp[(2 * t) * C::LDT + g]);
-            dmma(zt, st[1], Mp[(2 * t + 1) * C::LDT + g]);
-            double wv[2] = {0.0, 0.0};
-            dmma(wv, zt[0], Tp[(2 * t) * C::LDT + g]);
-            dmma(wv, zt[1], Tp[(2 * t + 1) * C::LDT + g]);
-            R[r0i] -= wv[0];
-            R[r1i] -= wv[1];
-            double vt[2] = {0.0, 0.0};
-            dmma(vt, wv[0], Mp[g * C::LDT + 2 * t]);
-            dmma(vt, wv[1], Mp[g * C::LDT + 2 * t + 1]);
-            *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-vt[0], -vt[1]);
+          if (!use_red) {
+            // (3a) reduces of the tiles q > p with panel p-1 first: their inputs (partials,
+            // T, M') are ready since B_{p-1}, so they overlap the chain warp's update of tile p
+            for (int q = p + 1 + ((d - (p + 1)) % C::DW + C::DW) % C::DW; q < C::NLT; q += C::DW) {
+              const int l0 = 8 * q;
+              const int r0i = rix<C>(j0 - 8 + 2 * t, l0 + g), r1i = rix<C>(j0 - 8 + 2 * t + 1, l0 + g);
+              double st[2];
+              sum_partials(Zp + q * 64, C::NLT * 64, st);
+              double zt[2] = {R[r0i], R[r1i]};
+              dmma(zt, st[0], Mp[(2 * t) * C::LDT + g]);
+              dmma(zt, st[1], Mp[(2 * t + 1) * C::LDT + g]);
+              double wv[2] = {0.0, 0.0};
+              dmma(wv, zt[0], Tp[(2 * t) * C::LDT + g]);
+              dmma(wv, zt[1], Tp[(2 * t + 1) * C::LDT + g]);
+              R[r0i] -= wv[0];
+              R[r1i] -= wv[1];
+              double vt[2] = {0.0, 0.0};
+              dmma(vt, wv[0], Mp[g * C::LDT + 2 * t]);
+              dmma(vt, wv[1], Mp[g * C::LDT + 2 * t + 1]);
+              *reinterpret_cast<double2*>(Ws + q * 64 + 2 * lane) = make_double2(-vt[0], -vt[1]);
+            }
+            if (d == 0) TR(1, 2);
+            named_bar(BAR_DATA, C::DW * 32);
+            if (d == 0) TR(1, 3);
           }
-          if (d == 0) TR(1, 2);
-          named_bar(BAR_DATA, C::DW * 32);
-          if (d == 0) TR(1, 3);
           // B operands of the panel p-1 update (X^T or Y^T rows of this warp), loaded once
           // for every tile: keeps the data warps' shared-memory traffic low
           double yb[C::KWT][2];
@@ -431,36 +490,68 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
             yb[it][0] = Ytw[(2 * t) * C::LDYT + 8 * it + g];
             yb[it][1] = Ytw[(2 * t + 1) * C::LDYT + 8 * it + g];
           }
-          // (3b) applies of the tiles q > p (independent of the chain's V of tile p)
+          if (use_red) {
+            // (1) tile p with panel p-1 (V from the chain), then (3b) the tiles q > p (V from
+            // the reducer warps)
+            mbar_wait(bar_v, ph_v);
+            ph_v ^= 1;
+            if (d == 0) TR(1, 1);
 #pragma unroll
-          for (int q = 0; q < C::NLT; ++q) {
-            if (q > p) {
-              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+            for (int q = 0; q < C::NLT; ++q) {
+              if (q == p) {
+                const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
 #pragma unroll
-              for (int it = 0; it < C::KWT; ++it) {
-                dmma(c[q][it], nw.x, yb[it][0]);
-                dmma(c[q][it], nw.y, yb[it][1]);
+                for (int it = 0; it < C::KWT; ++it) {
+                  dmma(c[q][it], nw.x, yb[it][0]);
+                  dmma(c[q][it], nw.y, yb[it][1]);
+                }
               }
             }
-          }
-          // (1) tile p with panel p-1, V from the chain
-          mbar_wait(bar_v, ph_v);
-          ph_v ^= 1;
-          if (d == 0) TR(1, 1);
+            mbar_wait(bar_v2, ph_v2);
+            ph_v2 ^= 1;
 #pragma unroll
-          for (int q = 0; q < C::NLT; ++q) {
-            if (q == p) {
-              const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+            for (int q = 0; q < C::NLT; ++q) {
+              if (q > p) {
+                const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
 #pragma unroll
-              for (int it = 0; it < C::KWT; ++it) {
-                dmma(c[q][it], nw.x, yb[it][0]);
-                dmma(c[q][it], nw.y, yb[it][1]);
+                for (int it = 0; it < C::KWT; ++it) {
+                  dmma(c[q][it], nw.x, yb[it][0]);
+                  dmma(c[q][it], nw.y, yb[it][1]);
+                }
+              }
+            }
+          } else {
+            // (3b) applies of the tiles q > p (independent of the chain's V of tile p)
+#pragma unroll
+            for (int q = 0; q < C::NLT; ++q) {
+              if (q > p) {
+                const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+#pragma unroll
+                for (int it = 0; it < C::KWT; ++it) {
+                  dmma(c[q][it], nw.x, yb[it][0]);
+                  dmma(c[q][it], nw.y, yb[it][1]);
+                }
+              }
+            }
+            // (1) tile p with panel p-1, V from the chain
+            mbar_wait(bar_v, ph_v);
+            ph_v ^= 1;
+            if (d == 0) TR(1, 1);
+#pragma unroll
+            for (int q = 0; q < C::NLT; ++q) {
+              if (q == p) {
+                const double2 nw = *reinterpret_cast<const double2*>(Ws + q * 64 + 2 * lane);
+#pragma unroll
+                for (int it = 0; it < C::KWT; ++it) {
+                  dmma(c[q][it], nw.x, yb[it][0]);
+                  dmma(c[q][it], nw.y, yb[it][1]);
+                }
               }
             }
           }
           if (flag[par ^ 1] == 0) {  // panel p-1 was explicit: the chain needs the direct Gram
             gram_partial(p, Gd);
-            named_bar(BAR_ALL, NALL);  // D_p
+            named_bar(BAR_GD, NALL);  // D_p
           }
         }
         double cp[C::KWT][2];
@@ -489,7 +580,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
         }
         if (p + 1 < C::NLT) gram_partial(p + 1, Gp);
         if (d == 0) TR(1, 5);
-        named_bar(BAR_ALL, NALL);  // B_p
+        named_bar(BAR_ALL, NB);  // B_p
         if (d == 0) TR(1, 6);
         if (flag[par] == 0) {
           double* Tc = smem_dyn + C::OFF_T + par * 8 * C::LDT;
@@ -515,11 +606,11 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
             }
           }
           named_bar(BAR_DATA, C::DW * 32);
-          named_bar(BAR_ALL, NALL);  // F_p
+          named_bar(BAR_ALL, NB);  // F_p
         }
       }
     }
-    named_bar(BAR_ALL, NALL);  // R final
+    named_bar(BAR_ALL, NB);  // R final
   }
 
   double* out = r_out + cta * C::NP * C::NP;

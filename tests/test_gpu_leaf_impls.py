@@ -15,12 +15,25 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"JQ_TSQR_IMPL": "cta"}, {"JQ_TSQR_EXPLICIT": "1"},
                                  {"JQ_TSQR_IMPL": "cta", "JQ_TSQR_EXPLICIT": "1"},
-                                 {"JQ_TSQR_DEBUG": "8"}],
-                         ids=["cta", "ws-explicit", "cta-explicit", "ws-fixed-roles"])
+                                 {"JQ_TSQR_DEBUG": "8"}, {"JQ_TSQR_CHAIN": "householder"},
+                                 {"JQ_TSQR_CHAIN": "householder", "JQ_TSQR_IMPL": "cta"},
+                                 {"JQ_TSQR_REDUCERS": "1"}],
+                         ids=["cta", "ws-explicit", "cta-explicit", "ws-fixed-roles", "ws-reflector-chain",
+                              "cta-reflector-chain", "ws-reducer-warps"])
 def test_leaf_impl_parity(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "figaro or householder or shard"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_svd_v_overlap_parity():
+    # JQ_SVD_V_OVERLAP=1: the V replay concurrently with the sweeps (opt-in)
+    e = dict(os.environ, JQ_SVD_V_OVERLAP="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "svd"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 

@@ -224,3 +224,14 @@ def test_c_gram_oracle_with_permuted_rows():
     g = cgram.join_gram(78, 3000, 3, 80, 2000, 4, t_a.keys, t_b.keys, pa, pb)
     g_ref = O.factorised_gram(t_a, t_b)
     assert np.abs(g - g_ref).max() <= 1e-12 * np.abs(g_ref).max()
+
+
+def test_c_gram_oracle_cartesian_matches_numpy():
+    from oracle import cgram
+    if not cgram.available():
+        pytest.skip("oracle/c not built")
+    g = cgram.join_gram(4001, 20000, 5, 4002, 15000, 6)
+    a = O.Table(O.datagen.uniform_matrix(4001, 20000, 5))
+    b = O.Table(O.datagen.uniform_matrix(4002, 15000, 6))
+    g_ref = O.factorised_gram(a, b)
+    assert np.abs(g - g_ref).max() <= 1e-12 * np.abs(g_ref).max()
