@@ -142,6 +142,19 @@ JQ_API int jq_gen_zipf_sorted_keys(jq_ctx* ctx, uint64_t seed, int64_t rows, con
 JQ_API int jq_gen_zipf_keys(jq_ctx* ctx, uint64_t seed, int64_t rows, const double* cdf, int64_t universe,
                             int64_t* keys_out);
 
+/* ---- data-io: CSV ingest -------------------------------- */
+/* Row and cell counts of a CSV table (comma separated, optional single header
+ * line, blank lines skipped); host only, multithreaded over the mmapped file. */
+JQ_API int jq_csv_scan(const char* path, int has_header, int64_t* rows, int64_t* cols);
+/* Parse the table into data (rows x (cols - [key_col >= 0]) f64, row-major) and
+ * keys (rows int64, key_col >= 0) -- host or device buffers.  Device outputs are
+ * streamed through pinned staging slots with the H2D copies on the context stream
+ * overlapping the parse.  Errors (JQ_E_INVALID) name the file line: ragged row,
+ * unparsable cell, non-finite value, unsorted keys.  Replaces read_table's parser
+ * (SPEC.md:458). */
+JQ_API int jq_csv_parse(jq_ctx* ctx, const char* path, int has_header, int key_col, int64_t rows, int64_t cols,
+                        double* data, int64_t* keys);
+
 /* ---- key sort for unsorted tables (opt-in; SPEC.md:204-206 raises by default) ---- */
 /* Stable LSD radix sort of m int64 keys: perm_out[i] = the original row of sorted
  * position i, equal to np.argsort(keys, kind="stable") bit for bit; keys_out

@@ -47,6 +47,8 @@ SIGNATURES = {
     "jq_gen_zipf_sorted_keys": [_P, C.c_uint64, _I64, _P, _I64, _P],
     "jq_gen_zipf_keys": [_P, C.c_uint64, _I64, _P, _I64, _P],
     "jq_sort_keys": [_P, _P, _I64, _P, _P],
+    "jq_csv_scan": [C.c_char_p, C.c_int, _P, _P],
+    "jq_csv_parse": [_P, C.c_char_p, C.c_int, C.c_int, _I64, _I64, _P, _P],
     "jq_gather_rows": [_P, _P, _I64, _I64, _P, _P],
     "jq_colsums": [_P, _P, _I64, _I64, _P],
     "jq_figaro_r_shard": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _P, C.c_int, _P],

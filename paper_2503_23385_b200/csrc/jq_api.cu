@@ -76,6 +76,13 @@ int sync_and_check_flags(jq_ctx* ctx) {
   return JQ_OK;
 }
 
+void stage_event(jq_ctx* ctx, int k) {
+  static const char* names[8] = {"jq: grouping", "jq: head/tail scan", "jq: scan done", "jq: TSQR leaves",
+                                 "jq: TSQR tree", "jq: R done / SVD", "jq: SVD done", "jq: stage 7"};
+  cudaEventRecord(ctx->ev[k], ctx->stream);
+  nvtxMarkA(names[k & 7]);
+}
+
 static float ev_ms(jq_ctx* ctx, int a, int b) {
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]) != cudaSuccess) {
@@ -273,7 +280,7 @@ static int figaro_r_footnote_blocks(jq_ctx* ctx, const double* a, int64_t m1, in
                                     int64_t m2, int64_t n2, double* r_out) {
   const int64_t n = n1 + n2;
   const int64_t pmax = int64_t(ctx->sms) * BLOCK_LEAVES_MAX_PER_SM;
-  cudaEventRecord(ctx->ev[2], ctx->stream);  // no scan stage
+  stage_event(ctx, 2);  // no scan stage
   double* ra = ws_alloc<double>(ctx, n1 * n1);
   double* rb = ws_alloc<double>(ctx, n2 * n2);
   double* rh = ws_alloc<double>(ctx, n * n);
@@ -285,7 +292,7 @@ static int figaro_r_footnote_blocks(jq_ctx* ctx, const double* a, int64_t m1, in
   ctx->record_tsqr_events = false;
   ctx->timing.tsqr_ctas = 0;
   ctx->timing.reduced_rows = 0;
-  cudaEventRecord(ctx->ev[3], ctx->stream);
+  stage_event(ctx, 3);
   FigaroArgs fa{};
   fa.b = a; fa.m2 = m1; fa.n2 = n1;
   fa.m1_global = m2; fa.m2_global = m1;
@@ -318,10 +325,10 @@ static int figaro_r_footnote_blocks(jq_ctx* ctx, const double* a, int64_t m1, in
   JQ_CHECK_LAUNCH(ctx);
   rc = tsqr_finish_pair(ctx, la, lb, ra, rb);
   if (rc) { ctx->record_tsqr_events = true; return rc; }
-  cudaEventRecord(ctx->ev[4], ctx->stream);
+  stage_event(ctx, 4);
   rc = footnote_small_head(ctx, ra, n1, rb, n2, head, 1, true, rh, r_out);
   ctx->record_tsqr_events = true;
-  cudaEventRecord(ctx->ev[5], ctx->stream);
+  stage_event(ctx, 5);
   return rc;
 }
 
@@ -329,7 +336,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
                                  const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
   const bool keyed = ka != nullptr;
   const int64_t n = n1 + n2;
-  cudaEventRecord(ctx->ev[0], ctx->stream);
+  stage_event(ctx, 0);
   Groups gr;
   int64_t ng = 1;
   if (keyed) {
@@ -339,7 +346,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     JQ_CUDA(cudaStreamSynchronize(ctx->stream));
     ng = hn[0];
   }
-  cudaEventRecord(ctx->ev[1], ctx->stream);
+  stage_event(ctx, 1);
   const int64_t cap = keyed ? gr.cap : 1;
   if (!keyed && n1 > 0 && n2 > 0 && carry_free_leaves()) return figaro_r_footnote_blocks(ctx, a, m1, n1, b, m2, n2, r_out);
   // A's scan in full; the tile pass of B's scan (the HBM-heavy part) runs on the spare
@@ -350,7 +357,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     JQ_TRY(segscan_dev(ctx, a, m1, n1, keyed ? gr.gid_a : nullptr, keyed ? gr.a_start : nullptr,
                        keyed ? gr.a_count : nullptr, keyed ? gr.d_n : nullptr, cap, &sa));
   if (n2 > 0) JQ_TRY(segscan_begin(ctx, b, m2, n2, keyed ? gr.gid_b : nullptr, cap, &sb, &side_b));
-  cudaEventRecord(ctx->ev[2], ctx->stream);
+  stage_event(ctx, 2);
   double* ra = ws_alloc<double>(ctx, std::max<int64_t>(n1 * n1, 1));
   double* rb = ws_alloc<double>(ctx, std::max<int64_t>(n2 * n2, 1));
   double* rh = ws_alloc<double>(ctx, n * n);
@@ -360,7 +367,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   ctx->record_tsqr_events = false;
   ctx->timing.tsqr_ctas = 0;
   ctx->timing.reduced_rows = 0;
-  cudaEventRecord(ctx->ev[3], ctx->stream);
+  stage_event(ctx, 3);
   // tails of A scaled by sqrt(m2g): the "B-part" of a source with an empty A-part
   FigaroArgs fa{};
   LeafSet leaves_a{};
@@ -398,7 +405,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     }
     if (rc) { ctx->record_tsqr_events = true; return rc; }
   }
-  cudaEventRecord(ctx->ev[4], ctx->stream);
+  stage_event(ctx, 4);
   if (ng <= FOOTNOTE_GIVENS_MAX_HEADS) {
     if (ng > 0) {
       head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng * n, 256), 4096), 256, 0, ctx->stream>>>(
@@ -408,7 +415,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     }
     const int rc = footnote_small_head(ctx, ra, n1, rb, n2, heads, ng, true, rh, r_out);
     ctx->record_tsqr_events = true;
-    cudaEventRecord(ctx->ev[5], ctx->stream);
+    stage_event(ctx, 5);
     return rc;
   }
   // head rows (G x n) -> R_H, then [blockdiag(R_A, R_B); R_H] -> canonical R
@@ -441,7 +448,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   JQ_CHECK_LAUNCH(ctx);
   int rc = tsqr_stack_dev(ctx, stack, 2, n, r_out, true);
   ctx->record_tsqr_events = true;
-  cudaEventRecord(ctx->ev[5], ctx->stream);
+  stage_event(ctx, 5);
   return rc;
 }
 
@@ -529,7 +536,7 @@ static int footnote_shard_blocks(jq_ctx* ctx, const double* a, int64_t a_rows, i
                                  double* sums_out = nullptr) {
   const int64_t n = n1 + n2;
   const int64_t pmax = int64_t(ctx->sms) * BLOCK_LEAVES_MAX_PER_SM;
-  cudaEventRecord(ctx->ev[2], ctx->stream);  // no scan stage
+  stage_event(ctx, 2);  // no scan stage
   double* ra = ws_alloc<double>(ctx, n1 * n1);
   double* rb = ws_alloc<double>(ctx, n2 * n2);
   double* rh = ws_alloc<double>(ctx, n * n);
@@ -539,7 +546,7 @@ static int footnote_shard_blocks(jq_ctx* ctx, const double* a, int64_t a_rows, i
   if (!ra || !rb || !rh || !sums_a || !sums_b || !rows)
     return fail(JQ_E_OOM, "workspace exhausted (footnote shard, carry-free leaves)");
   ctx->record_tsqr_events = false;
-  cudaEventRecord(ctx->ev[3], ctx->stream);
+  stage_event(ctx, 3);
   FigaroArgs fa{};
   fa.b = a; fa.m2 = a_rows; fa.n2 = n1;
   fa.m1_global = m2; fa.m2_global = m1;
@@ -579,7 +586,7 @@ static int footnote_shard_blocks(jq_ctx* ctx, const double* a, int64_t a_rows, i
   for (int k = 0; k < 2; ++k) ls[k]->count = block_stack_layout(ls[k]->count, ls[k]->np, &sd[k].first_d);
   rc = tsqr_finish_pair(ctx, la, lb, ra, rb);
   if (rc) { ctx->record_tsqr_events = true; return rc; }
-  cudaEventRecord(ctx->ev[4], ctx->stream);
+  stage_event(ctx, 4);
   if (include_head) {
     head_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(a_total, (int)n1, b_total, (int)n2, nullptr,
                                                                         nullptr, 1, m1, m2, rows);
@@ -587,7 +594,7 @@ static int footnote_shard_blocks(jq_ctx* ctx, const double* a, int64_t a_rows, i
   }
   rc = footnote_small_head(ctx, ra, n1, rb, n2, rows, include_head ? 3 : 2, false, rh, r_out);
   ctx->record_tsqr_events = true;
-  cudaEventRecord(ctx->ev[5], ctx->stream);
+  stage_event(ctx, 5);
   return rc;
 }
 
@@ -606,14 +613,14 @@ static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int6
   SideScan side_b;  // B's tile pass on the spare warps of A's leaf (as in figaro_r_footnote_dev)
   if (n1 > 0) JQ_TRY(segscan_dev(ctx, a, a_rows, n1, nullptr, nullptr, nullptr, nullptr, 1, &sa));
   if (n2 > 0) JQ_TRY(segscan_begin(ctx, b, b_rows, n2, nullptr, 1, &sb, &side_b));
-  cudaEventRecord(ctx->ev[2], ctx->stream);
+  stage_event(ctx, 2);
   double* ra = ws_alloc<double>(ctx, std::max<int64_t>(n1 * n1, 1));
   double* rb = ws_alloc<double>(ctx, std::max<int64_t>(n2 * n2, 1));
   double* rh = ws_alloc<double>(ctx, n * n);
   double* heads = ws_alloc<double>(ctx, n);
   if (!ra || !rb || !rh || !heads) return fail(JQ_E_OOM, "workspace exhausted (footnote shard)");
   ctx->record_tsqr_events = false;
-  cudaEventRecord(ctx->ev[3], ctx->stream);
+  stage_event(ctx, 3);
   int rc = JQ_OK;
   if (n1 > 0) {
     FigaroArgs fa{};
@@ -635,7 +642,7 @@ static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int6
   }
   ctx->record_tsqr_events = true;
   if (rc) return rc;
-  cudaEventRecord(ctx->ev[4], ctx->stream);
+  stage_event(ctx, 4);
   // one head row at most: blockdiag(R_A, R_B) plus a Givens absorb of the head row
   if (include_head) {
     head_rows_kernel<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(a_total, (int)n1, b_total, (int)n2, nullptr,
@@ -643,7 +650,7 @@ static int footnote_shard_dev(jq_ctx* ctx, const double* a, int64_t a_rows, int6
     JQ_CHECK_LAUNCH(ctx);
   }
   rc = footnote_small_head(ctx, ra, n1, rb, n2, heads, include_head ? 1 : 0, false, rh, r_out);
-  cudaEventRecord(ctx->ev[5], ctx->stream);
+  stage_event(ctx, 5);
   return rc;
 }
 
@@ -661,16 +668,16 @@ static int figaro_r_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, co
   const bool keyed = ka != nullptr;
   ctx->timing.tsqr_ctas = 0;
   ctx->timing.reduced_rows = 0;
-  cudaEventRecord(ctx->ev[0], ctx->stream);
+  stage_event(ctx, 0);
   Groups gr;
   if (keyed) JQ_TRY(group_keys_dev(ctx, ka, m1, kb, m2, &gr));
-  cudaEventRecord(ctx->ev[1], ctx->stream);
+  stage_event(ctx, 1);
   SegScan ss;
   const int64_t cap = keyed ? gr.cap : 1;
   if (n2 > 0)
     JQ_TRY(segscan_dev(ctx, b, m2, n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
                        keyed ? gr.b_count : nullptr, keyed ? gr.d_n : nullptr, cap, &ss));
-  cudaEventRecord(ctx->ev[2], ctx->stream);
+  stage_event(ctx, 2);
   FigaroArgs fa{};
   fa.a = a; fa.m1 = m1; fa.n1 = n1;
   fa.b = b; fa.m2 = m2; fa.n2 = n2;
@@ -755,7 +762,7 @@ static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n
   ctx->timing.tsqr_ctas = 0;
   ctx->timing.reduced_rows = 0;
   ctx->record_tsqr_events = false;
-  cudaEventRecord(ctx->ev[0], ctx->stream);
+  stage_event(ctx, 0);
   int64_t k = 0;  // global piece counter (buffer parity)
   bool first[2] = {true, true};
   // side 0 = A, side 1 = B.  Dense: B first (top rows need head(B)), footnote: any order.
@@ -811,7 +818,7 @@ static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n
     }
   }
   ctx->ws.used = mark;
-  cudaEventRecord(ctx->ev[4], ctx->stream);
+  stage_event(ctx, 4);
   int rc = JQ_OK;
   if (!foot) {
     canonicalize_dev(ctx, racc[0], n, dr);
@@ -822,10 +829,10 @@ static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n
     rc = footnote_small_head(ctx, racc[0], n1, racc[1], n2, heads, 1, true, rh, dr);
   }
   ctx->record_tsqr_events = true;
-  cudaEventRecord(ctx->ev[5], ctx->stream);
-  cudaEventRecord(ctx->ev[1], ctx->stream);
-  cudaEventRecord(ctx->ev[2], ctx->stream);
-  cudaEventRecord(ctx->ev[3], ctx->stream);
+  stage_event(ctx, 5);
+  stage_event(ctx, 1);
+  stage_event(ctx, 2);
+  stage_event(ctx, 3);
   return rc;
 }
 
@@ -940,6 +947,7 @@ int64_t jq_kernel_launches(jq_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int jq_canonicalize(jq_ctx* ctx, const double* r, int64_t n, double* out) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_canonicalize");
   if (n <= 0) return JQ_OK;
   JQ_TRY(begin_call(ctx));
   JQ_TRY(ws_reserve(ctx, stage_bytes(r, n * n) + stage_bytes((const double*)out, n * n)));
@@ -954,6 +962,7 @@ int jq_canonicalize(jq_ctx* ctx, const double* r, int64_t n, double* out) {
 
 int jq_householder_r(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, double* r) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_householder_r");
   if (cols <= 0) return fail(JQ_E_INVALID, "householder_r needs at least one column");
   if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
   if (rows < 0) return fail(JQ_E_INVALID, "negative row count");
@@ -972,6 +981,7 @@ int jq_householder_r(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, d
 int jq_figaro_r(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
                 const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_figaro_r");
   JQ_TRY(check_tables(m1, n1, ka, m2, n2, kb));
   JQ_TRY(begin_call(ctx));
   const int64_t n = n1 + n2;
@@ -1011,6 +1021,7 @@ int jq_figaro_svd(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const in
                   const double* b, int64_t m2, int64_t n2, const int64_t* kb, int want_v,
                   double* values, double* v, double* r) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_figaro_svd");
   JQ_TRY(check_tables(m1, n1, ka, m2, n2, kb));
   JQ_TRY(begin_call(ctx));
   const int64_t n = n1 + n2;
@@ -1030,7 +1041,7 @@ int jq_figaro_svd(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const in
   double* dr = ws_alloc<double>(ctx, n * n);
   JQ_TRY(figaro_r_dev(ctx, da, m1, n1, dka, db, m2, n2, dkb, dr));
   JQ_TRY(svd_dev(ctx, dr, n, want_v, dval, dv));
-  cudaEventRecord(ctx->ev[6], ctx->stream);
+  stage_event(ctx, 6);
   JQ_TRY(copy_out(ctx, values, (const double*)dval, n));
   if (want_v) JQ_TRY(copy_out(ctx, v, (const double*)dv, n * n));
   if (r) JQ_TRY(copy_out(ctx, r, (const double*)dr, n * n));
@@ -1044,6 +1055,7 @@ int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, 
                       int64_t m2, int64_t b_row0, const double* b_prefix, const double* b_total, int include_head,
                       double* r_local) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_figaro_r_shard");
   if (a_rows < 0 || b_rows < 0 || n1 < 0 || n2 < 0 || n1 + n2 == 0 || n1 + n2 > 256)
     return fail(JQ_E_INVALID, "bad shard geometry");
   if (m1 <= 0 || m2 <= 0 || b_row0 < 0 || b_row0 + b_rows > m2 || a_row0 < 0 || a_row0 + a_rows > m1)
@@ -1067,13 +1079,13 @@ int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, 
   JQ_TRY(stage_out(ctx, r_local, n * n, &dr));
   ctx->timing.tsqr_ctas = 0;
   ctx->timing.reduced_rows = 0;
-  cudaEventRecord(ctx->ev[0], ctx->stream);
-  cudaEventRecord(ctx->ev[1], ctx->stream);
+  stage_event(ctx, 0);
+  stage_event(ctx, 1);
   int rc = JQ_OK;
   if (!foot) {
     SegScan ss{};
     if (n2 > 0) JQ_TRY(segscan_dev(ctx, db, b_rows, n2, nullptr, nullptr, nullptr, nullptr, 1, &ss));
-    cudaEventRecord(ctx->ev[2], ctx->stream);
+    stage_event(ctx, 2);
     FigaroArgs fa{};
     fa.a = da; fa.m1 = a_rows; fa.n1 = n1;
     fa.b = db; fa.m2 = b_rows; fa.n2 = n2;
@@ -1095,6 +1107,7 @@ int jq_figaro_r_shard(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, 
 int jq_figaro_r_shard_local(jq_ctx* ctx, const double* a, int64_t a_rows, int64_t n1, int64_t m1, const double* b,
                             int64_t b_rows, int64_t n2, int64_t m2, double* r_local, double* sums) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_figaro_r_shard_local");
   if (a_rows <= 0 || b_rows <= 0 || n1 <= 0 || n2 <= 0 || n1 + n2 > 256)
     return fail(JQ_E_INVALID, "bad shard geometry (both sides need rows and columns)");
   if (m1 < a_rows || m2 < b_rows) return fail(JQ_E_INVALID, "bad global sizes for the shard");
@@ -1112,8 +1125,8 @@ int jq_figaro_r_shard_local(jq_ctx* ctx, const double* a, int64_t a_rows, int64_
   JQ_TRY(stage_out(ctx, sums, n, &ds));
   ctx->timing.tsqr_ctas = 0;
   ctx->timing.reduced_rows = 0;
-  cudaEventRecord(ctx->ev[0], ctx->stream);
-  cudaEventRecord(ctx->ev[1], ctx->stream);
+  stage_event(ctx, 0);
+  stage_event(ctx, 1);
   JQ_TRY(footnote_shard_blocks(ctx, da, a_rows, n1, m1, 0, nullptr, nullptr, db, b_rows, n2, m2, 0, nullptr, nullptr,
                                false, dr, ds));
   JQ_TRY(copy_out(ctx, r_local, (const double*)dr, n * n));
@@ -1127,6 +1140,7 @@ int jq_split_group_rows(jq_ctx* ctx, const double* part_sums, const int64_t* par
                         const int64_t* part_group, int64_t nparts, int64_t n1, int64_t n2, double* rows,
                         int64_t rows_capacity, int64_t* n_rows) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_split_group_rows");
   if (nparts < 0 || n1 < 0 || n2 < 0 || n1 + n2 == 0 || n1 + n2 > 1024) return fail(JQ_E_INVALID, "bad geometry");
   if (nparts > 0 && (!part_sums || !part_rows || !part_group)) return fail(JQ_E_INVALID, "null argument");
   const int64_t n = n1 + n2;
@@ -1179,6 +1193,7 @@ int jq_split_group_rows(jq_ctx* ctx, const double* part_sums, const int64_t* par
 
 int jq_tsqr_stack(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, double* r) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_tsqr_stack");
   if (count <= 0 || n <= 0 || n > 256) return fail(JQ_E_INVALID, "bad R stack geometry");
   JQ_TRY(begin_call(ctx));
   JQ_TRY(ws_reserve(ctx, stage_bytes(rs, count * n * n) + stage_bytes((const double*)r, n * n) +

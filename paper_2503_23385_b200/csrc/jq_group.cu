@@ -332,6 +332,7 @@ extern "C" int jq_group_keys(jq_ctx* ctx, const int64_t* ka, int64_t m1, const i
                              int64_t capacity, int64_t* n_groups, int64_t* keys, int64_t* a_start,
                              int64_t* a_count, int64_t* b_start, int64_t* b_count, int64_t* red_off) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_group_keys");
   if (!ka && m1 > 0) return fail(JQ_E_KEYS, "left table has no keys");
   if (!kb && m2 > 0) return fail(JQ_E_KEYS, "right table has no keys");
   JQ_TRY(begin_call(ctx));

@@ -390,6 +390,7 @@ using namespace jq;
 
 extern "C" int jq_head_tail(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, double* out) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_head_tail");
   if (rows <= 0) return fail(JQ_E_INVALID, "head/tail undefined for a matrix with 0 rows");
   if (cols <= 0) return JQ_OK;
   if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
@@ -414,6 +415,7 @@ extern "C" int jq_head_tail(jq_ctx* ctx, const double* m, int64_t rows, int64_t 
 
 extern "C" int jq_colsums(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, double* sums) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_colsums");
   if (cols <= 0) return JQ_OK;
   if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
   JQ_TRY(begin_call(ctx));
@@ -434,6 +436,7 @@ extern "C" int jq_reduce(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, c
                          const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* out,
                          int64_t out_capacity, int64_t* out_rows, int64_t* group_bounds) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_reduce");
   if ((ka == nullptr) != (kb == nullptr)) return fail(JQ_E_KEYS, "both tables must carry keys, or neither");
   if (n1 < 0 || n2 < 0 || n1 > 256 || n2 > 256) return fail(JQ_E_INVALID, "column counts must lie in 0..256");
   const bool keyed = ka != nullptr;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <string>
@@ -29,6 +30,14 @@ int fail(int code, const std::string& msg);
     int rc_ = (expr);         \
     if (rc_ != JQ_OK) return rc_; \
   } while (0)
+
+// NVTX (SURVEY.md §5 tracing): a range per public call (JQ_NVTX) and a mark per
+// pipeline stage boundary (stage_event), visible in Nsight Systems / Compute timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define JQ_NVTX(name) ::jq::NvtxRange jq_nvtx_range_(name)
 
 // Count launches of our own kernels (evidence for bench.py "gpu_launches").
 #define JQ_LAUNCHED(ctx) ((ctx)->launches++)
@@ -145,6 +154,8 @@ size_t stage_bytes(const T* p, size_t count) {
 }
 
 int sync_and_check_flags(jq_ctx* ctx);   // stream sync + read device flags
+// ctx->ev[k] (stage timing, jq_timing) + an NVTX mark naming the stage that begins there
+void stage_event(jq_ctx* ctx, int k);
 int begin_call(jq_ctx* ctx);              // device select + ws reset + clear flags
 
 // ---------------------------------------------------------------- device helpers

@@ -227,6 +227,7 @@ using namespace jq;
 
 extern "C" int jq_sort_keys(jq_ctx* ctx, const int64_t* keys, int64_t m, int64_t* keys_out, int64_t* perm_out) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_sort_keys");
   if (m < 0) return fail(JQ_E_INVALID, "negative size");
   if (m > 0 && (!keys || !perm_out)) return fail(JQ_E_INVALID, "null keys or permutation output");
   if (m == 0) return JQ_OK;
@@ -249,6 +250,7 @@ extern "C" int jq_sort_keys(jq_ctx* ctx, const int64_t* keys, int64_t m, int64_t
 extern "C" int jq_gather_rows(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int64_t* perm,
                               double* out) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_gather_rows");
   if (rows < 0 || cols < 0) return fail(JQ_E_INVALID, "negative size");
   if (rows == 0 || cols == 0) return JQ_OK;
   if (!x || !perm || !out) return fail(JQ_E_INVALID, "null argument");

@@ -655,6 +655,7 @@ using namespace jq;
 
 extern "C" int jq_svd_of_r(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values, double* v) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
+  JQ_NVTX("jq_svd_of_r");
   if (n < 0) return fail(JQ_E_INVALID, "negative size");
   if (n == 0) return JQ_OK;
   JQ_TRY(begin_call(ctx));

@@ -1511,19 +1511,19 @@ static int run_stream(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t ali
   if (!a || !b) return fail(JQ_E_OOM, "workspace exhausted (TSQR leaves)");
   ctx->timing.tsqr_ctas += leaves;
   ctx->timing.reduced_rows += vrows;
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
+  if (ctx->record_tsqr_events) stage_event(ctx, 3);
   JQ_TRY(segscan_tiles(ctx, src.side_job()));  // this leaf has no spare warps for it
   JQ_TRY((launch_tsqr<C, Src, false>(ctx, (int)leaves, src, rows_per_cta, vrows, nullptr, 0, a, use_tma)));
   if (defer) {
     *defer = LeafSet{a, b, leaves, C::NP, n, rows_per_cta};
     return JQ_OK;
   }
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (ctx->record_tsqr_events) stage_event(ctx, 4);
   double* fin = nullptr;
   JQ_TRY(tree_combine<C>(ctx, a, b, leaves, &fin));
   finalize_r_kernel<<<(int)cdiv(int64_t(n) * n, 256), 256, 0, ctx->stream>>>(fin, C::NP, n, canonical, r_out);
   JQ_CHECK_LAUNCH(ctx);
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[5], ctx->stream);
+  if (ctx->record_tsqr_events) stage_event(ctx, 5);
   return JQ_OK;
 }
 
@@ -1573,7 +1573,7 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t 
   if (!a || !b) return fail(JQ_E_OOM, "workspace exhausted (TSQR leaves)");
   ctx->timing.tsqr_ctas += ctas;
   ctx->timing.reduced_rows += vrows;
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[3], ctx->stream);
+  if (ctx->record_tsqr_events) stage_event(ctx, 3);
   if (CS::NSPARE == 0) JQ_TRY(segscan_tiles(ctx, src.side_job()));  // else the spare warps run it
   auto kern = tsqr_ws2_kernel<CS, Src>;
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM));
@@ -1585,12 +1585,12 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t 
     *defer = LeafSet{a, b, ctas, C::NP, n, rows_per_cta};
     return JQ_OK;
   }
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (ctx->record_tsqr_events) stage_event(ctx, 4);
   double* fin = nullptr;
   JQ_TRY(tree_combine<C>(ctx, a, b, ctas, &fin));
   finalize_r_kernel<<<(int)cdiv(int64_t(n) * n, 256), 256, 0, ctx->stream>>>(fin, C::NP, n, canonical, r_out);
   JQ_CHECK_LAUNCH(ctx);
-  if (ctx->record_tsqr_events) cudaEventRecord(ctx->ev[5], ctx->stream);
+  if (ctx->record_tsqr_events) stage_event(ctx, 5);
   return JQ_OK;
 }
 

@@ -54,3 +54,46 @@ def test_cli_usage_and_io_exit_codes(tmp_path):
     assert run(["verify", "--left", missing, "--right", missing]) == 2
     assert run(["svd", "--left", missing, "--right", missing, "--values-only", "--with-v",
                 "--out", "x"]) == 2                                     # mutually exclusive flags
+
+
+def test_native_csv_edge_cases(tmp_path):
+    p = tmp_path / "e.csv"
+    p.write_text("h1,h2\r\n\r\n 1.5 , +2.0\r\n\n3e-3,-4\r\n")     # CRLF, blank lines, spaces, signs
+    t = tableio.read_table(str(p), has_header=True)
+    assert np.array_equal(t.data, [[1.5, 2.0], [3e-3, -4.0]])
+    (tmp_path / "empty.csv").write_text("")
+    assert tableio.read_table(str(tmp_path / "empty.csv")).data.shape[0] == 0
+    (tmp_path / "inf.csv").write_text("1,2\n3,inf\n")
+    with pytest.raises(ValueError, match=":2: non-finite"):
+        tableio.read_table(str(tmp_path / "inf.csv"))
+    (tmp_path / "wide.csv").write_text("1,2\n3,4,5\n")
+    with pytest.raises(ValueError, match=":2: ragged"):
+        tableio.read_table(str(tmp_path / "wide.csv"))
+    with pytest.raises(ValueError):
+        tableio.read_table(str(tmp_path / "nope.csv"))
+
+
+def test_native_csv_multi_chunk_round_trip_and_line_numbers(tmp_path):
+    """> 4 MB files are parsed by several threads in newline-aligned chunks: values,
+    keys and error line numbers must not depend on the chunking."""
+    rng = np.random.default_rng(2)
+    m = 120_000
+    keys = np.sort(rng.integers(-50, 5000, m))
+    data = rng.random((m, 4)) * 10.0 ** rng.integers(-8, 8, (m, 4))
+    p = tmp_path / "big.csv"
+    tableio.write_table(tableio.Table(data, keys), str(p))
+    assert p.stat().st_size > (8 << 20)
+    t = tableio.read_table(str(p), key_col=0)
+    assert np.array_equal(t.data, data) and np.array_equal(t.keys, keys)
+    lines = p.read_text().splitlines()
+    bad = 100_001
+    lines[bad - 1] = lines[bad - 1].replace(",", ",x", 1)
+    q = tmp_path / "bad.csv"
+    q.write_text("\n".join(lines) + "\n")
+    with pytest.raises(ValueError, match=f":{bad}: cannot parse"):
+        tableio.read_table(str(q), key_col=0)
+    lines = p.read_text().splitlines()
+    lines[bad - 1] = "-100," + lines[bad - 1].split(",", 1)[1]   # unsorted key deep in the file
+    q.write_text("\n".join(lines) + "\n")
+    with pytest.raises(ValueError, match=f":{bad}: keys are not sorted"):
+        tableio.read_table(str(q), key_col=0)
