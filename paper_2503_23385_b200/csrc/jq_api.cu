@@ -96,6 +96,9 @@ static float ev_ms(jq_ctx* ctx, int a, int b) {
 static size_t figaro_ws(int64_t m1, int64_t n1, int64_t m2, int64_t n2, bool keyed, int sms) {
   const int64_t cap = keyed ? std::max<int64_t>(1, std::min(m1, m2)) : 1;
   const int64_t n = n1 + n2;
+  if (n > 256)  // wide path: the reduced matrix (<= m1 + m2 - 1 rows) + the wide TSQR
+    return (keyed ? group_ws_bytes(m1, m2) : 0) + reduce_emit_ws_bytes(m2, n2, cap) +
+           ws_bytes(size_t(m1 + m2) * n, 8) + wide_tsqr_ws_bytes(m1 + m2, n, sms) + ws_bytes(size_t(n) * n, 8);
   size_t dense = (keyed ? group_ws_bytes(m1, m2) : 0) + segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) +
                  figaro_tsqr_ws_bytes(m1, m2, n, sms) + ws_bytes(size_t(n) * n, 8);
   size_t foot = (keyed ? group_ws_bytes(m1, m2) : 0) + segscan_ws_bytes(m1, std::max<int64_t>(n1, 1), cap) +
@@ -662,8 +665,43 @@ static bool use_footnote(const jq_ctx* ctx, int64_t rows, int64_t n) {
 }
 
 // Device-resident figaro_r: R (n x n, canonical) into r_out (device).
+// Wide joins (n1 + n2 > 256): the reduced matrix is emitted into the workspace
+// (reduce_emit_dev, SPEC row order) and factored by the wide TSQR (jq_wide.cu).
+static int figaro_r_wide(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
+                         const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
+  const bool keyed = ka != nullptr;
+  const int64_t n = n1 + n2;
+  ctx->timing.tsqr_ctas = 0;
+  stage_event(ctx, 0);
+  Groups gr;
+  int64_t total = m1 + m2 - 1;
+  const int64_t cap = keyed ? std::max<int64_t>(1, std::min(m1, m2)) : 1;
+  if (keyed) {
+    JQ_TRY(group_keys_dev(ctx, ka, m1, kb, m2, &gr));
+    int64_t hn[2];
+    JQ_CUDA(cudaMemcpyAsync(hn, gr.d_n, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    JQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    total = hn[1];
+  }
+  stage_event(ctx, 1);
+  ctx->timing.reduced_rows = total;
+  if (total <= 0) {  // empty join: R = 0
+    JQ_CUDA(cudaMemsetAsync(r_out, 0, size_t(n) * n * 8, ctx->stream));
+    for (int k = 2; k <= 5; ++k) stage_event(ctx, k);
+    return JQ_OK;
+  }
+  double* red = ws_alloc<double>(ctx, size_t(total) * n);
+  if (!red) return fail(JQ_E_OOM, "workspace exhausted (wide reduced matrix)");
+  JQ_TRY(reduce_emit_dev(ctx, a, m1, n1, b, m2, n2, keyed ? &gr : nullptr, cap, total, red));
+  stage_event(ctx, 2);
+  JQ_TRY(wide_tsqr_dev(ctx, red, total, n, r_out, true));
+  stage_event(ctx, 5);
+  return JQ_OK;
+}
+
 static int figaro_r_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
                         const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
+  if (n1 + n2 > 256) return figaro_r_wide(ctx, a, m1, n1, ka, b, m2, n2, kb, r_out);
   if (use_footnote(ctx, m1 + m2, n1 + n2)) return figaro_r_footnote_dev(ctx, a, m1, n1, ka, b, m2, n2, kb, r_out);
   const bool keyed = ka != nullptr;
   ctx->timing.tsqr_ctas = 0;
@@ -723,7 +761,7 @@ static int64_t env_bytes(const char* name, int64_t dflt) {
 
 static bool use_streamed(const double* a, int64_t m1, int64_t n1, const double* b, int64_t m2, int64_t n2,
                          const int64_t* ka) {
-  if (ka) return false;
+  if (ka || n1 + n2 > 256) return false;
   if (is_device_ptr(a) || is_device_ptr(b)) return false;
   return (m1 * n1 + m2 * n2) * 8 >= env_bytes("JQ_STREAM_MIN_BYTES", int64_t(1) << 30);
 }
@@ -860,7 +898,7 @@ static int check_tables(int64_t m1, int64_t n1, const int64_t* ka, int64_t m2, i
   if ((ka == nullptr) != (kb == nullptr)) return fail(JQ_E_KEYS, "both tables must carry keys, or neither");
   if (m1 < 0 || m2 < 0 || n1 < 0 || n2 < 0) return fail(JQ_E_INVALID, "negative size");
   if (n1 + n2 == 0) return fail(JQ_E_INVALID, "the join has no columns");
-  if (n1 > 256 || n2 > 256 || n1 + n2 > 256) return fail(JQ_E_INVALID, "n1 + n2 above 256 is not supported");
+  if (n1 + n2 > 512) return fail(JQ_E_INVALID, "n1 + n2 above 512 is not supported");
   if (!ka && (m1 == 0 || m2 == 0)) return fail(JQ_E_INVALID, "reduce_cartesian needs non-empty inputs");
   return JQ_OK;
 }
@@ -964,7 +1002,7 @@ int jq_householder_r(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, d
   if (!ctx) return fail(JQ_E_INVALID, "null context");
   JQ_NVTX("jq_householder_r");
   if (cols <= 0) return fail(JQ_E_INVALID, "householder_r needs at least one column");
-  if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
+  if (cols > 512) return fail(JQ_E_INVALID, "more than 512 columns");
   if (rows < 0) return fail(JQ_E_INVALID, "negative row count");
   JQ_TRY(begin_call(ctx));
   JQ_TRY(ws_reserve(ctx, stage_bytes(m, rows * cols) + stage_bytes((const double*)r, cols * cols) +
@@ -1194,10 +1232,11 @@ int jq_split_group_rows(jq_ctx* ctx, const double* part_sums, const int64_t* par
 int jq_tsqr_stack(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, double* r) {
   if (!ctx) return fail(JQ_E_INVALID, "null context");
   JQ_NVTX("jq_tsqr_stack");
-  if (count <= 0 || n <= 0 || n > 256) return fail(JQ_E_INVALID, "bad R stack geometry");
+  if (count <= 0 || n <= 0 || n > 512) return fail(JQ_E_INVALID, "bad R stack geometry");
   JQ_TRY(begin_call(ctx));
   JQ_TRY(ws_reserve(ctx, stage_bytes(rs, count * n * n) + stage_bytes((const double*)r, n * n) +
-                             2 * ws_bytes(size_t(count + 1) * 256 * 256, 8)));
+                             (n > 256 ? wide_tsqr_ws_bytes(count * n, n, ctx->sms)
+                                      : 2 * ws_bytes(size_t(count + 1) * 256 * 256, 8))));
   const double* drs;
   double* dr;
   JQ_TRY(stage_in(ctx, rs, count * n * n, &drs));

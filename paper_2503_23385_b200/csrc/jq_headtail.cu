@@ -21,16 +21,17 @@
 
 namespace jq {
 
-constexpr int MAXC = 8;  // columns per lane (cols <= 256)
+constexpr int MAXC = 16;  // columns per lane (cols <= 512)
 
-// One warp per TILE_ROWS tile (segscan_tile, jq_segscan.cuh).
+// One warp per TILE_ROWS tile (segscan_tile, jq_segscan.cuh); MC columns per lane.
+template <int MC>
 __global__ void __launch_bounds__(256) segscan_tile_kernel(
     const double* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ gid,
     int64_t ntiles, double* __restrict__ agg, int* __restrict__ flag, double* __restrict__ totals) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= ntiles) return;
-  segscan_tile(x, rows, cols, gid, t, agg, flag, totals, lane);
+  segscan_tile<8, MC>(x, rows, cols, gid, t, agg, flag, totals, lane);
 }
 
 // <= 64 columns: the narrow tile pass (fewer registers -> more warps, 16 rows in flight)
@@ -151,7 +152,7 @@ size_t segscan_ws_bytes(int64_t rows, int64_t cols, int64_t groups_cap) {
 // end = the carry scan over tiles and the fix-up of groups that span tiles.
 int segscan_begin(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, const int32_t* gid,
                   int64_t groups_cap, SegScan* s, SideScan* side) {
-  if (cols > 32 * MAXC) return fail(JQ_E_INVALID, "more than 256 columns per table");
+  if (cols > 32 * MAXC) return fail(JQ_E_INVALID, "more than 512 columns per table");
   s->ntiles = std::max<int64_t>(1, cdiv(rows, TILE_ROWS));
   s->rows = rows;
   s->cols = cols;
@@ -190,8 +191,11 @@ int segscan_tiles(jq_ctx* ctx, const SideScan& side) {
   else if (narrow_tiles() && side.cols <= 64)
     segscan_tile_narrow_kernel<2><<<grid, 32 * wpb, 0, ctx->stream>>>(
         side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
+  else if (side.cols <= 256)
+    segscan_tile_kernel<8><<<grid, 32 * wpb, 0, ctx->stream>>>(
+        side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
   else
-    segscan_tile_kernel<<<grid, 32 * wpb, 0, ctx->stream>>>(
+    segscan_tile_kernel<16><<<grid, 32 * wpb, 0, ctx->stream>>>(
         side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
   JQ_CHECK_LAUNCH(ctx);
   if (k >= 0) {  // algorithmic bytes: the rows read once (+ their segment ids)
@@ -354,9 +358,12 @@ static void launch_tail_emit(jq_ctx* ctx, int cols, unsigned grid, const double*
   else if (cols <= 128)
     tail_emit_kernel<4><<<grid, 256, 0, ctx->stream>>>(x, rows, cols, gid, gstart, scale_count, scale_all,
                                                        out_base, out_base_all, out_ld, col0, carry, ntiles, out);
-  else
+  else if (cols <= 256)
     tail_emit_kernel<8><<<grid, 256, 0, ctx->stream>>>(x, rows, cols, gid, gstart, scale_count, scale_all,
                                                        out_base, out_base_all, out_ld, col0, carry, ntiles, out);
+  else
+    tail_emit_kernel<16><<<grid, 256, 0, ctx->stream>>>(x, rows, cols, gid, gstart, scale_count, scale_all,
+                                                        out_base, out_base_all, out_ld, col0, carry, ntiles, out);
 }
 
 __global__ void tail_base_kernel(const int64_t* __restrict__ red_off, const int64_t* __restrict__ a_count,
@@ -383,6 +390,48 @@ static unsigned grid_for(int64_t work, int threads = 256, int64_t cap = 148 * 16
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(work, threads), cap));
 }
 
+// The reduced matrix in SPEC row order into dout (total_rows x
+// (n1 + n2), device): scan of B, top rows [sqrt(m2g) A_g | head(B_g)], tail rows
+// [0 | sqrt(m1g) tail(B_g)].  gr = grouping (keyed) or nullptr (Cartesian).  Shared by
+// jq_reduce and figaro_r's wide path (n1 + n2 > 256: reduce, then jq_wide.cu's TSQR).
+int reduce_emit_dev(jq_ctx* ctx, const double* da, int64_t m1, int64_t n1, const double* db, int64_t m2,
+                    int64_t n2, const Groups* gr, int64_t cap, int64_t total_rows, double* dout) {
+  const bool keyed = gr != nullptr;
+  const int64_t n = n1 + n2;
+  if (n2 == 0)  // bottom rows are exact-zero rows of width n1
+    JQ_CUDA(cudaMemsetAsync(dout, 0, total_rows * n * 8, ctx->stream));
+  SegScan ss;
+  const int64_t cols_b = std::max<int64_t>(n2, 1);
+  if (n2 > 0) {
+    JQ_TRY(segscan_dev(ctx, db, m2, n2, keyed ? gr->gid_b : nullptr, keyed ? gr->b_start : nullptr,
+                       keyed ? gr->b_count : nullptr, keyed ? gr->d_n : nullptr, cap, &ss));
+  } else {
+    JQ_TRY(segscan_dev(ctx, db, 0, cols_b, nullptr, nullptr, nullptr, nullptr, cap, &ss));
+  }
+  top_emit_kernel<<<grid_for(m1 * 32), 256, 0, ctx->stream>>>(
+      da, m1, (int)n1, keyed ? gr->gid_a : nullptr, keyed ? gr->a_start : nullptr,
+      keyed ? gr->b_count : nullptr, m2, keyed ? gr->red_off : nullptr, ss.totals, (int)n2, dout);
+  JQ_CHECK_LAUNCH(ctx);
+  if (n2 > 0) {
+    int64_t* base = nullptr;
+    if (keyed) {
+      base = ws_alloc<int64_t>(ctx, cap);
+      if (!base) return fail(JQ_E_OOM, "workspace exhausted (reduce)");
+      tail_base_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(gr->red_off, gr->a_count, gr->d_n, base);
+      JQ_CHECK_LAUNCH(ctx);
+    }
+    launch_tail_emit(ctx, (int)n2, (unsigned)cdiv(ss.ntiles, 8), db, m2, keyed ? gr->gid_b : nullptr,
+                     keyed ? gr->b_start : nullptr, keyed ? gr->a_count : nullptr, (double)m1, base, m1, (int)n,
+                     (int)n1, ss.carry, ss.ntiles, dout);
+    JQ_CHECK_LAUNCH(ctx);
+  }
+  return JQ_OK;
+}
+
+size_t reduce_emit_ws_bytes(int64_t m2, int64_t n2, int64_t cap) {
+  return segscan_ws_bytes(m2, std::max<int64_t>(n2, 1), cap) + ws_bytes(cap, 8) + 4096;
+}
+
 // ------------------------------------------------------------------ public API
 }  // namespace jq
 
@@ -393,7 +442,7 @@ extern "C" int jq_head_tail(jq_ctx* ctx, const double* m, int64_t rows, int64_t 
   JQ_NVTX("jq_head_tail");
   if (rows <= 0) return fail(JQ_E_INVALID, "head/tail undefined for a matrix with 0 rows");
   if (cols <= 0) return JQ_OK;
-  if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
+  if (cols > 512) return fail(JQ_E_INVALID, "more than 512 columns");
   JQ_TRY(begin_call(ctx));
   size_t need = stage_bytes(m, rows * cols) + stage_bytes((const double*)out, rows * cols) +
                 segscan_ws_bytes(rows, cols, 1);
@@ -417,7 +466,7 @@ extern "C" int jq_colsums(jq_ctx* ctx, const double* x, int64_t rows, int64_t co
   if (!ctx) return fail(JQ_E_INVALID, "null context");
   JQ_NVTX("jq_colsums");
   if (cols <= 0) return JQ_OK;
-  if (cols > 256) return fail(JQ_E_INVALID, "more than 256 columns");
+  if (cols > 512) return fail(JQ_E_INVALID, "more than 512 columns");
   JQ_TRY(begin_call(ctx));
   JQ_TRY(ws_reserve(ctx, stage_bytes(x, rows * cols) + stage_bytes((const double*)sums, cols) +
                              segscan_ws_bytes(rows, cols, 1)));
@@ -438,7 +487,7 @@ extern "C" int jq_reduce(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, c
   if (!ctx) return fail(JQ_E_INVALID, "null context");
   JQ_NVTX("jq_reduce");
   if ((ka == nullptr) != (kb == nullptr)) return fail(JQ_E_KEYS, "both tables must carry keys, or neither");
-  if (n1 < 0 || n2 < 0 || n1 > 256 || n2 > 256) return fail(JQ_E_INVALID, "column counts must lie in 0..256");
+  if (n1 < 0 || n2 < 0 || n1 > 512 || n2 > 512) return fail(JQ_E_INVALID, "column counts must lie in 0..512");
   const bool keyed = ka != nullptr;
   if (!keyed && (m1 <= 0 || m2 <= 0)) return fail(JQ_E_INVALID, "reduce_cartesian needs non-empty inputs");
   JQ_TRY(begin_call(ctx));
@@ -482,32 +531,7 @@ extern "C" int jq_reduce(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, c
   JQ_TRY(stage_in(ctx, a, m1 * n1, &da));
   JQ_TRY(stage_in(ctx, b, m2 * n2, &db));
   JQ_TRY(stage_out(ctx, out, total_rows * n, &dout));
-  if (n2 == 0)  // bottom rows are exact-zero rows of width n1
-    JQ_CUDA(cudaMemsetAsync(dout, 0, total_rows * n * 8, ctx->stream));
-  SegScan ss;
-  const int64_t cols_b = std::max<int64_t>(n2, 1);
-  if (n2 > 0) {
-    JQ_TRY(segscan_dev(ctx, db, m2, n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
-                       keyed ? gr.b_count : nullptr, keyed ? gr.d_n : nullptr, cap, &ss));
-  } else {
-    JQ_TRY(segscan_dev(ctx, db, 0, cols_b, nullptr, nullptr, nullptr, nullptr, cap, &ss));
-  }
-  top_emit_kernel<<<grid_for(m1 * 32), 256, 0, ctx->stream>>>(
-      da, m1, (int)n1, keyed ? gr.gid_a : nullptr, keyed ? gr.a_start : nullptr,
-      keyed ? gr.b_count : nullptr, m2, keyed ? gr.red_off : nullptr, ss.totals, (int)n2, dout);
-  JQ_CHECK_LAUNCH(ctx);
-  if (n2 > 0) {
-    int64_t* base = nullptr;
-    if (keyed) {
-      base = ws_alloc<int64_t>(ctx, cap);
-      tail_base_kernel<<<grid_for(cap), 256, 0, ctx->stream>>>(gr.red_off, gr.a_count, gr.d_n, base);
-      JQ_CHECK_LAUNCH(ctx);
-    }
-    launch_tail_emit(ctx, (int)n2, (unsigned)cdiv(ss.ntiles, 8), db, m2, keyed ? gr.gid_b : nullptr,
-                     keyed ? gr.b_start : nullptr, keyed ? gr.a_count : nullptr, (double)m1, base, m1, (int)n,
-                     (int)n1, ss.carry, ss.ntiles, dout);
-    JQ_CHECK_LAUNCH(ctx);
-  }
+  JQ_TRY(reduce_emit_dev(ctx, da, m1, n1, db, m2, n2, keyed ? &gr : nullptr, cap, total_rows, dout));
   JQ_TRY(copy_out(ctx, out, (const double*)dout, total_rows * n));
   return sync_and_check_flags(ctx);
 }

@@ -306,6 +306,14 @@ __device__ __forceinline__ void join_row(const JoinArgs& ja, int64_t v, int64_t&
 int join_tsqr_dev(jq_ctx* ctx, const JoinArgs& ja, double* r_out, bool canonical);
 size_t figaro_tsqr_ws_bytes(int64_t m1, int64_t m2, int64_t n, int sms);
 
+// The reduced matrix into device memory (jq_headtail.cu; gr = nullptr: Cartesian).
+int reduce_emit_dev(jq_ctx* ctx, const double* da, int64_t m1, int64_t n1, const double* db, int64_t m2,
+                    int64_t n2, const Groups* gr, int64_t cap, int64_t total_rows, double* dout);
+size_t reduce_emit_ws_bytes(int64_t m2, int64_t n2, int64_t cap);
+// Wide Householder TSQR, 256 < n <= 512 (jq_wide.cu).
+int wide_tsqr_dev(jq_ctx* ctx, const double* m, int64_t rows, int64_t n, double* r_out, bool canonical);
+size_t wide_tsqr_ws_bytes(int64_t rows, int64_t n, int sms);
+
 // SVD (jq_svd.cu).
 size_t svd_ws_bytes(int64_t n);
 int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values, double* v);

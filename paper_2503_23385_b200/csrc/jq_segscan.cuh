@@ -8,7 +8,7 @@
 
 namespace jq {
 
-constexpr int SEG_MAXC = 8;  // columns per lane (cols <= 256)
+constexpr int SEG_MAXC = 8;  // columns per lane (cols <= 256); the standalone kernel also has 16 (<= 512)
 
 // Tile t.  Segment id of row r: gid[r] (or 0 when gid is null = one segment).  Writes
 // agg[t] (sum of the segment open at the tile end, restricted to the tile), flag[t]
@@ -16,7 +16,7 @@ constexpr int SEG_MAXC = 8;  // columns per lane (cols <= 256)
 // in-tile partial sum into totals[seg].  Rows are loaded BATCH at a time (a lone warp
 // must keep enough bytes in flight); the additions happen row by row in the same order
 // as with any other batching.
-template <int BATCH = 8>
+template <int BATCH = 8, int MAXCL = SEG_MAXC>
 __device__ __forceinline__ void segscan_tile(const double* __restrict__ x, int64_t rows, int cols,
                                              const int32_t* __restrict__ gid, int64_t t, double* __restrict__ agg,
                                              int* __restrict__ flag, double* __restrict__ totals, int lane) {
@@ -115,9 +115,9 @@ __device__ __forceinline__ void segscan_tile(const double* __restrict__ x, int64
     if (lane == 0) flag[t] = any_start;
     return;
   }
-  double s[SEG_MAXC];
+  double s[MAXCL];
 #pragma unroll
-  for (int k = 0; k < SEG_MAXC; ++k) s[k] = 0.0;
+  for (int k = 0; k < MAXCL; ++k) s[k] = 0.0;
   for (int64_t r = r0; r < r1; ++r) {
     const int sr = gid ? gid[r] : 0;
     const bool start = (r == 0) || (r > r0 && sr != seg);
@@ -125,14 +125,14 @@ __device__ __forceinline__ void segscan_tile(const double* __restrict__ x, int64
       // previous segment ended at r-1 inside this tile
       if (seg >= 0)
 #pragma unroll
-        for (int k = 0; k < SEG_MAXC; ++k)
+        for (int k = 0; k < MAXCL; ++k)
           if (k * 32 + lane < cols) totals[(int64_t)seg * cols + k * 32 + lane] = s[k];
       any_start = 1;
     }
     seg = sr;
     const double* row = x + r * cols;
 #pragma unroll
-    for (int k = 0; k < SEG_MAXC; ++k) {
+    for (int k = 0; k < MAXCL; ++k) {
       const int c = k * 32 + lane;
       if (c < cols) {
         const double v = __ldg(row + c);
@@ -144,10 +144,10 @@ __device__ __forceinline__ void segscan_tile(const double* __restrict__ x, int64
   const bool ends_here = (r1 == rows) || (gid && gid[r1] != seg);
   if (ends_here && seg >= 0)
 #pragma unroll
-    for (int k = 0; k < SEG_MAXC; ++k)
+    for (int k = 0; k < MAXCL; ++k)
       if (k * 32 + lane < cols) totals[(int64_t)seg * cols + k * 32 + lane] = s[k];
 #pragma unroll
-  for (int k = 0; k < SEG_MAXC; ++k)
+  for (int k = 0; k < MAXCL; ++k)
     if (k * 32 + lane < cols) agg[t * cols + k * 32 + lane] = s[k];
   if (lane == 0) flag[t] = any_start;
 }

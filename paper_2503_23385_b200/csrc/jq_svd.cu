@@ -162,17 +162,23 @@ __global__ void __launch_bounds__(SVDC_THREADS)
 jacobi_coop_kernel(double* __restrict__ A, double* __restrict__ V, int n, int want_v, double tol, int max_sweeps,
                    int* flags, double* __restrict__ part, int* __restrict__ rotated_sweep, double* __restrict__ values,
                    double* __restrict__ vout, int n_out) {
+  // thread i owns rows i and i + SVDC_THREADS (n <= 2 SVDC_THREADS = 512)
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
+  constexpr int RPT = 2;
   __shared__ double red[96];
-  __shared__ double sig[256];
-  __shared__ int perm[256];
+  __shared__ double sig[RPT * SVDC_THREADS];
+  __shared__ int perm[RPT * SVDC_THREADS];
   const int pi = blockIdx.x, i = threadIdx.x;
   // |R|_F^2 (fixed-order two-level sum) -> negligible-column threshold
   {
     double f = 0.0;
     for (int j = pi; j < n; j += gridDim.x)
-      if (i < n) f = fma(A[(size_t)j * n + i], A[(size_t)j * n + i], f);
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int row = i + u * SVDC_THREADS;
+        if (row < n) f = fma(A[(size_t)j * n + row], A[(size_t)j * n + row], f);
+      }
     double z1 = 0.0, z2 = 0.0;
     block_sum3(f, z1, z2, red);
     if (i == 0) part[pi] = f;
@@ -189,8 +195,17 @@ jacobi_coop_kernel(double* __restrict__ A, double* __restrict__ V, int n, int wa
       if (p > q) { const int tmp = p; p = q; q = tmp; }
       double* ap = A + (size_t)p * n;
       double* aq = A + (size_t)q * n;
-      const double x = i < n ? ap[i] : 0.0, y = i < n ? aq[i] : 0.0;
-      double al = x * x, be = y * y, ga = x * y;
+      double x[RPT], y[RPT];
+      double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int row = i + u * SVDC_THREADS;
+        x[u] = row < n ? ap[row] : 0.0;
+        y[u] = row < n ? aq[row] : 0.0;
+        al = fma(x[u], x[u], al);
+        be = fma(y[u], y[u], be);
+        ga = fma(x[u], y[u], ga);
+      }
       block_sum3(al, be, ga, red);
       const bool rot = !(al <= tiny || be <= tiny || ga == 0.0 || fabs(ga) < tol * (sqrt(al) * sqrt(be)));
       if (rot) {
@@ -198,15 +213,19 @@ jacobi_coop_kernel(double* __restrict__ A, double* __restrict__ V, int n, int wa
         const double t = zeta >= 0.0 ? 1.0 / (zeta + sqrt(1.0 + zeta * zeta))
                                      : -1.0 / (-zeta + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        if (i < n) {
-          ap[i] = c * x - s * y;
-          aq[i] = s * x + c * y;
-          if (want_v) {
-            double* vp = V + (size_t)p * n;
-            double* vq = V + (size_t)q * n;
-            const double u = vp[i], w = vq[i];
-            vp[i] = c * u - s * w;
-            vq[i] = s * u + c * w;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const int row = i + u * SVDC_THREADS;
+          if (row < n) {
+            ap[row] = c * x[u] - s * y[u];
+            aq[row] = s * x[u] + c * y[u];
+            if (want_v) {
+              double* vp = V + (size_t)p * n;
+              double* vq = V + (size_t)q * n;
+              const double uu = vp[row], w = vq[row];
+              vp[row] = c * uu - s * w;
+              vq[row] = s * uu + c * w;
+            }
           }
         }
         if (i == 0) rotated_sweep[sweep] = 1;  // benign race: every writer stores 1
@@ -218,7 +237,12 @@ jacobi_coop_kernel(double* __restrict__ A, double* __restrict__ V, int n, int wa
   if (sweep == max_sweeps && pi == 0 && i == 0) atomicOr(flags, FLAG_NOCONV);
   // sigma = column norms (CTA pi: columns pi, pi + grid, ...), then CTA 0 sorts
   for (int j = pi; j < n; j += gridDim.x) {
-    double s = (i < n) ? A[(size_t)j * n + i] * A[(size_t)j * n + i] : 0.0, z1 = 0.0, z2 = 0.0;
+    double s = 0.0, z1 = 0.0, z2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int row = i + u * SVDC_THREADS;
+      if (row < n) s = fma(A[(size_t)j * n + row], A[(size_t)j * n + row], s);
+    }
     block_sum3(s, z1, z2, red);
     if (i == 0) part[j] = sqrt(s);
   }
@@ -573,13 +597,13 @@ static int launch_jacobi_cluster(jq_ctx* ctx, const double* A, int np, double* s
 }
 
 int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values, double* v) {
-  if (n > 256) return fail(JQ_E_INVALID, "svd_of_r supports n <= 256");
+  if (n > 512) return fail(JQ_E_INVALID, "svd_of_r supports n <= 512");
   if (n == 0) return JQ_OK;
   static const bool coop = [] {  // JQ_SVD_IMPL=coop: the grid-barrier kernel (A/B tests)
     const char* e = getenv("JQ_SVD_IMPL");
     return e && strcmp(e, "coop") == 0;
   }();
-  if (n >= 31 && !coop) {
+  if (n >= 31 && n <= 256 && !coop) {
     // cluster path: zero columns pad the tournament to a multiple of 32 (never rotated,
     // sigma 0, ranked after every real column)
     const int npc = (int)((n + 31) / 32 * 32);

@@ -1468,6 +1468,7 @@ size_t tsqr_pair_ws_bytes(int64_t n, int sms) {
 }
 
 size_t tsqr_ws_bytes(int64_t rows, int64_t n, int sms) {
+  if (n > 256) return wide_tsqr_ws_bytes(rows, n, sms);
   int np = np_for(n);
   if (np < 0) return 0;
   int64_t leaves = std::max<int64_t>(1, std::min<int64_t>(int64_t(sms) * 32, cdiv(rows, 32) + 16));
@@ -1689,6 +1690,7 @@ int tsqr_finish_pair(jq_ctx* ctx, const LeafSet& x, const LeafSet& y, double* rx
 
 int tsqr_dense_dev(jq_ctx* ctx, const double* m, int64_t rows, int64_t cols, double* r_out,
                    bool canonical) {
+  if (cols > 256) return wide_tsqr_dev(ctx, m, rows, cols, r_out, canonical);  // jq_wide.cu
   DenseSrc src{m, rows, cols};
   const int tma = (reinterpret_cast<uintptr_t>(m) & 15) == 0;
   return dispatch_stream(ctx, src, std::max<int64_t>(rows, 1), 64, (int)cols, canonical, r_out, tma);
@@ -1740,7 +1742,8 @@ int tsqr_stack_dev(jq_ctx* ctx, const double* rs, int64_t count, int64_t n, doub
     case 128: return stack_impl<Cfg<128>>(ctx, rs, count, n, r_out, canonical);
     case 256: return stack_impl<Cfg<256>>(ctx, rs, count, n, r_out, canonical);
   }
-  return fail(JQ_E_INVALID, "column count above 256 is not supported by the TSQR kernels");
+  if (n <= 512) return wide_tsqr_dev(ctx, rs, count * n, n, r_out, canonical);  // the stack as rows
+  return fail(JQ_E_INVALID, "column count above 512 is not supported by the TSQR kernels");
 }
 
 int figaro_tsqr_dev(jq_ctx* ctx, const FigaroArgs& fa, double* r_out, bool canonical) {

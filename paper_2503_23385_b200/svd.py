@@ -28,6 +28,8 @@ def svd_of_r(r, want_vectors: bool = False) -> SvdResult:
     if r.shape[0] != r.shape[1]:
         raise ValueError(f"svd_of_r needs a square upper-triangular R, got {r.shape[0]}x{r.shape[1]}")
     n = r.shape[1]
+    if n > 512:
+        raise ValueError(f"svd_of_r supports n <= 512 (got {n})")
     vals = like((n,), r)
     v = like((n, n), r) if want_vectors else None
     N.use_torch_stream(r)

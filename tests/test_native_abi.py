@@ -77,6 +77,8 @@ def test_host_validation_errors_before_any_gpu_work():
         P.svd_of_r(np.ones((3, 4)))                        # R is n x n
     with pytest.raises(ValueError, match="square"):
         P.svd_of_r(np.ones((4, 3)), True)
+    with pytest.raises(ValueError, match="512"):
+        P.svd_of_r(np.eye(513))                            # wide cap (jq_svd.cu coop kernel)
 
 
 def test_default_stream_maps_to_legacy_handle():
