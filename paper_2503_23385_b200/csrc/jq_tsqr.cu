@@ -117,6 +117,10 @@ __device__ __forceinline__ int rix(int r, int c) {
 // rows to fetch (ptr, raw columns rc, rows available), turns the fetched raw rows
 // into Claim-1 rows in place (prep) and yields C[i][l] for the register load.
 
+// sub-segments per loader warp in the multi-loader tail transform (independent
+// recurrences in flight per lane; FigaroSrc::seg_pass1 / seg_pass2)
+constexpr int SEG_SUB = 4;
+
 struct DenseSrc {
   const double* m;
   int64_t rows, cols;
@@ -138,10 +142,11 @@ struct DenseSrc {
   template <class C>
   __device__ void seg_coeffs(double*, int64_t, int, int, int, int) const {}
   template <class C>
-  __device__ void seg_pass1(const double*, const double*, double*, int64_t, int, int, int, int) const {}
+  __device__ void seg_pass1(const double*, const double*, double*, int64_t, int, int, int, int,
+                            double (&)[SEG_SUB][2], bool (&)[SEG_SUB][2]) const {}
   template <class C>
   __device__ void seg_pass2(double*, double*, const double*, const double*, double, double, int64_t, int, int, int,
-                            int, int, int) const {}
+                            int, int, int, const double (&)[SEG_SUB][2], const bool (&)[SEG_SUB][2]) const {}
   SideScan side_job() const { return SideScan{}; }
   __device__ void side_scan(int, int, int) const {}
   // after the leaf's last chunk: S holds the running prefix (carry-free leaves export it)
@@ -496,69 +501,141 @@ struct FigaroSrc {
     }
     const int64_t b0 = v0 - m1pad;
     int* imode = reinterpret_cast<int*>(mode);
-    for (int i = i0 + lane; i < i1; i += 32) {
+    // all row gathers of the segment first (group id, then the group's start and the
+    // other side's count): two dependent rounds of global loads instead of 2 per row
+    constexpr int IT = (C::K / C::NLOAD + 31) / 32;
+    const int e = min(i1, nrows);
+    int gg[IT];
+    int64_t st[IT], cnt[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int i = i0 + lane + 32 * it;
+      gg[it] = (i < e && fa.gid_b) ? __ldg(fa.gid_b + b0 + i) : 0;
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int i = i0 + lane + 32 * it;
+      st[it] = 0;
+      cnt[it] = fa.m1_global;
+      if (fa.gid_b && i < e && gg[it] >= 0) {
+        st[it] = __ldg(fa.b_start + gg[it]);
+        cnt[it] = __ldg(fa.a_count + gg[it]);
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int i = i0 + lane + 32 * it;
+      if (i >= i1) break;
       int md = 0;
       double a1 = 0.0, a2 = 0.0;
-      if (i < nrows) {
+      if (i < nrows && gg[it] >= 0) {
         const int64_t br = b0 + i;
-        int64_t rr = 0;
-        double m1g = 0.0;
-        bool valid = true;
-        if (fa.gid_b) {
-          const int g = fa.gid_b[br];
-          valid = g >= 0;
-          if (valid) { rr = br - fa.b_start[g]; m1g = (double)fa.a_count[g]; }
+        const int64_t rr = fa.gid_b ? br - st[it] : cart_row(br);
+        const double m1g = (double)cnt[it];
+        if (rr == 0) {
+          md = 1;
         } else {
-          rr = cart_row(br);
-          m1g = (double)fa.m1_global;
-        }
-        if (valid) {
-          if (rr == 0) {
-            md = 1;
-          } else {
-            const double rd = (double)rr;
-            md = 2;
-            a2 = (m1g * rsqrt_nr(m1g)) * rsqrt_nr(rd * (rd + 1.0));
-            a1 = rd * a2;
-          }
+          const double rd = (double)rr;
+          md = 2;
+          a2 = (m1g * rsqrt_nr(m1g)) * rsqrt_nr(rd * (rd + 1.0));
+          a1 = rd * a2;
         }
       }
-      c1[i] = a1; c2[i] = a2; imode[i] = md;
+      // packed per-row coefficients of the branch-free passes: out = c1 x - c2 S and
+      // S <- keep S + w x (group start: keep 0, w 1; tail row: 1, 1; no row: 1, 0) --
+      // exactly the selects of the row mode (multiplications by 0 / 1 are exact)
+      *reinterpret_cast<double4*>(scratch + 3 * C::K + 4 * i) =
+          make_double4(a1, a2, md == 1 ? 0.0 : 1.0, md == 0 ? 0.0 : 1.0);
+      (void)imode;
     }
   }
+  // Segment [i0, i1) in SEG_SUB sub-segments processed in lockstep (independent
+  // recurrences: the per-row latency is paid once per SEG_SUB rows).  pass1: each
+  // sub-segment's (sum since its last group start, group start seen) per column, kept
+  // in registers, and their combination -> lsr (the segment's aggregate).
   template <class C>
   __device__ void seg_pass1(const double* raw, const double* scratch, double* lsr, int64_t v0, int nrows, int lane,
-                            int i0, int i1) const {
+                            int i0, int i1, double (&sl)[SEG_SUB][2], bool (&sr)[SEG_SUB][2]) const {
     if (v0 < m1pad) return;
-    const int* imode = reinterpret_cast<const int*>(scratch + 2 * C::K);
     const int n2 = (int)fa.n2;
     const int e = min(i1, nrows);
+    const int L = (i1 - i0 + SEG_SUB - 1) / SEG_SUB;
+    const double4* cf = reinterpret_cast<const double4*>(scratch + 3 * C::K);
+    int cnt[SEG_SUB];
+#pragma unroll
+    for (int u = 0; u < SEG_SUB; ++u) cnt[u] = max(0, min(L, e - (i0 + u * L)));
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = lane + 32 * h;
+#pragma unroll
+      for (int u = 0; u < SEG_SUB; ++u) { sl[u][h] = 0.0; sr[u][h] = false; }
       if (c >= n2) continue;
-      double loc = 0.0, reset = 0.0;
-      for (int i = i0; i < e; ++i) {
-        const double xv = raw[i * n2 + c];
-        const int md = imode[i];
-        if (md == 1) { loc = xv; reset = 1.0; }
-        else if (md == 2) loc += xv;
+      // sub-segment cursors (strength-reduced addressing); rows r < cnt[SEG_SUB-1] exist in
+      // every sub-segment (cnt is non-increasing), the few others are predicated
+      const double* xp[SEG_SUB];
+      const double4* cp[SEG_SUB];
+#pragma unroll
+      for (int u = 0; u < SEG_SUB; ++u) {
+        xp[u] = raw + (i0 + u * L) * n2 + c;
+        cp[u] = cf + i0 + u * L;
+      }
+      const int rfull = cnt[SEG_SUB - 1];
+      for (int r = 0; r < rfull; ++r) {
+        double xv[SEG_SUB];
+        double4 q[SEG_SUB];
+#pragma unroll
+        for (int u = 0; u < SEG_SUB; ++u) {
+          xv[u] = *xp[u];
+          q[u] = *cp[u];
+          xp[u] += n2;
+          ++cp[u];
+        }
+#pragma unroll
+        for (int u = 0; u < SEG_SUB; ++u) {
+          sl[u][h] = fma(q[u].z, sl[u][h], q[u].w * xv[u]);
+          sr[u][h] = sr[u][h] || q[u].z == 0.0;
+        }
+      }
+      for (int r = rfull; r < L; ++r) {
+#pragma unroll
+        for (int u = 0; u < SEG_SUB; ++u) {
+          if (r < cnt[u]) {
+            const double xv = *xp[u];
+            const double4 q = *cp[u];
+            xp[u] += n2;
+            ++cp[u];
+            sl[u][h] = fma(q.z, sl[u][h], q.w * xv);
+            sr[u][h] = sr[u][h] || q.z == 0.0;
+          }
+        }
+      }
+      double loc = 0.0;
+      bool rst = false;
+#pragma unroll
+      for (int u = 0; u < SEG_SUB; ++u) {
+        loc = sr[u][h] ? sl[u][h] : loc + sl[u][h];
+        rst = rst || sr[u][h];
       }
       lsr[c] = loc;
-      lsr[64 + c] = reset;
+      lsr[64 + c] = rst ? 1.0 : 0.0;
     }
   }
-  // s_in0 / s_in1: S of this lane's columns read before the barrier that precedes this
-  // pass (the last segment rewrites S at its end)
+  // pass2: carry-in of the segment (S and the earlier segments), of each sub-segment,
+  // then the in-place transform of the sub-segments in lockstep.  s_in0 / s_in1: S of
+  // this lane's columns read before the barrier that precedes this pass (the last
+  // segment rewrites S at its end).
   template <class C>
   __device__ void seg_pass2(double* raw, double* S, const double* scratch, const double* lsr_all, double s_in0,
-                            double s_in1, int64_t v0, int nrows, int lane, int i0, int i1, int seg, int nseg) const {
+                            double s_in1, int64_t v0, int nrows, int lane, int i0, int i1, int seg, int nseg,
+                            const double (&sl)[SEG_SUB][2], const bool (&sr)[SEG_SUB][2]) const {
     if (v0 < m1pad) return;
-    const double* c1 = scratch;
-    const double* c2 = scratch + C::K;
-    const int* imode = reinterpret_cast<const int*>(scratch + 2 * C::K);
     const int n2 = (int)fa.n2;
     const int e = min(i1, nrows);
+    const int L = (i1 - i0 + SEG_SUB - 1) / SEG_SUB;
+    const double4* cf = reinterpret_cast<const double4*>(scratch + 3 * C::K);
+    int cnt[SEG_SUB];
+#pragma unroll
+    for (int u = 0; u < SEG_SUB; ++u) cnt[u] = max(0, min(L, e - (i0 + u * L)));
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = lane + 32 * h;
@@ -568,22 +645,53 @@ struct FigaroSrc {
         const double l = lsr_all[k * 128 + c], r = lsr_all[k * 128 + 64 + c];
         sv = r != 0.0 ? l : sv + l;
       }
-      for (int ib = i0; ib < e; ib += 4) {
-        double xv[4];
+      double su[SEG_SUB];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) xv[k] = ib + k < e ? raw[(ib + k) * n2 + c] : 0.0;
+      for (int u = 0; u < SEG_SUB; ++u) {
+        su[u] = sv;
+        sv = sr[u][h] ? sl[u][h] : sv + sl[u][h];
+      }
+      if (seg == nseg - 1) S[c] = sv;  // the chunk's carry-out (all reads of S happened before)
+      double* xp[SEG_SUB];
+      const double4* cp[SEG_SUB];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (ib + k < e) {
-            const int md = imode[ib + k];
-            double out = 0.0;
-            if (md == 1) sv = xv[k];
-            else if (md == 2) { out = fma(c1[ib + k], xv[k], -c2[ib + k] * sv); sv += xv[k]; }
-            raw[(ib + k) * n2 + c] = out;
+      for (int u = 0; u < SEG_SUB; ++u) {
+        xp[u] = raw + (i0 + u * L) * n2 + c;
+        cp[u] = cf + i0 + u * L;
+      }
+      const int rfull = cnt[SEG_SUB - 1];
+      // tail rows: c1 x - c2 S; group starts and empty rows have c1 = c2 = 0 -> 0
+      for (int r = 0; r < rfull; ++r) {
+        double xv[SEG_SUB];
+        double4 q[SEG_SUB];
+#pragma unroll
+        for (int u = 0; u < SEG_SUB; ++u) {
+          xv[u] = *xp[u];
+          q[u] = *cp[u];
+        }
+#pragma unroll
+        for (int u = 0; u < SEG_SUB; ++u) {
+          const double out = fma(q[u].x, xv[u], -q[u].y * su[u]);
+          su[u] = fma(q[u].z, su[u], q[u].w * xv[u]);
+          *xp[u] = out;
+          xp[u] += n2;
+          ++cp[u];
+        }
+      }
+      for (int r = rfull; r < L; ++r) {
+#pragma unroll
+        for (int u = 0; u < SEG_SUB; ++u) {
+          if (r < cnt[u]) {
+            const double xv = *xp[u];
+            const double4 q = *cp[u];
+            const double out = fma(q.x, xv, -q.y * su[u]);
+            su[u] = fma(q.z, su[u], q.w * xv);
+            *xp[u] = out;
+            xp[u] += n2;
+            ++cp[u];
           }
         }
       }
-      if (seg == nseg - 1) S[c] = sv;
     }
   }
 

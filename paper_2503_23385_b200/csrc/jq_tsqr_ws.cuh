@@ -56,8 +56,9 @@ struct CfgS {
   static constexpr int OFF_TAU = OFF_U + 64;
   static constexpr int OFF_SC = OFF_TAU + 8;
   static constexpr int OFF_P = OFF_SC + 8;                // [2][DW][8]
-  static constexpr int OFF_LD = OFF_P + 2 * DW * 8;       // loader per-row scalars [3][K]
-  static constexpr int OFF_S = OFF_LD + 3 * K;            // loader running prefix
+  static constexpr int OFF_LD = OFF_P + 2 * DW * 8;       // loader per-row scalars: c1, c2, mode [3][K], then
+  // the multi-loader transform's packed {c1, c2, keep, w} per row [K][4]
+  static constexpr int OFF_S = OFF_LD + 7 * K;            // loader running prefix
   static constexpr int OFF_FLAG = OFF_S + NP;             // [2] chain accepted, by parity
   static constexpr int OFF_GP = OFF_FLAG + 2;             // [DW][64] C^T C partials of the next tile (ws2)
   static constexpr int OFF_GD = OFF_GP + DW * 64;         // [DW][64] direct Gram partials (ws2)
@@ -72,6 +73,7 @@ struct CfgS {
   static_assert(SMEM <= (MIN_CTAS == 1 ? 227 : 113) * 1024, "shared memory per CTA");
   static_assert(NP <= 128, "loader transform assumes <= 128 columns per side");
   static_assert(OFF_LD - OFF_U >= 16 * LDT + 16, "factor_panel_chol scratch (U .. P)");
+  static_assert((OFF_LD + 3 * K) % 2 == 0, "16-byte aligned packed loader coefficients");
 };
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned count) {
@@ -308,13 +310,20 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
         src.template prep_warp<C>(raw, S, scratch, r0, nr, lane);
       } else {
         named_bar(BAR_LOAD, C::NLOAD * 32);  // raw rows of the chunk in shared memory
+        if (li == 0) TR(2, 4);
         const int i0 = li * C::K / C::NLOAD, i1 = (li + 1) * C::K / C::NLOAD;
         src.template seg_coeffs<C>(scratch, r0, nr, lane, i0, i1);
         __syncwarp();
-        src.template seg_pass1<C>(raw, scratch, lsr + li * 128, r0, nr, lane, i0, i1);
+        if (li == 0) TR(2, 5);
+        double sub_l[SEG_SUB][2];
+        bool sub_r[SEG_SUB][2];
+        src.template seg_pass1<C>(raw, scratch, lsr + li * 128, r0, nr, lane, i0, i1, sub_l, sub_r);
         const double s_in0 = lane < C::NP ? S[lane] : 0.0, s_in1 = lane + 32 < C::NP ? S[lane + 32] : 0.0;
+        if (li == 0) TR(2, 6);
         named_bar(BAR_LOAD, C::NLOAD * 32);  // segment sums published, S read by every segment
-        src.template seg_pass2<C>(raw, S, scratch, lsr, s_in0, s_in1, r0, nr, lane, i0, i1, li, C::NLOAD);
+        if (li == 0) TR(2, 7);
+        src.template seg_pass2<C>(raw, S, scratch, lsr, s_in0, s_in1, r0, nr, lane, i0, i1, li, C::NLOAD, sub_l,
+                                  sub_r);
         named_bar(BAR_LOAD, C::NLOAD * 32);  // chunk transformed
       }
       TR(2, 3);
