@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "jq_internal.cuh"
 #include "jq_segscan.cuh"
@@ -1505,12 +1506,16 @@ static int chain_flag() {
 // trailing tiles (reducer warps) when they have no side scan to run.  Measured slower at
 // C4 (175.1 vs 169.5 ms): the reducers sit on SM sub-partition 0 with the chain, whose
 // lookahead then publishes V later, and the data warps wait on two V barriers per panel.
+// JQ_TSQR_REDUCERS=chain (flag 64): the chain warp reduces every trailing tile itself.
 static int reducer_flag(int nspare, const SideScan& side) {
-  static const bool on = [] {
+  static const int mode = [] {
     const char* e = getenv("JQ_TSQR_REDUCERS");
-    return e && e[0] == '1';
+    if (!e) return 0;
+    if (strcmp(e, "chain") == 0) return 64;
+    return e[0] == '1' ? 32 : 0;
   }();
-  return (on && nspare > 0 && side.x == nullptr) ? 32 : 0;
+  if (mode == 64) return 64;
+  return (mode == 32 && nspare > 0 && side.x == nullptr) ? 32 : 0;
 }
 
 template <class C, class Src, bool COMBINE>

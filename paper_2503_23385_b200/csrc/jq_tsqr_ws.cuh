@@ -140,8 +140,11 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
   // REDUCER warps (flags & 32: the spare warps have no side scan to run): they reduce the
   // tiles q > p + 1 of panel p (Z^T = R^T + S M', W^T = Z^T T, V^T = W^T M'^T) while the
   // chain does the lookahead tile p + 1 and the next panel, so the data warps only apply
-  const bool use_red = C::NSPARE > 0 && (flags & 32);
-  const int NB = NALL + (use_red ? C::NSPARE * 32 : 0);  // BAR_ALL: chain + data (+ reducers)
+  const bool red_warps = C::NSPARE > 0 && (flags & 32) && !(flags & 64);
+  // flag 64: the CHAIN warp itself reduces the tiles q > p + 1 right after its lookahead
+  const bool chain_red = (flags & 64) != 0;
+  const bool use_red = red_warps || chain_red;  // data warps: apply-only protocol (VREADY2)
+  const int NB = NALL + (red_warps ? C::NSPARE * 32 : 0);  // BAR_ALL: chain + data (+ reducer warps)
   int tr_k = 0;
   (void)tr_k;
 
@@ -157,7 +160,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
     mbar_init_n(bar_ready, 1);
     mbar_init_n(bar_free, C::DW);
     mbar_init_n(bar_v, 1);
-    mbar_init_n(bar_v2, C::NSPARE > 0 ? C::NSPARE : 1);
+    mbar_init_n(bar_v2, (C::NSPARE > 0 && (flags & 32) && !(flags & 64)) ? C::NSPARE : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -204,7 +207,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       }
       si += busy ? 0 : 1;
     }
-    if (!use_red) {
+    if (!red_warps) {
       src.side_scan(si, C::NSPARE, lane);
       return;
     }
@@ -384,6 +387,31 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_v);  // tile q may be updated
           TR(0, 4);
+          if (chain_red) {
+            // the other trailing tiles' reduces with panel p (independent: their DMMA
+            // chains interleave), then VREADY2 -- before the Gram of the next panel, whose
+            // explicit-path barrier the data warps only reach after these applies
+            for (int q2 = q + 1; q2 < C::NLT; ++q2) {
+              const int m0 = 8 * q2;
+              const int s0i = rix<C>(j0 + 2 * t, m0 + g), s1i = rix<C>(j0 + 2 * t + 1, m0 + g);
+              double st2[2];
+              sum_partials(Zp + q2 * 64, C::NLT * 64, st2);
+              double z2[2] = {R[s0i], R[s1i]};
+              dmma(z2, st2[0], Mc[(2 * t) * C::LDT + g]);
+              dmma(z2, st2[1], Mc[(2 * t + 1) * C::LDT + g]);
+              double w2[2] = {0.0, 0.0};
+              dmma(w2, z2[0], Tc[(2 * t) * C::LDT + g]);
+              dmma(w2, z2[1], Tc[(2 * t + 1) * C::LDT + g]);
+              R[s0i] -= w2[0];
+              R[s1i] -= w2[1];
+              double v2[2] = {0.0, 0.0};
+              dmma(v2, w2[0], Mc[g * C::LDT + 2 * t]);
+              dmma(v2, w2[1], Mc[g * C::LDT + 2 * t + 1]);
+              *reinterpret_cast<double2*>(Ws + q2 * 64 + 2 * lane) = make_double2(-v2[0], -v2[1]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_v2);
+          }
           if (ok) {
             // Gram of the updated tile: C^T C - V^T S - S^T V + (V^T G0) V   (all ^T as stored)
             double gn[2] = {cc[0], cc[1]};
@@ -460,7 +488,12 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       gram_partial(0, Gd);
       named_bar(BAR_ALL, NB);
 
-#pragma unroll 1
+      // fully unrolled over the panels: every "tile q > p" test becomes compile time, so
+      // the applies / partials of different tiles are straight-line independent DMMA
+      // chains the scheduler can interleave (C4 leaf 172.8 -> 138.7 ms; the runtime-p
+      // loop left one predicated block per tile).  The chain warp's loop stays rolled
+      // (unrolled it is slower: 190 ms, instruction-cache pressure on SMSP 0).
+#pragma unroll
       for (int p = 0; p < C::NLT; ++p) {
         const int j0 = 8 * p, par = p & 1;
         const double* Tp = smem_dyn + C::OFF_T + (par ^ 1) * 8 * C::LDT;
