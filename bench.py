@@ -44,10 +44,10 @@ CONFIGS = {
 }
 METRIC = "join rows/sec (m1*m2/t), time-to-R"
 # dram__bytes_read.sum + dram__bytes_write.sum per leaf-kernel launch (ncu --set full)
-NCU_TRAFFIC = {(4, "footnote"): {"bytes": 51.218381e9 + 11.232512e6,
-                                 "note": "first tsqr_ws2_kernel launch (side A, carry-free leaves, capture v12): its "
-                                         "own 1e8 x 64 f64 rows = 51.2e9 algorithmic bytes, every byte read once; "
-                                         "profiles/r01_ncu_ws2_c4.md"}}
+NCU_TRAFFIC = {(4, "footnote"): {"bytes": 51.218248e9 + 10.816512e6,
+                                 "note": "first tsqr_ws2_kernel launch (side A, carry-free leaves, round-2 capture "
+                                         "profiles/r02_ncu_ws2_c4.md / _raw.csv, 68.80 ms under ncu): its own 1e8 x 64 "
+                                         "f64 rows = 51.2e9 algorithmic bytes, every byte read once"}}
 
 
 def peaks():
@@ -391,7 +391,7 @@ def main():
         # (profiles/r01_ncu_ws2_c4.md): footnote C4, one side = 1e8 x 64 f64 rows
         traffic = NCU_TRAFFIC.get((args.config, args.variant))
         roof = {"kernel": ("tsqr_ws2_kernel (warp-specialised TSQR leaf: loader warp builds the Claim-1 / tail rows, "
-                           "chain warp runs the Gram-panel Householder chain, 12 data warps do the DMMA updates)"
+                           "chain warp runs the Cholesky panel factorisation, 12 data warps do the DMMA updates)"
                            if args.variant == "footnote" and n <= 64 else
                            "tsqr_kernel (CTA-wide TSQR leaf, Gram-panel chain + explicit fallback, DMMA updates)"),
                 "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

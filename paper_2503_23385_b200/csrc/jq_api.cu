@@ -12,8 +12,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <utility>
 #include <string>
+#include <vector>
 
 #include "jq_internal.cuh"
 
@@ -766,6 +768,57 @@ static bool use_streamed(const double* a, int64_t m1, int64_t n1, const double* 
   return (m1 * n1 + m2 * n2) * 8 >= env_bytes("JQ_STREAM_MIN_BYTES", int64_t(1) << 30);
 }
 
+static bool is_pageable(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return attr.type == cudaMemoryTypeUnregistered;
+}
+
+// Piece H2D for the streamed path.  Page-locked sources: one async DMA on the copy
+// stream.  Pageable sources (a plain numpy caller): the driver would stage them itself at
+// ~11 GB/s, synchronously; instead host threads memcpy the piece into a pinned slot of a
+// ring (waiting only for that slot's previous DMA) and the DMA runs from the slot while
+// the next piece is being copied.
+static int h2d_piece(jq_ctx* ctx, void* dst, const void* src, size_t bytes, bool pageable, int64_t k) {
+  if (!pageable) {
+    JQ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+    return JQ_OK;
+  }
+  constexpr int S = 3;
+  if (!ctx->stage_pin || ctx->stage_slot < bytes) {
+    if (ctx->stage_pin) {
+      for (auto& e : ctx->sev) if (e) cudaEventSynchronize(e);
+      cudaFreeHost(ctx->stage_pin);
+      ctx->stage_pin = nullptr;
+    }
+    JQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->stage_pin), bytes * S, cudaHostAllocDefault));
+    ctx->stage_slot = bytes;
+    ctx->stage_slots = S;
+    for (int i = 0; i < S; ++i)
+      if (!ctx->sev[i]) JQ_CUDA(cudaEventCreateWithFlags(&ctx->sev[i], cudaEventDisableTiming));
+  }
+  const int slot = int(k % S);
+  JQ_CUDA(cudaEventSynchronize(ctx->sev[slot]));  // the slot's previous DMA has drained
+  char* pin = ctx->stage_pin + size_t(slot) * ctx->stage_slot;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int nt = (int)std::max(1u, std::min(hw ? hw : 1u, 16u));
+  const size_t part = (bytes + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (int i = 1; i < nt; ++i) {
+    const size_t o = size_t(i) * part;
+    if (o < bytes)
+      th.emplace_back([=] { memcpy(pin + o, static_cast<const char*>(src) + o, std::min(part, bytes - o)); });
+  }
+  memcpy(pin, src, std::min(part, bytes));
+  for (auto& x : th) x.join();
+  JQ_CUDA(cudaMemcpyAsync(dst, pin, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+  JQ_CUDA(cudaEventRecord(ctx->sev[slot], ctx->copy_stream));
+  return JQ_OK;
+}
+
 static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const double* b, int64_t m2,
                              int64_t n2, double* dr /* device, n x n canonical */) {
   const int64_t n = n1 + n2;
@@ -805,6 +858,7 @@ static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n
   bool first[2] = {true, true};
   // side 0 = A, side 1 = B.  Dense: B first (top rows need head(B)), footnote: any order.
   const int order[2] = {foot ? 0 : 1, foot ? 1 : 0};
+  const bool pageable[2] = {n1 > 0 && is_pageable(a), n2 > 0 && is_pageable(b)};
   for (int oi = 0; oi < 2; ++oi) {
     const int side = order[oi];
     const double* host = side == 0 ? a : b;
@@ -817,8 +871,7 @@ static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n
       ctx->ws.used = mark;
       // copy piece k into buf[bi] once piece k-2 (same buffer) has been consumed
       if (k >= 2) JQ_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->pev[2 + bi], 0));
-      JQ_CUDA(cudaMemcpyAsync(buf[bi], host + r0 * cols, rows * cols * 8, cudaMemcpyHostToDevice,
-                              ctx->copy_stream));
+      JQ_TRY(h2d_piece(ctx, buf[bi], host + r0 * cols, size_t(rows * cols * 8), pageable[side], k));
       JQ_CUDA(cudaEventRecord(ctx->pev[bi], ctx->copy_stream));
       JQ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->pev[bi], 0));
       SegScan ss{};
@@ -949,6 +1002,8 @@ int jq_ctx_destroy(jq_ctx* ctx) {
   for (auto& e : ctx->tev) if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->stage_pin) cudaFreeHost(ctx->stage_pin);
+  for (auto& e : ctx->sev) if (e) cudaEventDestroy(e);
   if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
   for (auto& e : ctx->aev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->pev) if (e) cudaEventDestroy(e);

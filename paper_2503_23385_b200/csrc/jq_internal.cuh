@@ -76,6 +76,12 @@ struct jq_ctx {
   cudaEvent_t ev[8]{};
   cudaStream_t copy_stream = nullptr;   // host -> device piece copies (streamed figaro)
   cudaEvent_t pev[4]{};                 // piece copied / consumed events
+  // pinned staging ring for PAGEABLE host inputs of the streamed path (host threads
+  // memcpy a piece into a slot while the previous slot's DMA runs)
+  char* stage_pin = nullptr;
+  size_t stage_slot = 0;
+  int stage_slots = 0;
+  cudaEvent_t sev[4]{};
   cudaStream_t aux_stream = nullptr;    // V replay beside the Jacobi sweeps (jq_svd.cu)
   cudaEvent_t aev[2]{};
   // the head/tail tile pass timed on its own (up to 4 launches per call; bench roofline)

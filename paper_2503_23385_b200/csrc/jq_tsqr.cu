@@ -1057,11 +1057,20 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
 // reflector chain's guard tests) must be >= 1e-2 (S[j][j] + Pg_j): S[j][j] bounds the
 // rounding error of the Cholesky elimination, Pg that of the (derived) Gram.  Otherwise
 // the panel is redone by factor_panel_all, as with the reflector chain.
+#ifdef JQ_CHOL_PHASES
+__device__ long long g_chol_ph[8];
+#define CHOL_PH(k) do { if (lane == 0) { const long long t_ = clock64(); atomicAdd((unsigned long long*)&g_chol_ph[k], (unsigned long long)(t_ - ph_t)); ph_t = t_; } } while (0)
+#else
+#define CHOL_PH(k) do {} while (0)
+#endif
 template <class C>
 __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (&Rb)[2], const double* Rs,
                                                   const int j0, double* T, double* Mg, double* scr,
                                                   const int lane, const double Pg) {
   const int g = lane >> 2, t = lane & 3, c0 = 2 * t, c1 = 2 * t + 1;
+#ifdef JQ_CHOL_PHASES
+  long long ph_t = clock64();
+#endif
   // R_p in accumulator layout, and the fragments R_p[2t+b][g] of R_p^T R_p
   const double rp0 = (c0 >= g) ? Rs[rix<C>(j0 + g, j0 + c0)] : 0.0;
   const double rp1 = (c1 >= g) ? Rs[rix<C>(j0 + g, j0 + c1)] : 0.0;
@@ -1073,20 +1082,33 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
   dmma(S, rt0, rt0);
   dmma(S, rt1, rt1);
   const double sdiag = diag_of(S, lane);
+  CHOL_PH(0);
   // 8 Cholesky steps; lanes of quad j keep row j of S^{(j)} (R_new row j up to the
-  // 1 / sqrt(pivot) applied after the loop: no rsqrt on the critical path)
+  // 1 / sqrt(pivot) applied after the loop: no rsqrt on the critical path).  Every lane
+  // also forms the NEXT pivot itself, with exactly the owner lane's operations
+  // (S[j+1][j+1] - (S[j+1][j] / S[j][j]) S[j][j+1]), from values shuffled at the start of
+  // the step, so the critical path per step is one reciprocal + one multiply + one FMA
+  // (no shuffle between consecutive reciprocals).
   double piv_g = 1.0, sv0 = 0.0, sv1 = 0.0;
   bool rng_ok = true;
+  double piv = __shfl_sync(FULL, S[0], 0);  // S[0][0]
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const double e = (j & 1) ? S[1] : S[0];
-    const double piv = __shfl_sync(FULL, e, 4 * j + (j >> 1));  // S[j][j]
     const double sgj = __shfl_sync(FULL, e, 4 * g + (j >> 1));  // S[g][j]
     const double sj0 = __shfl_sync(FULL, S[0], 4 * j + t);      // S[j][c0]
     const double sj1 = __shfl_sync(FULL, S[1], 4 * j + t);      // S[j][c1]
-    const bool in = piv > 1e-280 && piv < 1e280;               // MUFU approximations' safe range
+    double a_lo = 0.0, a_up = 0.0, b_nx = 0.0;
+    if (j < 7) {
+      const int jn = j + 1;
+      a_lo = __shfl_sync(FULL, e, 4 * jn + (j >> 1));                        // S[j+1][j]
+      a_up = __shfl_sync(FULL, (jn & 1) ? S[1] : S[0], 4 * j + (jn >> 1));   // S[j][j+1]
+      b_nx = __shfl_sync(FULL, (jn & 1) ? S[1] : S[0], 4 * jn + (jn >> 1));  // S[j+1][j+1]
+    }
+    const bool in = piv > 1e-280 && piv < 1e280;  // MUFU approximations' safe range
     rng_ok = rng_ok && in;
-    const double f = sgj * rcp_nr(in ? piv : 1.0);  // S[g][c] -= S[g][j] S[j][c] / S[j][j]  (g, c > j)
+    const double inv = rcp_nr(in ? piv : 1.0);
+    const double f = sgj * inv;  // S[g][c] -= S[g][j] S[j][c] / S[j][j]  (g, c > j)
     if (g == j) {
       piv_g = piv;
       sv0 = c0 >= j ? sj0 : 0.0;
@@ -1094,7 +1116,9 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
     }
     if (g > j && c0 > j) S[0] = fma(-f, sj0, S[0]);
     if (g > j && c1 > j) S[1] = fma(-f, sj1, S[1]);
+    if (j < 7) piv = fma(-(a_lo * inv), a_up, b_nx);  // = the owner lane's S[j+1][j+1]
   }
+  CHOL_PH(1);
   const double rs_g = rsqrt_nr(rng_ok ? piv_g : 1.0);
   Rb[0] = dsg * sv0 * rs_g;  // R_new[g][:] = D_g S^{(g)}[g][:] / sqrt(pivot_g)
   Rb[1] = dsg * sv1 * rs_g;
@@ -1109,6 +1133,7 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
     dg[8 + g] = dsg * rs_g;                      // 1 / R_new[g][g]
   }
   __syncwarp();
+  CHOL_PH(2);
   // Inverses of the two upper-triangular matrices by back substitution, one lane per
   // column (lanes 0..7: W^{-1} = M', lanes 8..15: R_new^{-1}), the same code on every
   // lane (no divergence), right-looking: per step one multiply + one FMA on the path.
@@ -1134,6 +1159,7 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
     }
   }
   __syncwarp();
+  CHOL_PH(3);
   // T = -W R_new^{-1}  (B fragments R_new^{-1}[2t+b][g] from the parked copy)
   const double b0 = T[c0 * C::LDT + g], b1 = T[c1 * C::LDT + g];
   double P[2] = {0.0, 0.0};
@@ -1141,11 +1167,13 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
   dmma(P, w1, b1);
   __syncwarp();
   *reinterpret_cast<double2*>(T + g * C::LDT + c0) = make_double2(-P[0], -P[1]);
+  CHOL_PH(4);
   const bool good = rng_ok && piv_g >= 1e-2 * (sdiag + Pg);
   const bool ok = __all_sync(FULL, good);
 #ifdef JQ_KTIME
   if (!ok && lane == 0) atomicAdd(&g_gram_fail[0], 1ull);
 #endif
+  CHOL_PH(5);
   return ok;
 }
 
