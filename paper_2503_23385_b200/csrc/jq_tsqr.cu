@@ -1534,6 +1534,15 @@ static int chain_flag() {
 // trailing tiles (reducer warps) when they have no side scan to run.  Measured slower at
 // C4 (175.1 vs 169.5 ms): the reducers sit on SM sub-partition 0 with the chain, whose
 // lookahead then publishes V later, and the data warps wait on two V barriers per panel.
+// JQ_TSQR_PROBE_NOPREP=1 (flag 128): the loader skips its transform -- WRONG results,
+// a timing probe of how much the loader's work slows the chain on its sub-partition.
+static int probe_flag() {
+  static const int f = [] {
+    const char* e = getenv("JQ_TSQR_PROBE_NOPREP");
+    return (e && e[0] == '1') ? 128 : 0;
+  }();
+  return f;
+}
 // JQ_TSQR_REDUCERS=chain (flag 64): the chain warp reduces every trailing tile itself.
 static int reducer_flag(int nspare, const SideScan& side) {
   static const int mode = [] {
@@ -1721,7 +1730,8 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t 
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::SMEM));
   kern<<<(int)ctas, CS::THREADS, CS::SMEM, ctx->stream>>>(src, rows_per_cta, vrows, a,
                                                           (use_tma ? 1 : 0) | (explicit_panels ? 2 : 0) | debug_flags |
-                                                              chain_flag() | reducer_flag(CS::NSPARE, src.side_job()));
+                                                              chain_flag() | reducer_flag(CS::NSPARE, src.side_job()) |
+                                                              probe_flag());
   JQ_CHECK_LAUNCH(ctx);
   if (defer) {
     *defer = LeafSet{a, b, ctas, C::NP, n, rows_per_cta};

@@ -310,7 +310,7 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
         TR(2, 2);
       }
       if (C::NLOAD == 1) {
-        src.template prep_warp<C>(raw, S, scratch, r0, nr, lane);
+        if (!(flags & 128)) src.template prep_warp<C>(raw, S, scratch, r0, nr, lane);  // 128: timing probe only
       } else {
         named_bar(BAR_LOAD, C::NLOAD * 32);  // raw rows of the chunk in shared memory
         if (li == 0) TR(2, 4);
