@@ -352,7 +352,10 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     ng = hn[0];
   }
   stage_event(ctx, 1);
-  const int64_t cap = keyed ? gr.cap : 1;
+  // per-group arrays (scan totals: memset and written per group) sized by the ACTUAL
+  // group count, known on the host here -- not by the min(m1, m2) capacity of the
+  // grouping tables (at C3 that was 2 x 2.56 GB of memset per call)
+  const int64_t cap = keyed ? std::max<int64_t>(ng, 1) : 1;
   if (!keyed && n1 > 0 && n2 > 0 && carry_free_leaves()) return figaro_r_footnote_blocks(ctx, a, m1, n1, b, m2, n2, r_out);
   // A's scan in full; the tile pass of B's scan (the HBM-heavy part) runs on the spare
   // warps of A's TSQR leaf (FigaroArgs::side), B's carries right after it
@@ -676,15 +679,16 @@ static int figaro_r_wide(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, c
   ctx->timing.tsqr_ctas = 0;
   stage_event(ctx, 0);
   Groups gr;
-  int64_t total = m1 + m2 - 1;
-  const int64_t cap = keyed ? std::max<int64_t>(1, std::min(m1, m2)) : 1;
+  int64_t total = m1 + m2 - 1, ng = 1;
   if (keyed) {
     JQ_TRY(group_keys_dev(ctx, ka, m1, kb, m2, &gr));
     int64_t hn[2];
     JQ_CUDA(cudaMemcpyAsync(hn, gr.d_n, 16, cudaMemcpyDeviceToHost, ctx->stream));
     JQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    ng = hn[0];
     total = hn[1];
   }
+  const int64_t cap = keyed ? std::max<int64_t>(ng, 1) : 1;
   stage_event(ctx, 1);
   ctx->timing.reduced_rows = total;
   if (total <= 0) {  // empty join: R = 0
@@ -710,10 +714,17 @@ static int figaro_r_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, co
   ctx->timing.reduced_rows = 0;
   stage_event(ctx, 0);
   Groups gr;
-  if (keyed) JQ_TRY(group_keys_dev(ctx, ka, m1, kb, m2, &gr));
+  int64_t ng = 1;
+  if (keyed) {
+    JQ_TRY(group_keys_dev(ctx, ka, m1, kb, m2, &gr));
+    int64_t hn[2];  // the group count sizes the per-group scan totals (see the footnote path)
+    JQ_CUDA(cudaMemcpyAsync(hn, gr.d_n, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    JQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    ng = hn[0];
+  }
   stage_event(ctx, 1);
   SegScan ss;
-  const int64_t cap = keyed ? gr.cap : 1;
+  const int64_t cap = keyed ? std::max<int64_t>(ng, 1) : 1;
   if (n2 > 0)
     JQ_TRY(segscan_dev(ctx, b, m2, n2, keyed ? gr.gid_b : nullptr, keyed ? gr.b_start : nullptr,
                        keyed ? gr.b_count : nullptr, keyed ? gr.d_n : nullptr, cap, &ss));

@@ -5,8 +5,9 @@
 // (`group_keys`: unique -> intersect1d -> cumsum) is the parity target.
 //
 // Pipeline (all integer, hence deterministic):
-//   sortedness check -> run heads -> exclusive scan = run id per row ->
-//   run tables (start, key) -> binary-search match of A runs in B runs ->
+//   per 2048-key tile (both sides in one launch): run heads + sortedness check ->
+//   tile offsets (one CTA) -> run tables (start, key) + run id per row (one launch) ->
+//   binary-search match of A runs in B runs ->
 //   scan of match flags = group ids in ascending key order -> group tables,
 //   red_off = exclusive scan of (a_count + b_count - 1) -> per-row group ids.
 // Tables that arrive unsorted are sorted first, opt-in, by the GPU stable LSD radix
@@ -130,27 +131,6 @@ __global__ void check_sorted_kernel(const int64_t* __restrict__ k, int64_t n, in
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, bit);
 }
 
-__global__ void run_head_kernel(const int64_t* __restrict__ k, int64_t n, int64_t* __restrict__ head) {
-  GRID_STRIDE(i, n) head[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
-}
-
-// runid[i] = (exclusive scan of heads)[i] + head[i] - 1  -> written in place of the scan
-__global__ void run_tables_kernel(const int64_t* __restrict__ k, int64_t n, const int64_t* __restrict__ head,
-                                  int64_t* __restrict__ scan, int64_t* __restrict__ run_start,
-                                  int64_t* __restrict__ run_key) {
-  GRID_STRIDE(i, n) {
-    if (head[i]) {
-      const int64_t u = scan[i];
-      run_start[u] = i;
-      run_key[u] = k[i];
-    }
-  }
-}
-
-__global__ void runid_kernel(const int64_t* __restrict__ head, int64_t n, int64_t* __restrict__ scan) {
-  GRID_STRIDE(i, n) scan[i] = scan[i] + head[i] - 1;  // run index of row i
-}
-
 // match A runs against B runs (both ascending): match[u] = index of equal key in B or -1
 __global__ void match_kernel(const int64_t* __restrict__ ka_run, const int64_t* __restrict__ nra_p,
                              const int64_t* __restrict__ kb_run, const int64_t* __restrict__ nrb_p,
@@ -196,27 +176,127 @@ __global__ void group_tables_kernel(const int64_t* __restrict__ match, const int
 
 __global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) { GRID_STRIDE(i, n) p[i] = v; }
 
-__global__ void row_gid_kernel(const int64_t* __restrict__ runid, int64_t n, const int32_t* __restrict__ r_to_g,
-                               int32_t* __restrict__ gid) {
-  GRID_STRIDE(i, n) gid[i] = r_to_g[runid[i]];
-}
-
-__global__ void counts_kernel(const int64_t* __restrict__ head_scan_a, int64_t m1,
-                              const int64_t* __restrict__ head_a, const int64_t* __restrict__ head_scan_b,
-                              int64_t m2, const int64_t* __restrict__ head_b, int64_t* nra, int64_t* nrb) {
-  // number of runs = runid[last] + 1 (runid written in place of the scan)
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    nra[0] = m1 ? head_scan_a[m1 - 1] + 1 : 0;
-    nrb[0] = m2 ? head_scan_b[m2 - 1] + 1 : 0;
-  }
-}
-
 __global__ void finish_counts_kernel(const int64_t* __restrict__ gscan, const int64_t* __restrict__ nra,
                                      const int64_t* __restrict__ red_off, int64_t* d_n) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     const int64_t g = gscan[nra[0]];  // total matched = scan at [len]
     d_n[0] = g;
     d_n[1] = red_off[g];
+  }
+}
+
+// ---- fused run detection, both sides in one launch each (round 2: 14 -> 3 launches)
+// Tile t of the concatenated key streams (A tiles, then B tiles; SCAN_TILE keys each).
+struct RunSides {
+  const int64_t* k[2];
+  int64_t m[2];
+  int64_t tiles0;      // tiles of side A
+  int64_t* cnt;        // [tilesA + tilesB] run heads per tile -> exclusive offsets (in place)
+  int64_t* rs[2];      // run start row
+  int64_t* rk[2];      // run key
+  int32_t* runid[2];   // run index of every row
+  int32_t* r_to_g_b;   // side B runs -> group (initialised to -1 here)
+  int* flags;
+};
+__device__ __forceinline__ void run_tile(const RunSides& rs, int64_t& t, int& side, int64_t& i0, int64_t& i1) {
+  side = t < rs.tiles0 ? 0 : 1;
+  if (side) t -= rs.tiles0;
+  i0 = t * SCAN_TILE;
+  i1 = min(rs.m[side], i0 + SCAN_TILE);
+}
+// heads per tile + the sortedness check (unsorted keys raise)
+__global__ void __launch_bounds__(SCAN_THREADS) run_count_kernel(RunSides rs) {
+  __shared__ int64_t ws[SCAN_THREADS / 32];
+  __shared__ int64_t tot;
+  int64_t t = blockIdx.x, i0, i1;
+  int side;
+  run_tile(rs, t, side, i0, i1);
+  const int64_t* k = rs.k[side];
+  int64_t h = 0;
+  int bad = 0;
+  const int64_t b = i0 + threadIdx.x * SCAN_ITEMS;
+#pragma unroll
+  for (int u = 0; u < SCAN_ITEMS; ++u) {
+    const int64_t i = b + u;
+    if (i < i1) {
+      const int64_t ki = __ldg(k + i);
+      if (i == 0) h += 1;
+      else {
+        const int64_t kp = __ldg(k + i - 1);
+        h += ki != kp;
+        bad |= kp > ki;
+      }
+    }
+  }
+  block_exclusive_scan(h, ws, &tot);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(rs.flags, side ? FLAG_UNSORTED_B : FLAG_UNSORTED_A);
+  if (threadIdx.x == 0) rs.cnt[blockIdx.x] = tot;
+}
+// exclusive offsets of the per-tile counts, per side (one CTA); runs of A / B -> nr[0..1]
+__global__ void __launch_bounds__(SCAN_THREADS) run_offsets_kernel(int64_t* cnt, int64_t tiles0, int64_t tiles1,
+                                                                   int64_t* nr) {
+  __shared__ int64_t ws[SCAN_THREADS / 32];
+  __shared__ int64_t tot;
+  for (int side = 0; side < 2; ++side) {
+    int64_t* c = cnt + (side ? tiles0 : 0);
+    const int64_t nt = side ? tiles1 : tiles0;
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < nt; b0 += SCAN_THREADS) {
+      const int64_t i = b0 + threadIdx.x;
+      const int64_t v = i < nt ? c[i] : 0;
+      const int64_t ex = block_exclusive_scan(v, ws, &tot);
+      if (i < nt) c[i] = carry + ex;
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) nr[side] = carry;
+  }
+}
+// run tables (start row, key) at the heads, run id of every row; B's run -> group map = -1
+__global__ void __launch_bounds__(SCAN_THREADS) run_tables_fused_kernel(RunSides rs) {
+  __shared__ int64_t ws[SCAN_THREADS / 32];
+  __shared__ int64_t tot;
+  int64_t t = blockIdx.x, i0, i1;
+  int side;
+  run_tile(rs, t, side, i0, i1);
+  const int64_t* k = rs.k[side];
+  const int64_t b = i0 + threadIdx.x * SCAN_ITEMS;
+  int64_t key[SCAN_ITEMS];
+  int hd[SCAN_ITEMS];
+  int64_t h = 0;
+#pragma unroll
+  for (int u = 0; u < SCAN_ITEMS; ++u) {
+    const int64_t i = b + u;
+    hd[u] = 0;
+    key[u] = 0;
+    if (i < i1) {
+      key[u] = __ldg(k + i);
+      hd[u] = (i == 0 || __ldg(k + i - 1) != key[u]) ? 1 : 0;
+      h += hd[u];
+    }
+  }
+  int64_t run = rs.cnt[blockIdx.x] + block_exclusive_scan(h, ws, &tot);  // heads before this thread
+#pragma unroll
+  for (int u = 0; u < SCAN_ITEMS; ++u) {
+    const int64_t i = b + u;
+    if (i < i1) {
+      if (hd[u]) {
+        rs.rs[side][run] = i;
+        rs.rk[side][run] = key[u];
+        if (side) rs.r_to_g_b[run] = -1;
+        ++run;
+      }
+      rs.runid[side][i] = (int32_t)(run - 1);
+    }
+  }
+}
+
+__global__ void row_gid2_kernel(const int32_t* __restrict__ runid_a, int64_t m1, const int32_t* __restrict__ ra_to_g,
+                                int32_t* __restrict__ gid_a, const int32_t* __restrict__ runid_b, int64_t m2,
+                                const int32_t* __restrict__ rb_to_g, int32_t* __restrict__ gid_b) {
+  GRID_STRIDE(i, m1 + m2) {
+    if (i < m1) gid_a[i] = ra_to_g[runid_a[i]];
+    else gid_b[i - m1] = rb_to_g[runid_b[i - m1]];
   }
 }
 
@@ -239,12 +319,11 @@ size_t group_ws_bytes(int64_t m1, int64_t m2) {
 int group_keys_dev(jq_ctx* ctx, const int64_t* ka, int64_t m1, const int64_t* kb, int64_t m2, Groups* g) {
   const int64_t cap = std::max<int64_t>(1, std::min(m1, m2));
   const int64_t M1 = std::max<int64_t>(1, m1), M2 = std::max<int64_t>(1, m2);
-  int64_t* head_a = ws_alloc<int64_t>(ctx, M1 + 1);
-  int64_t* scan_a = ws_alloc<int64_t>(ctx, M1 + 1);
+  int32_t* runid_a = ws_alloc<int32_t>(ctx, M1);
   int64_t* rs_a = ws_alloc<int64_t>(ctx, M1);
   int64_t* rk_a = ws_alloc<int64_t>(ctx, M1);
-  int64_t* head_b = ws_alloc<int64_t>(ctx, M2 + 1);
-  int64_t* scan_b = ws_alloc<int64_t>(ctx, M2 + 1);
+  int32_t* runid_b = ws_alloc<int32_t>(ctx, M2);
+  int64_t* tile_cnt = ws_alloc<int64_t>(ctx, cdiv(M1, SCAN_TILE) + cdiv(M2, SCAN_TILE) + 2);
   int64_t* rs_b = ws_alloc<int64_t>(ctx, M2);
   int64_t* rk_b = ws_alloc<int64_t>(ctx, M2);
   int64_t* match = ws_alloc<int64_t>(ctx, M1);
@@ -269,43 +348,44 @@ int group_keys_dev(jq_ctx* ctx, const int64_t* ka, int64_t m1, const int64_t* kb
   int64_t* nrb = counters + 3;
   JQ_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(int64_t), ctx->stream));
 
-  if (m1 > 1) {
-    check_sorted_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(ka, m1, FLAG_UNSORTED_A, ctx->d_flags);
-    JQ_CHECK_LAUNCH(ctx);
-  }
-  if (m2 > 1) {
-    check_sorted_kernel<<<gridn(m2), 256, 0, ctx->stream>>>(kb, m2, FLAG_UNSORTED_B, ctx->d_flags);
-    JQ_CHECK_LAUNCH(ctx);
-  }
   if (m1 == 0 || m2 == 0) {
+    if (m1 > 1) {
+      check_sorted_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(ka, m1, FLAG_UNSORTED_A, ctx->d_flags);
+      JQ_CHECK_LAUNCH(ctx);
+    }
+    if (m2 > 1) {
+      check_sorted_kernel<<<gridn(m2), 256, 0, ctx->stream>>>(kb, m2, FLAG_UNSORTED_B, ctx->d_flags);
+      JQ_CHECK_LAUNCH(ctx);
+    }
     JQ_CUDA(cudaMemsetAsync(g->red_off, 0, 8, ctx->stream));
     if (m1) { fill_i32_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(g->gid_a, m1, -1); JQ_CHECK_LAUNCH(ctx); }
     if (m2) { fill_i32_kernel<<<gridn(m2), 256, 0, ctx->stream>>>(g->gid_b, m2, -1); JQ_CHECK_LAUNCH(ctx); }
     return JQ_OK;
   }
-  // runs of each side
-  run_head_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(ka, m1, head_a);
+  if (m1 >= (int64_t(1) << 31) || m2 >= (int64_t(1) << 31))
+    return fail(JQ_E_INVALID, "grouping supports fewer than 2^31 rows per table");
+  // runs of both sides: heads per tile (+ sortedness), tile offsets, run tables + run ids
+  RunSides rsd;
+  rsd.k[0] = ka; rsd.k[1] = kb;
+  rsd.m[0] = m1; rsd.m[1] = m2;
+  const int64_t ta = cdiv(m1, SCAN_TILE), tb = cdiv(m2, SCAN_TILE);
+  rsd.tiles0 = ta;
+  rsd.cnt = tile_cnt;
+  rsd.rs[0] = rs_a; rsd.rs[1] = rs_b;
+  rsd.rk[0] = rk_a; rsd.rk[1] = rk_b;
+  rsd.runid[0] = runid_a; rsd.runid[1] = runid_b;
+  rsd.r_to_g_b = rb_to_g;
+  rsd.flags = ctx->d_flags;
+  run_count_kernel<<<(unsigned)(ta + tb), SCAN_THREADS, 0, ctx->stream>>>(rsd);
   JQ_CHECK_LAUNCH(ctx);
-  JQ_TRY(scan_i64_dev(ctx, head_a, m1, nullptr, scan_a));
-  run_tables_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(ka, m1, head_a, scan_a, rs_a, rk_a);
+  run_offsets_kernel<<<1, SCAN_THREADS, 0, ctx->stream>>>(tile_cnt, ta, tb, nra);  // nra, nrb = nra + 1
   JQ_CHECK_LAUNCH(ctx);
-  runid_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(head_a, m1, scan_a);
-  JQ_CHECK_LAUNCH(ctx);
-  run_head_kernel<<<gridn(m2), 256, 0, ctx->stream>>>(kb, m2, head_b);
-  JQ_CHECK_LAUNCH(ctx);
-  JQ_TRY(scan_i64_dev(ctx, head_b, m2, nullptr, scan_b));
-  run_tables_kernel<<<gridn(m2), 256, 0, ctx->stream>>>(kb, m2, head_b, scan_b, rs_b, rk_b);
-  JQ_CHECK_LAUNCH(ctx);
-  runid_kernel<<<gridn(m2), 256, 0, ctx->stream>>>(head_b, m2, scan_b);
-  JQ_CHECK_LAUNCH(ctx);
-  counts_kernel<<<1, 32, 0, ctx->stream>>>(scan_a, m1, head_a, scan_b, m2, head_b, nra, nrb);
+  run_tables_fused_kernel<<<(unsigned)(ta + tb), SCAN_THREADS, 0, ctx->stream>>>(rsd);
   JQ_CHECK_LAUNCH(ctx);
   // intersect
   match_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(rk_a, nra, rk_b, nrb, match, mflag);
   JQ_CHECK_LAUNCH(ctx);
   JQ_TRY(scan_i64_dev(ctx, mflag, m1, nra, gidx));
-  fill_i32_kernel<<<gridn(m2), 256, 0, ctx->stream>>>(rb_to_g, m2, -1);
-  JQ_CHECK_LAUNCH(ctx);
   group_tables_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(match, gidx, nra, m1, rs_a, rk_a, nrb, m2, rs_b,
                                                           g->keys, g->a_start, g->a_count, g->b_start,
                                                           g->b_count, rowcnt, ra_to_g, rb_to_g);
@@ -317,9 +397,8 @@ int group_keys_dev(jq_ctx* ctx, const int64_t* ka, int64_t m1, const int64_t* kb
   JQ_TRY(scan_i64_dev(ctx, rowcnt, cap, ng_dev, g->red_off));
   finish_counts_kernel<<<1, 32, 0, ctx->stream>>>(gidx, nra, g->red_off, g->d_n);
   JQ_CHECK_LAUNCH(ctx);
-  row_gid_kernel<<<gridn(m1), 256, 0, ctx->stream>>>(scan_a, m1, ra_to_g, g->gid_a);
-  JQ_CHECK_LAUNCH(ctx);
-  row_gid_kernel<<<gridn(m2), 256, 0, ctx->stream>>>(scan_b, m2, rb_to_g, g->gid_b);
+  row_gid2_kernel<<<gridn(m1 + m2), 256, 0, ctx->stream>>>(runid_a, m1, ra_to_g, g->gid_a, runid_b, m2, rb_to_g,
+                                                          g->gid_b);
   JQ_CHECK_LAUNCH(ctx);
   return JQ_OK;
 }

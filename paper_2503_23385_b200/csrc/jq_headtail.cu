@@ -531,7 +531,8 @@ extern "C" int jq_reduce(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, c
   JQ_TRY(stage_in(ctx, a, m1 * n1, &da));
   JQ_TRY(stage_in(ctx, b, m2 * n2, &db));
   JQ_TRY(stage_out(ctx, out, total_rows * n, &dout));
-  JQ_TRY(reduce_emit_dev(ctx, da, m1, n1, db, m2, n2, keyed ? &gr : nullptr, cap, total_rows, dout));
+  JQ_TRY(reduce_emit_dev(ctx, da, m1, n1, db, m2, n2, keyed ? &gr : nullptr, keyed ? std::max<int64_t>(ng, 1) : 1,
+                         total_rows, dout));
   JQ_TRY(copy_out(ctx, out, (const double*)dout, total_rows * n));
   return sync_and_check_flags(ctx);
 }
