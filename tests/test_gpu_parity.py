@@ -494,3 +494,29 @@ def test_figaro_r_mixed_gram_and_explicit_panels(P, variant, keys):
     check_r(r, O.canonicalize(O.householder_r_lapack(red)))
     g = O.gram(red)
     assert np.abs(r.T @ r - g).max() <= 1e-12 * np.abs(g).max()
+
+
+@pytest.mark.parametrize("scale", [1e-150, 1e-60, 1e-8, 1e8, 1e60, 1e150])
+def test_extreme_scales_fall_back_correctly(P, scale):
+    """Data scaled so that the Cholesky panel's minors (~ S^8) leave the MUFU range or
+    overflow: the guard must route those panels to the reflector chain / explicit path,
+    and R must still match LAPACK relatively (SPEC.md:250-258 has no scale limit)."""
+    rng = np.random.default_rng(int(abs(np.log10(scale))))
+    m = rng.random((20_000, 24)) * scale
+    r = np.asarray(P.canonicalize(P.householder_r(m)))
+    r_ref = O.canonicalize(O.householder_r_lapack(m))
+    assert np.all(np.isfinite(r))
+    assert rel_fro(np.abs(r), np.abs(r_ref)) <= 1e-10
+    a, b = rng.random((5000, 10)) * scale, rng.random((4000, 12)) * scale
+    P.set_variant("footnote")
+    try:
+        rf = np.asarray(P.figaro_r(P.Table(a), P.Table(b)))
+    finally:
+        P.set_variant("dense")
+    g = O.factorised_gram(O.Table(a), O.Table(b))
+    rg = O.gram_r(g) if scale < 1e100 and scale > 1e-100 else None
+    if rg is not None:
+        assert rel_fro(np.abs(rf), np.abs(rg)) <= 1e-10
+    else:  # the Gram itself over/underflows in float64: compare with LAPACK on the reduced matrix
+        red = O.reduce_cartesian(a, b).matrix
+        assert rel_fro(np.abs(rf), np.abs(O.canonicalize(O.householder_r_lapack(red)))) <= 1e-10
