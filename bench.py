@@ -244,9 +244,10 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-rows", type=int, default=1_000_000)
-    ap.add_argument("--variant", default="footnote", choices=["footnote", "dense"],
+    ap.add_argument("--variant", default="auto", choices=["auto", "footnote", "dense"],
                     help="figaro reduction timed as the headline (the other one is timed too and "
-                         "reported under 'variants')")
+                         "reported under 'variants'); auto = what the library's default picks for "
+                         "this shape (footnote from (m1 + m2)(n1 + n2) > 1e8 reduced elements)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-memory e2e step")
@@ -254,6 +255,9 @@ def main():
                     help="(testing) run the multi-GPU code path even with one rank (torchrun, 1 process)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.variant == "auto":  # the library's "auto" rule (jq_api.cu use_footnote)
+        c = CONFIGS[args.config]
+        args.variant = "footnote" if 2.0 * c["m"] * 2 * c["n"] > 1e8 else "dense"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     sharded_path = world > 1 or args.force_sharded
