@@ -1083,54 +1083,45 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
   dmma(S, rt1, rt1);
   const double sdiag = diag_of(S, lane);
   CHOL_PH(0);
-  // 8 elimination steps in fraction-free (Bareiss) form:
-  //   M^{(k+1)}[g][c] = (p_k M[g][c] - M[g][k] M[k][c]) / p_{k-1},   p_k = M^{(k)}[k][k]
-  // (p_k = the leading (k+1) x (k+1) minor of S; the Cholesky pivot is d_k = p_k / p_{k-1}
-  // and S^{(k)}[k][c] = M^{(k)}[k][c] / p_{k-1}).  The only reciprocal, 1 / p_k, is needed
-  // one step later, so it leaves the critical path: per step the next minor costs one FMA
-  // and one multiply after the current one (every lane forms it from values shuffled at
-  // the start of the step, with the owner lane's exact operations).  Lanes of quad j keep
-  // row j of M^{(j)}; R_new's scaling happens after the loop, in parallel.
-  double pk_g = 1.0, pkm1_g = 1.0, sv0 = 0.0, sv1 = 0.0;
+  // 8 Cholesky steps; lanes of quad j keep row j of S^{(j)} (R_new row j up to the
+  // 1 / sqrt(pivot) applied after the loop: no rsqrt on the critical path).  Every lane
+  // also forms the NEXT pivot itself, with exactly the owner lane's operations
+  // (S[j+1][j+1] - (S[j+1][j] / S[j][j]) S[j][j+1]), from values shuffled at the start of
+  // the step, so the critical path per step is one reciprocal + one multiply + one FMA
+  // (no shuffle between consecutive reciprocals).
+  double piv_g = 1.0, sv0 = 0.0, sv1 = 0.0;
   bool rng_ok = true;
-  double pm = __shfl_sync(FULL, S[0], 0);  // p_0 = S[0][0]
-  double ipp = 1.0, pp = 1.0;              // 1 / p_{k-1}, p_{k-1}
+  double piv = __shfl_sync(FULL, S[0], 0);  // S[0][0]
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const double e = (j & 1) ? S[1] : S[0];
-    const double sgj = __shfl_sync(FULL, e, 4 * g + (j >> 1));  // M[g][j]
-    const double sj0 = __shfl_sync(FULL, S[0], 4 * j + t);      // M[j][c0]
-    const double sj1 = __shfl_sync(FULL, S[1], 4 * j + t);      // M[j][c1]
+    const double sgj = __shfl_sync(FULL, e, 4 * g + (j >> 1));  // S[g][j]
+    const double sj0 = __shfl_sync(FULL, S[0], 4 * j + t);      // S[j][c0]
+    const double sj1 = __shfl_sync(FULL, S[1], 4 * j + t);      // S[j][c1]
     double a_lo = 0.0, a_up = 0.0, b_nx = 0.0;
     if (j < 7) {
       const int jn = j + 1;
-      a_lo = __shfl_sync(FULL, e, 4 * jn + (j >> 1));                        // M[j+1][j]
-      a_up = __shfl_sync(FULL, (jn & 1) ? S[1] : S[0], 4 * j + (jn >> 1));   // M[j][j+1]
-      b_nx = __shfl_sync(FULL, (jn & 1) ? S[1] : S[0], 4 * jn + (jn >> 1));  // M[j+1][j+1]
+      a_lo = __shfl_sync(FULL, e, 4 * jn + (j >> 1));                        // S[j+1][j]
+      a_up = __shfl_sync(FULL, (jn & 1) ? S[1] : S[0], 4 * j + (jn >> 1));   // S[j][j+1]
+      b_nx = __shfl_sync(FULL, (jn & 1) ? S[1] : S[0], 4 * jn + (jn >> 1));  // S[j+1][j+1]
     }
-    const bool in = pm > 1e-280 && pm < 1e280;  // minors in the MUFU approximations' range
+    const bool in = piv > 1e-280 && piv < 1e280;  // MUFU approximations' safe range
     rng_ok = rng_ok && in;
+    const double inv = rcp_nr(in ? piv : 1.0);
+    const double f = sgj * inv;  // S[g][c] -= S[g][j] S[j][c] / S[j][j]  (g, c > j)
     if (g == j) {
-      pk_g = pm;
-      pkm1_g = pp;
+      piv_g = piv;
       sv0 = c0 >= j ? sj0 : 0.0;
       sv1 = c1 >= j ? sj1 : 0.0;
     }
-    if (g > j && c0 > j) S[0] = fma(pm, S[0], -(sgj * sj0)) * ipp;
-    if (g > j && c1 > j) S[1] = fma(pm, S[1], -(sgj * sj1)) * ipp;
-    const double pn = fma(pm, b_nx, -(a_lo * a_up)) * ipp;  // = the owner lane's M^{(j+1)}[j+1][j+1]
-    ipp = rcp_nr(in ? pm : 1.0);
-    pp = pm;
-    pm = pn;
+    if (g > j && c0 > j) S[0] = fma(-f, sj0, S[0]);
+    if (g > j && c1 > j) S[1] = fma(-f, sj1, S[1]);
+    if (j < 7) piv = fma(-(a_lo * inv), a_up, b_nx);  // = the owner lane's S[j+1][j+1]
   }
   CHOL_PH(1);
-  // true pivot d_g = p_g / p_{g-1}; R_new[g][:] = D_g M^{(g)}[g][:] / (p_{g-1} sqrt(d_g))
-  const double ipkm1 = rcp_nr(pkm1_g);
-  const double piv_g = pk_g * ipkm1;
-  rng_ok = rng_ok && piv_g > 1e-280 && piv_g < 1e280;
   const double rs_g = rsqrt_nr(rng_ok ? piv_g : 1.0);
-  Rb[0] = dsg * (sv0 * ipkm1) * rs_g;
-  Rb[1] = dsg * (sv1 * ipkm1) * rs_g;
+  Rb[0] = dsg * sv0 * rs_g;  // R_new[g][:] = D_g S^{(g)}[g][:] / sqrt(pivot_g)
+  Rb[1] = dsg * sv1 * rs_g;
   const double w0 = rp0 - Rb[0], w1 = rp1 - Rb[1];
   // W and R_new in natural layout (scratch), their diagonals' reciprocals
   double* Un = scr;                 // [2][8][LDT]: W, R_new
