@@ -99,7 +99,7 @@ struct Cfg {
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(KW % 8 == 0, "whole row tiles per warp");
-  static_assert(OFF_S - OFF_U >= 16 * LDT + 16, "factor_panel_chol scratch (U .. P)");
+  static_assert(OFF_S - OFF_U >= 16 * LDT + 16 + 32, "factor_panel_chol scratch (U .. P)");
 };
 
 // R element (r, c), c >= 8 * (r / 8), in the packed (smem) or dense (global) layout
@@ -1053,10 +1053,12 @@ __device__ __forceinline__ bool factor_panel_gram(double (&G)[2], double (&Rb)[2
 // correction) between two shuffles -- versus rsqrt then rcp plus the T column in the
 // reflector chain -- then W^{-1} and R_new^{-1} by back substitution (one lane per
 // column, operands in shared memory `scr`: >= 16 LDT + 16 doubles, the explicit path's
-// U / taus / scales / partials, idle while the chain runs) and one 8 x 8 DMMA product.  Guard: every pivot (= R_new[j][j]^2, the quantity the
-// reflector chain's guard tests) must be >= 1e-2 (S[j][j] + Pg_j): S[j][j] bounds the
-// rounding error of the Cholesky elimination, Pg that of the (derived) Gram.  Otherwise
-// the panel is redone by factor_panel_all, as with the reflector chain.
+// U / taus / scales / partials, idle while the chain runs) and one 8 x 8 DMMA product.
+// Guard (the reflector chain's, made slightly stricter): pivot_c (= R_new[c][c]^2 =
+// alpha_c^2 + |x_c'|^2) >= 1e-2 (S[c][c] + P_c), with P_c = sum_k M[k][c]^2 Pg_k bounding the
+// rounding error of |x_c'|^2 from the (derived) Gram's -- M = M' diag(W) read off the
+// back substitution -- and S[c][c] >= alpha_c^2 that of the elimination itself.  Otherwise
+// the panel goes to the reflector chain, then the explicit path.
 #ifdef JQ_CHOL_PHASES
 __device__ long long g_chol_ph[8];
 #define CHOL_PH(k) do { if (lane == 0) { const long long t_ = clock64(); atomicAdd((unsigned long long*)&g_chol_ph[k], (unsigned long long)(t_ - ph_t)); ph_t = t_; } } while (0)
@@ -1128,15 +1130,22 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
   double* dg = scr + 16 * C::LDT;   // [2][8]: 1 / W[i][i], 1 / R_new[i][i]
   *reinterpret_cast<double2*>(Un + g * C::LDT + c0) = make_double2(w0, w1);
   *reinterpret_cast<double2*>(Un + (8 + g) * C::LDT + c0) = make_double2(Rb[0], Rb[1]);
+  double* gq = scr + 16 * C::LDT + 16;  // [4][8]: pivot, W[g][g]^2, S[g][g], Pg of row g (guard)
   if (t == 0) {
-    dg[g] = rcp_nr(alpha - dsg * piv_g * rs_g);  // W[g][g] = alpha - R_new[g][g]
+    const double wgg = alpha - dsg * piv_g * rs_g;  // W[g][g] = alpha - R_new[g][g]
+    dg[g] = rcp_nr(wgg);
     dg[8 + g] = dsg * rs_g;                      // 1 / R_new[g][g]
+    gq[g] = piv_g;
+    gq[8 + g] = wgg * wgg;
+    gq[16 + g] = sdiag;
+    gq[24 + g] = Pg;
   }
   __syncwarp();
   CHOL_PH(2);
   // Inverses of the two upper-triangular matrices by back substitution, one lane per
   // column (lanes 0..7: W^{-1} = M', lanes 8..15: R_new^{-1}), the same code on every
   // lane (no divergence), right-looking: per step one multiply + one FMA on the path.
+  bool good_c = true;
   {
     const int m = (lane >> 3) & 1, c = lane & 7;
     const double* U = Un + m * 8 * C::LDT;
@@ -1157,6 +1166,20 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
 #pragma unroll
       for (int i = 0; i < 8; ++i) out[i * C::LDT + c] = x[i];
     }
+    // Guard, tracking nothing in the elimination: the chunk columns' combination of
+    // eliminated column c is x_c' = X M[:, c] with M = M' diag(W) (y_c = x_c' / W[c][c]),
+    // so the rounding error of |x_c'|^2 from the Gram's is bounded by
+    // P_c = W[c][c]^2 sum_k M'[k][c]^2 Pg_k (lane c < 8 holds column c of M').
+    if (lane < 8) {
+      double pa = 0.0, pb = 0.0;  // two short chains (the chain warp is latency-bound)
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        pa = fma(x[k] * x[k], gq[24 + k], pa);
+        pb = fma(x[k + 1] * x[k + 1], gq[24 + k + 1], pb);
+      }
+      // pivot >= 1e-2 (S[c][c] + P_c): S[c][c] >= alpha_c^2 covers both conditions
+      good_c = gq[c] >= 1e-2 * fma(pa + pb, gq[8 + c], gq[16 + c]);
+    }
   }
   __syncwarp();
   CHOL_PH(3);
@@ -1168,7 +1191,7 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
   __syncwarp();
   *reinterpret_cast<double2*>(T + g * C::LDT + c0) = make_double2(-P[0], -P[1]);
   CHOL_PH(4);
-  const bool good = rng_ok && piv_g >= 1e-2 * (sdiag + Pg);
+  const bool good = rng_ok && good_c;
   const bool ok = __all_sync(FULL, good);
 #ifdef JQ_KTIME
   if (!ok && lane == 0) atomicAdd(&g_gram_fail[0], 1ull);

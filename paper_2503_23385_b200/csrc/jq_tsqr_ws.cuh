@@ -72,7 +72,7 @@ struct CfgS {
   static constexpr size_t SMEM = size_t(TOTAL) * sizeof(double);
   static_assert(SMEM <= (MIN_CTAS == 1 ? 227 : 113) * 1024, "shared memory per CTA");
   static_assert(NP <= 128, "loader transform assumes <= 128 columns per side");
-  static_assert(OFF_LD - OFF_U >= 16 * LDT + 16, "factor_panel_chol scratch (U .. P)");
+  static_assert(OFF_LD - OFF_U >= 16 * LDT + 16 + 32, "factor_panel_chol scratch (U .. P)");
   static_assert((OFF_LD + 3 * K) % 2 == 0, "16-byte aligned packed loader coefficients");
 };
 
