@@ -576,11 +576,14 @@ def run_e2e(args, host, jrows, r_ref):
             for key in ("A", "B"):
                 cudart.cudaHostUnregister(host[key][0].ctypes.data)
                 host[key] = (host[key][0], False)
+            P.figaro_r(ta, tb)            # warm-up: the context allocates its pinned staging ring once
             t0 = time.perf_counter()
             rp = P.figaro_r(ta, tb)
             tp = time.perf_counter() - t0
             pageable = {"value": jrows / tp, "ms_per_step": tp * 1e3, "steps": 1,
-                        "parity": rel_err_abs(rp, r_ref)}
+                        "parity": rel_err_abs(rp, r_ref),
+                        "note": "plain numpy inputs: host threads copy them through a pinned staging ring "
+                                "(allocated once per context, in the warm-up call)"}
         h2d = host["A"][0].nbytes + host["B"][0].nbytes
         if host["ka"] is not None:
             h2d += host["ka"].nbytes + host["kb"].nbytes

@@ -779,7 +779,50 @@ static bool use_streamed(const double* a, int64_t m1, int64_t n1, const double* 
   return (m1 * n1 + m2 * n2) * 8 >= env_bytes("JQ_STREAM_MIN_BYTES", int64_t(1) << 30);
 }
 
-static bool is_pageable(const void* p) {
+// H2D of PAGEABLE host memory through a pinned staging ring: the driver would stage
+// such copies itself at ~11 GB/s, synchronously; instead host threads memcpy each chunk
+// (<= 512 MB) into a pinned slot (waiting only for that slot's previous DMA) and the DMA
+// runs from the slot on `stream` while the next chunk is being copied.  The ring (3 slots)
+// is allocated on first use and kept by the context.
+int pinned_ring_copy(jq_ctx* ctx, cudaStream_t stream, void* dst, const void* src, size_t bytes) {
+  constexpr int S = 3;
+  const size_t slot_max = size_t(512) << 20;
+  const size_t want = std::min(slot_max, bytes);
+  if (!ctx->stage_pin || ctx->stage_slot < want) {
+    if (ctx->stage_pin) {
+      for (auto& e : ctx->sev) if (e) cudaEventSynchronize(e);
+      cudaFreeHost(ctx->stage_pin);
+      ctx->stage_pin = nullptr;
+    }
+    JQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->stage_pin), want * S, cudaHostAllocDefault));
+    ctx->stage_slot = want;
+    ctx->stage_slots = S;
+    for (int i = 0; i < S; ++i)
+      if (!ctx->sev[i]) JQ_CUDA(cudaEventCreateWithFlags(&ctx->sev[i], cudaEventDisableTiming));
+  }
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int nt = (int)std::max(1u, std::min(hw ? hw : 1u, 16u));
+  for (size_t off = 0; off < bytes; off += ctx->stage_slot) {
+    const size_t len = std::min(ctx->stage_slot, bytes - off);
+    const int slot = ctx->stage_next++ % S;
+    JQ_CUDA(cudaEventSynchronize(ctx->sev[slot]));  // the slot's previous DMA has drained
+    char* pin = ctx->stage_pin + size_t(slot) * ctx->stage_slot;
+    const char* from = static_cast<const char*>(src) + off;
+    const size_t part = (len + nt - 1) / nt;
+    std::vector<std::thread> th;
+    for (int i = 1; i < nt; ++i) {
+      const size_t o = size_t(i) * part;
+      if (o < len) th.emplace_back([=] { memcpy(pin + o, from + o, std::min(part, len - o)); });
+    }
+    memcpy(pin, from, std::min(part, len));
+    for (auto& x : th) x.join();
+    JQ_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin, len, cudaMemcpyHostToDevice, stream));
+    JQ_CUDA(cudaEventRecord(ctx->sev[slot], stream));
+  }
+  return JQ_OK;
+}
+
+bool is_pageable(const void* p) {
   cudaPointerAttributes attr;
   if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
     cudaGetLastError();
@@ -788,46 +831,21 @@ static bool is_pageable(const void* p) {
   return attr.type == cudaMemoryTypeUnregistered;
 }
 
-// Piece H2D for the streamed path.  Page-locked sources: one async DMA on the copy
-// stream.  Pageable sources (a plain numpy caller): the driver would stage them itself at
-// ~11 GB/s, synchronously; instead host threads memcpy the piece into a pinned slot of a
-// ring (waiting only for that slot's previous DMA) and the DMA runs from the slot while
-// the next piece is being copied.
+// Host -> device copy of a staged input: large pageable sources through the pinned ring.
+int h2d_copy(jq_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes >= (size_t(64) << 20) && is_pageable(src)) return pinned_ring_copy(ctx, ctx->stream, dst, src, bytes);
+  JQ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return JQ_OK;
+}
+
+// Piece H2D for the streamed path (copy stream; pageable pieces through the ring).
 static int h2d_piece(jq_ctx* ctx, void* dst, const void* src, size_t bytes, bool pageable, int64_t k) {
+  (void)k;
   if (!pageable) {
     JQ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
     return JQ_OK;
   }
-  constexpr int S = 3;
-  if (!ctx->stage_pin || ctx->stage_slot < bytes) {
-    if (ctx->stage_pin) {
-      for (auto& e : ctx->sev) if (e) cudaEventSynchronize(e);
-      cudaFreeHost(ctx->stage_pin);
-      ctx->stage_pin = nullptr;
-    }
-    JQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->stage_pin), bytes * S, cudaHostAllocDefault));
-    ctx->stage_slot = bytes;
-    ctx->stage_slots = S;
-    for (int i = 0; i < S; ++i)
-      if (!ctx->sev[i]) JQ_CUDA(cudaEventCreateWithFlags(&ctx->sev[i], cudaEventDisableTiming));
-  }
-  const int slot = int(k % S);
-  JQ_CUDA(cudaEventSynchronize(ctx->sev[slot]));  // the slot's previous DMA has drained
-  char* pin = ctx->stage_pin + size_t(slot) * ctx->stage_slot;
-  const unsigned hw = std::thread::hardware_concurrency();
-  const int nt = (int)std::max(1u, std::min(hw ? hw : 1u, 16u));
-  const size_t part = (bytes + nt - 1) / nt;
-  std::vector<std::thread> th;
-  for (int i = 1; i < nt; ++i) {
-    const size_t o = size_t(i) * part;
-    if (o < bytes)
-      th.emplace_back([=] { memcpy(pin + o, static_cast<const char*>(src) + o, std::min(part, bytes - o)); });
-  }
-  memcpy(pin, src, std::min(part, bytes));
-  for (auto& x : th) x.join();
-  JQ_CUDA(cudaMemcpyAsync(dst, pin, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
-  JQ_CUDA(cudaEventRecord(ctx->sev[slot], ctx->copy_stream));
-  return JQ_OK;
+  return pinned_ring_copy(ctx, ctx->copy_stream, dst, src, bytes);
 }
 
 static int figaro_r_streamed(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const double* b, int64_t m2,

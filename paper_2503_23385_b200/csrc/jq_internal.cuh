@@ -81,6 +81,7 @@ struct jq_ctx {
   char* stage_pin = nullptr;
   size_t stage_slot = 0;
   int stage_slots = 0;
+  int64_t stage_next = 0;
   cudaEvent_t sev[4]{};
   cudaStream_t aux_stream = nullptr;    // V replay beside the Jacobi sweeps (jq_svd.cu)
   cudaEvent_t aev[2]{};
@@ -127,6 +128,9 @@ T* ws_alloc(jq_ctx* ctx, size_t count) {
 inline size_t ws_bytes(size_t count, size_t elem) { return (count * elem + 255) & ~size_t(255); }
 
 bool is_device_ptr(const void* p);
+bool is_pageable(const void* p);
+// H2D of a staged input on ctx->stream (large pageable sources via a pinned ring)
+int h2d_copy(jq_ctx* ctx, void* dst, const void* src, size_t bytes);
 
 // Input staging: returns a device pointer for `p` (device pointers pass through;
 // host buffers are copied into workspace memory on the context stream).
@@ -135,7 +139,7 @@ int stage_in(jq_ctx* ctx, const T* p, size_t count, const T** out) {
   if (p == nullptr || count == 0 || is_device_ptr(p)) { *out = p; return JQ_OK; }
   T* d = ws_alloc<T>(ctx, count);
   if (!d) return fail(JQ_E_OOM, "workspace exhausted while staging input");
-  JQ_CUDA(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  JQ_TRY(h2d_copy(ctx, d, p, count * sizeof(T)));
   *out = d;
   return JQ_OK;
 }
