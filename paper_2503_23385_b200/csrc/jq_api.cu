@@ -75,6 +75,7 @@ int sync_and_check_flags(jq_ctx* ctx) {
   if (f & FLAG_UNSORTED_A) return fail(JQ_E_UNSORTED, "left table keys are not sorted non-decreasing");
   if (f & FLAG_UNSORTED_B) return fail(JQ_E_UNSORTED, "right table keys are not sorted non-decreasing");
   if (f & FLAG_NOCONV) return fail(JQ_E_NOCONV, "Jacobi SVD did not converge in 64 sweeps");
+  if (f & FLAG_BADINDEX) return fail(JQ_E_INVALID, "row permutation entry out of range");
   return JQ_OK;
 }
 

@@ -57,7 +57,7 @@ struct Workspace {
 };
 
 // Device-side error flags raised by validation kernels (read once per call).
-enum DevFlag : int { FLAG_UNSORTED_A = 1, FLAG_UNSORTED_B = 2, FLAG_NOCONV = 4 };
+enum DevFlag : int { FLAG_UNSORTED_A = 1, FLAG_UNSORTED_B = 2, FLAG_NOCONV = 4, FLAG_BADINDEX = 8 };
 
 }  // namespace jq
 

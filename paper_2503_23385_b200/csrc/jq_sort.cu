@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(RS_THREADS) scatter_kernel(const int64_t* __re
 // is one contiguous read, no per-element integer division.
 template <class V>
 __global__ void gather_rows_kernel(const V* __restrict__ x, int64_t rows, int64_t items, int lshift,
-                                   const int64_t* __restrict__ perm, V* __restrict__ out) {
+                                   const int64_t* __restrict__ perm, V* __restrict__ out, int* flags) {
   const int L = 1 << lshift;
   const int lane = threadIdx.x & 31, sub = lane >> lshift, c0 = lane & (L - 1);
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -139,7 +139,12 @@ __global__ void gather_rows_kernel(const V* __restrict__ x, int64_t rows, int64_
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w * rpw < rows; w += warps) {
     const int64_t i = w * rpw + sub;
     if (i >= rows) continue;
-    const V* src = x + __ldg(perm + i) * items;
+    const int64_t pi = __ldg(perm + i);
+    if (pi < 0 || pi >= rows) {  // a caller's bad permutation: flag it, never read out of bounds
+      if (c0 == 0) atomicOr(flags, FLAG_BADINDEX);
+      continue;
+    }
+    const V* src = x + pi * items;
     V* dst = out + i * items;
     for (int64_t c = c0; c < items; c += L) dst[c] = __ldg(src + c);
   }
@@ -214,9 +219,10 @@ int gather_rows_dev(jq_ctx* ctx, const double* x, int64_t rows, int64_t cols, co
   const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(warps, 8), int64_t(ctx->sms) * 16);
   if (vec)
     gather_rows_kernel<double2><<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const double2*>(x), rows, items,
-                                                                 lshift, perm, reinterpret_cast<double2*>(out));
+                                                                 lshift, perm, reinterpret_cast<double2*>(out),
+                                                                 ctx->d_flags);
   else
-    gather_rows_kernel<double><<<blocks, 256, 0, ctx->stream>>>(x, rows, items, lshift, perm, out);
+    gather_rows_kernel<double><<<blocks, 256, 0, ctx->stream>>>(x, rows, items, lshift, perm, out, ctx->d_flags);
   JQ_CHECK_LAUNCH(ctx);
   return JQ_OK;
 }

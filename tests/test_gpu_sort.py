@@ -63,6 +63,14 @@ def test_radix_sort_torch_device(P):
     assert np.array_equal(perm.cpu().numpy(), rp) and np.array_equal(sk.cpu().numpy(), rk)
 
 
+def test_gather_rows_rejects_bad_permutation(P):
+    x = np.ones((100, 4))
+    with pytest.raises(ValueError, match="out of range"):
+        P.gather_rows(x, np.r_[np.arange(99), 100].astype(np.int64))
+    with pytest.raises(ValueError, match="out of range"):
+        P.gather_rows(x, np.r_[-1, np.arange(1, 100)].astype(np.int64))
+
+
 @pytest.mark.parametrize("cols", [1, 3, 16, 33])
 def test_gather_rows_bit_exact(P, cols):
     rng = np.random.default_rng(cols)
