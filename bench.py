@@ -44,10 +44,10 @@ CONFIGS = {
 }
 METRIC = "join rows/sec (m1*m2/t), time-to-R"
 # dram__bytes_read.sum + dram__bytes_write.sum per leaf-kernel launch (ncu --set full)
-NCU_TRAFFIC = {(4, "footnote"): {"bytes": 51.218248e9 + 10.816512e6,
-                                 "note": "first tsqr_ws2_kernel launch (side A, carry-free leaves, round-2 capture "
-                                         "profiles/r02_ncu_ws2_c4.md / _raw.csv, 68.80 ms under ncu): its own 1e8 x 64 "
-                                         "f64 rows = 51.2e9 algorithmic bytes, every byte read once"}}
+NCU_TRAFFIC = {(4, "footnote"): {"bytes": 51.217598e9 + 16.129024e6,
+                                 "note": "first tsqr_ws2_kernel launch (side A, carry-free leaves, round-2 final capture "
+                                         "profiles/r02_ncu_ws2_c4.md / _final_raw.csv, 71.90 ms under ncu): its own "
+                                         "1e8 x 64 f64 rows = 51.2e9 algorithmic bytes, every byte read once"}}
 
 
 def peaks():
