@@ -1769,6 +1769,14 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t 
   return JQ_OK;
 }
 
+static bool ws128() {
+  static const bool on = [] {
+    const char* e = getenv("JQ_TSQR_WS128");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <class Src>
 static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
                            bool canonical, double* r_out, int use_tma, LeafSet* defer = nullptr) {
@@ -1784,8 +1792,10 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
     case 64:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
       return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
-    case 128:  // (CfgS<128, 16, 8, 1, 8> -- 64-row chunks beside the 70 KB R -- measured slower:
-      // C4 dense 1094 vs 861 ms, C5 22.5 vs 21.6 ms; the chain cost is per panel, not per row)
+    case 128:  // CfgS<128, 16, 8, 1, 8> (opt-in, JQ_TSQR_WS128=1): 64-row chunks beside the 70 KB R
+      // -- slower also with the round-2 leaf (C5 14.9 vs 13.2 ms, C4 dense 1118 vs 864 ms): the
+      // chain costs per panel, and a 64-row chunk amortises it over too few rows)
+      if (ws128()) return run_stream_ws<CfgS<128, 16, 8, 1, 8>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
       return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
   }

@@ -58,7 +58,8 @@ struct CfgS {
   static constexpr int OFF_P = OFF_SC + 8;                // [2][DW][8]
   static constexpr int OFF_LD = OFF_P + 2 * DW * 8;       // loader per-row scalars: c1, c2, mode [3][K], then
   // the multi-loader transform's packed {c1, c2, keep, w} per row [K][4]
-  static constexpr int OFF_S = OFF_LD + 7 * K;            // loader running prefix
+  static constexpr int OFF_S = OFF_LD + (NP <= 32 ? 7 : 3) * K;  // loader running prefix (the packed
+  // coefficients are only used by the multi-loader transform, NP <= 32)
   static constexpr int OFF_FLAG = OFF_S + NP;             // [2] chain accepted, by parity
   static constexpr int OFF_GP = OFF_FLAG + 2;             // [DW][64] C^T C partials of the next tile (ws2)
   static constexpr int OFF_GD = OFF_GP + DW * 64;         // [DW][64] direct Gram partials (ws2)
@@ -74,6 +75,7 @@ struct CfgS {
   static_assert(NP <= 128, "loader transform assumes <= 128 columns per side");
   static_assert(OFF_LD - OFF_U >= 16 * LDT + 16 + 32, "factor_panel_chol scratch (U .. P)");
   static_assert((OFF_LD + 3 * K) % 2 == 0, "16-byte aligned packed loader coefficients");
+  static_assert(NP <= 32 || NLOAD == 1, "the packed loader coefficients need the 7 K scratch");
 };
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned count) {
