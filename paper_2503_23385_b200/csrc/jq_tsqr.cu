@@ -49,6 +49,19 @@ namespace jq {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
+// f(IntC<P>), ..., f(IntC<N-1>): a loop whose index is a compile-time constant in the body
+template <int P, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (P < N) {
+    f(IntC<P>{});
+    static_for<P + 1, N>(f);
+  }
+}
+
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d[0]), "+d"(d[1])
@@ -122,6 +135,42 @@ __device__ __forceinline__ int rix(int r, int c) {
 // recurrences in flight per lane; FigaroSrc::seg_pass1 / seg_pass2)
 constexpr int SEG_SUB = 4;
 
+// bar.sync id, n: a barrier among the n threads (whole warps) that execute it
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// the same barrier, returning the AND of `v` over the n threads
+__device__ __forceinline__ bool named_bar_and(int id, int n, bool v) {
+  int r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.s32 p, %1, 0;\n bar.red.and.pred q, %2, %3, p;\n selp.s32 %0, 1, 0, q;\n}\n"
+      : "=r"(r)
+      : "r"(v ? 1 : 0), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
+// the barrier among the NW row warps of a direct chunk load: __syncthreads (BAR 0, the
+// CTA-wide leaf) or named barrier BAR (the data warps of the warp-specialised leaf)
+template <int NW, int BAR>
+struct RowBar {
+  static constexpr int NW_ = NW;
+  __device__ static void sync() {
+    if constexpr (BAR == 0) __syncthreads();
+    else named_bar(BAR, NW * 32);
+  }
+  __device__ static bool sync_and(bool v) {
+    if constexpr (BAR == 0) return __syncthreads_and(v);
+    else return named_bar_and(BAR, NW * 32, v);
+  }
+};
+
+// chunk row held in register slot (it, b) of lane quad t of `warp` by the direct-load
+// leaves: 2 KWT consecutive rows per thread (the staged path: row 8 it + 2 t + b)
+template <class C>
+__device__ __forceinline__ int direct_row(int warp, int t, int it, int b) {
+  return warp * C::KW + t * (2 * C::KWT) + 2 * it + b;
+}
+
 struct DenseSrc {
   const double* m;
   int64_t rows, cols;
@@ -135,6 +184,24 @@ struct DenseSrc {
   template <class C>
   __device__ double value(const double* raw, const double*, int64_t, int i, int l, int nrows, int rcols) const {
     return (i < nrows && l < rcols) ? raw[i * rcols + l] : 0.0;
+  }
+  // direct chunk load (load_direct): global -> the C^T registers of the NW row warps
+  // (Bar::NW_), no shared-memory staging; the rows v0 .. v0 + nr - 1 (the rest zero)
+  static constexpr bool DIRECT = true;
+  template <class C, class Bar, class Mark>
+  __device__ void load_direct(double (&c)[C::NLT][C::KWT][2], int64_t v0, int nr, double*, double*, double*,
+                              double*, int warp, int lane, Mark) const {
+    const int g = lane >> 2, t = lane & 3, nc = (int)cols;
+    const double* base = m + v0 * cols;
+#pragma unroll
+    for (int q = 0; q < C::NLT; ++q)
+#pragma unroll
+      for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int i = direct_row<C>(warp, t, it, b), l = 8 * q + g;
+          c[q][it][b] = (i < nr && l < nc) ? __ldg(base + (int64_t)i * cols + l) : 0.0;
+        }
   }
   // warp-specialised loader (tsqr_ws_kernel): chunk rows never cross limit(v0)
   __device__ int64_t limit(int64_t) const { return INT64_MAX; }
@@ -158,6 +225,7 @@ struct DenseSrc {
 // raw rows, no loader work: rc() = 0)
 struct JoinSrc : DenseSrc {
   JoinArgs ja;
+  static constexpr bool DIRECT = false;  // rows generated in value()
   __device__ int rc(int64_t) const { return 0; }
   __device__ const double* ptr(int64_t) const { return nullptr; }
   __device__ int64_t avail(int64_t v0) const { return ja.rows - v0; }
@@ -335,6 +403,211 @@ struct FigaroSrc {
 
   __device__ int64_t limit(int64_t v0) const { return v0 < m1pad ? m1pad : INT64_MAX; }
 
+  // ---- direct chunk load (load_direct) by the NW row warps (Bar::NW_; `warp` = the
+  // caller's row-warp index).  A part: [c1 A_i | c2 totals(B_g)] per row.  B part: the tail
+  // transform out_r = c1_r x_r - c2_r S_r, S_{r+1} = keep_r S_r + w_r x_r (keep 0 at a
+  // group start, w 0 for a row without a group) is a scan of affine maps S -> K S + A along
+  // the chunk rows, done in the DMMA register layout.  The chunk's rows are assigned to the
+  // register slots so that a thread holds 2 KWT CONSECUTIVE rows (direct_row; R is
+  // invariant under a row permutation of the chunk): the thread folds its rows into one
+  // map, the maps are scanned across the 4 lanes t of the column by shuffles, and the
+  // warps' totals over the warps (one column per thread) from the running prefix S.  Fast
+  // path (only tail rows in the chunk): plain prefix sums.  lo: [NLT][NW*32] (the
+  // thread's offsets), wt: [NW][NP] double2, coef: c1 | c2 | mode per chunk row (3 K); all
+  // three idle between chunks.  Chunks never cross m1pad (limit()).
+  static constexpr bool DIRECT = true;
+  template <class C, class Bar, class Mark>
+  __device__ void load_direct(double (&c)[C::NLT][C::KWT][2], int64_t v0, int nr, double* S, double* lo, double* wt,
+                              double* coef, int warp, int lane, Mark mark) const {
+    static_assert(C::NLT <= 32, "one keep bit per tile");
+    constexpr int NW = Bar::NW_, NT = NW * 32;
+    const int g = lane >> 2, t = lane & 3, rt = warp * 32 + lane;
+    const int n1 = (int)fa.n1, n2 = (int)fa.n2;
+    int* cmode = reinterpret_cast<int*>(coef + 2 * C::K);
+    if (v0 < m1pad) {
+      // ---- top block rows: [sqrt(m2g) A_i | head(B_g)]; no scan
+      for (int i = rt; i < C::K; i += NT) {
+        int gg = -1;
+        double m2g = 0.0;
+        if (i < nr) {
+          const int64_t r = v0 + i;
+          gg = fa.gid_a ? __ldg(fa.gid_a + r) : 0;
+          if (gg >= 0) m2g = fa.gid_a ? (double)__ldg(fa.b_count + gg) : (double)fa.m2_global;
+        }
+        const double rs2 = gg >= 0 && m2g > 0.0 ? rsqrt_nr(m2g) : 0.0;
+        coef[i] = m2g * rs2;
+        coef[C::K + i] = rs2;
+        cmode[i] = gg;
+      }
+      Bar::sync();
+      const double* ab = fa.a + v0 * fa.n1;
+#pragma unroll
+      for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int i = direct_row<C>(warp, t, it, b);
+          const int gg = cmode[i];
+          const double c1v = coef[i], c2v = coef[C::K + i];
+#pragma unroll
+          for (int q = 0; q < C::NLT; ++q) {
+            const int l = 8 * q + g;
+            double v = 0.0;
+            if (i < nr && gg >= 0) {
+              if (l < n1) v = __ldg(ab + (int64_t)i * n1 + l) * c1v;
+              else if (l < n) v = __ldg(fa.b_totals + (int64_t)gg * n2 + (l - n1)) * c2v;
+            }
+            c[q][it][b] = v;
+          }
+        }
+      Bar::sync();  // coef / cmode read before the next chunk rewrites them
+      return;
+    }
+    const int64_t b0 = v0 - m1pad;
+    // per-row coefficients, one thread per chunk row: c1, c2 -> coef, the row mode -> cmode
+    bool tails = true;  // every row a tail row (or past the chunk)
+    for (int i = rt; i < C::K; i += NT) {
+      int md = 0;
+      double c1v = 0.0, c2v = 0.0;
+      if (i < nr) {
+        const int64_t br = b0 + i;
+        int64_t rr = 0;
+        double m1g = 0.0;
+        bool valid = true;
+        if (fa.gid_b) {
+          const int gg = __ldg(fa.gid_b + br);
+          valid = gg >= 0;
+          if (valid) { rr = br - __ldg(fa.b_start + gg); m1g = (double)__ldg(fa.a_count + gg); }
+        } else {
+          rr = cart_row(br);
+          m1g = (double)fa.m1_global;
+        }
+        if (valid) {
+          if (rr == 0) {
+            md = 1;
+          } else {
+            const double rd = (double)rr;
+            md = 2;
+            c2v = (m1g * rsqrt_nr(m1g)) * rsqrt_nr(rd * (rd + 1.0));
+            c1v = rd * c2v;
+          }
+        }
+        tails = tails && md == 2;
+      }
+      coef[i] = c1v;
+      coef[C::K + i] = c2v;
+      cmode[i] = md;
+    }
+    const double* bb = fa.b + b0 * fa.n2 - n1;
+#pragma unroll
+    for (int q = 0; q < C::NLT; ++q)
+#pragma unroll
+      for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int i = direct_row<C>(warp, t, it, b), l = 8 * q + g;
+          c[q][it][b] = (i < nr && l >= n1 && l < n) ? __ldg(bb + (int64_t)i * n2 + l) : 0.0;
+        }
+    const bool fast = Bar::sync_and(tails);
+    unsigned kb = 0, wb = 0;  // bit 2 it + b: keep S / add x
+#pragma unroll
+    for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int md = cmode[direct_row<C>(warp, t, it, b)];
+        if (md != 1) kb |= 1u << (2 * it + b);
+        if (md != 0) wb |= 1u << (2 * it + b);
+      }
+    mark(7);
+    // phase 1: per tile, the thread's map from the warp's first row (K bit, A -> lo) and
+    // the warp's total map (-> wt)
+    unsigned kx = 0;
+    if (fast) {
+#pragma unroll
+      for (int q = 0; q < C::NLT; ++q) {
+        double A = 0.0;
+#pragma unroll
+        for (int it = 0; it < C::KWT; ++it) A += c[q][it][0] + c[q][it][1];
+#pragma unroll
+        for (int d = 1; d < 4; d <<= 1) {
+          const double Ae = __shfl_up_sync(0xffffffffu, A, d, 4);
+          if (t >= d) A += Ae;
+        }
+        const double Ax = __shfl_up_sync(0xffffffffu, A, 1, 4);
+        const double At = __shfl_sync(0xffffffffu, A, 3, 4);
+        lo[q * NT + rt] = t == 0 ? 0.0 : Ax;
+        if (t == 0) *reinterpret_cast<double2*>(wt + 2 * (warp * C::NP + 8 * q + g)) = make_double2(1.0, At);
+      }
+      kx = ~0u;
+    } else {
+#pragma unroll
+      for (int q = 0; q < C::NLT; ++q) {
+        double K = 1.0, A = 0.0;
+#pragma unroll
+        for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const bool kk = (kb >> (2 * it + b)) & 1, ww = (wb >> (2 * it + b)) & 1;
+            A = (kk ? A : 0.0) + (ww ? c[q][it][b] : 0.0);
+            K = kk ? K : 0.0;
+          }
+#pragma unroll
+        for (int d = 1; d < 4; d <<= 1) {
+          const double Ke = __shfl_up_sync(0xffffffffu, K, d, 4), Ae = __shfl_up_sync(0xffffffffu, A, d, 4);
+          if (t >= d) { A = fma(K, Ae, A); K *= Ke; }
+        }
+        const double Kx = __shfl_up_sync(0xffffffffu, K, 1, 4), Ax = __shfl_up_sync(0xffffffffu, A, 1, 4);
+        const double Kt = __shfl_sync(0xffffffffu, K, 3, 4), At = __shfl_sync(0xffffffffu, A, 3, 4);
+        lo[q * NT + rt] = t == 0 ? 0.0 : Ax;
+        if (t == 0 || Kx != 0.0) kx |= 1u << q;
+        if (t == 0) *reinterpret_cast<double2*>(wt + 2 * (warp * C::NP + 8 * q + g)) = make_double2(Kt, At);
+      }
+    }
+    Bar::sync();
+    mark(8);
+    // the warps' carry-ins per column from the running prefix S; S <- the chunk's carry-out
+    for (int l = rt; l < C::NP; l += NT) {
+      if (l >= n1 && l < n) {
+        double sv = S[l - n1];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const double2 mp = *reinterpret_cast<const double2*>(wt + 2 * (w * C::NP + l));
+          wt[2 * (w * C::NP + l)] = sv;
+          sv = fma(mp.x, sv, mp.y);
+        }
+        S[l - n1] = sv;
+      }
+    }
+    Bar::sync();
+    mark(9);
+    // phase 2: the transform
+    double c1r[C::KWT][2], c2r[C::KWT][2];
+#pragma unroll
+    for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int i = direct_row<C>(warp, t, it, b);
+        c1r[it][b] = coef[i];
+        c2r[it][b] = coef[C::K + i];
+      }
+#pragma unroll
+    for (int q = 0; q < C::NLT; ++q) {
+      const int l = 8 * q + g;
+      if (l >= n1 && l < n) {
+        double sv = (((kx >> q) & 1) ? wt[2 * (warp * C::NP + l)] : 0.0) + lo[q * NT + rt];
+#pragma unroll
+        for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const double x = c[q][it][b];
+            c[q][it][b] = fma(c1r[it][b], x, -c2r[it][b] * sv);
+            if (fast) sv += x;
+            else sv = (((kb >> (2 * it + b)) & 1) ? sv : 0.0) + (((wb >> (2 * it + b)) & 1) ? x : 0.0);
+          }
+      }
+    }
+    Bar::sync();  // wt / lo / coef read before the caller reuses them
+  }
+
   // prep by ONE warp (the loader warp of tsqr_ws_kernel): per-row scalars, then the
   // B-part tail transform in place, lane = column (sequential over the chunk rows,
   // loads batched by 4); S is the running prefix of the loader.
@@ -504,7 +777,7 @@ struct FigaroSrc {
     int* imode = reinterpret_cast<int*>(mode);
     // all row gathers of the segment first (group id, then the group's start and the
     // other side's count): two dependent rounds of global loads instead of 2 per row
-    constexpr int IT = (C::K / C::NLOAD + 31) / 32;
+    constexpr int IT = (C::K / (C::NLOAD > 0 ? C::NLOAD : 1) + 31) / 32;
     const int e = min(i1, nrows);
     int gg[IT];
     int64_t st[IT], cnt[IT];
@@ -765,6 +1038,13 @@ __device__ __forceinline__ void bulk_fetch(uint64_t* bar, void* dst, const void*
   }
 }
 
+// thread 0: pull the next chunk's rows into L2 (the direct-load leaf reads them from there)
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes16) {
+  if (bytes16)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(__cvta_generic_to_global(src)), "r"(bytes16)
+                 : "memory");
+}
+
 // ------------------------------------------------------------------ panel factorisation
 #ifdef JQ_PANEL_TIMING
 __device__ long long g_ptime[16];
@@ -787,11 +1067,6 @@ __device__ long long g_ptime[16];
 // x . c_g, one quad reduction, and a CTA-wide fixed-order sum of the WARPS partials
 // gives d_g (g = j: |x|^2; g > j: reflector dot product; g < j: T entries).
 // On return cp holds Y (scaled) and Yt (this warp's rows) / T / R rows are written.
-// bar.sync id, n: a barrier among the n threads (whole warps) that execute it
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 // NW = warps holding rows (partials summed in warp order), BAR = 0: __syncthreads,
 // else named barrier BAR over those NW warps; `warp` = the caller's row-warp index.
 template <class C, int NW = C::WARPS, int BAR = 0>
@@ -1209,11 +1484,11 @@ __device__ __forceinline__ bool factor_panel_chol(const double (&G)[2], double (
 #define JQ_PROBE 0
 #endif
 #ifdef JQ_KTIME
-__device__ unsigned long long g_ktime[8];
-#define KT_DECL long long kt_acc[5] = {0, 0, 0, 0, 0}; long long kt_t = clock64();
+__device__ unsigned long long g_ktime[16];
+#define KT_DECL long long kt_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}; long long kt_t = clock64();
 #define KT_MARK(i) do { long long n_ = clock64(); kt_acc[i] += n_ - kt_t; kt_t = n_; } while (0)
-#define KT_FLUSH() do { if (lane == 0) for (int i_ = 0; i_ < 5; ++i_) atomicAdd(&g_ktime[i_], (unsigned long long)kt_acc[i_]); \
-                        if (tid == 0) atomicAdd(&g_ktime[7], 1ull); } while (0)
+#define KT_FLUSH() do { if (lane == 0) for (int i_ = 0; i_ < 10; ++i_) atomicAdd(&g_ktime[i_], (unsigned long long)kt_acc[i_]); \
+                        if (tid == 0) atomicAdd(&g_ktime[15], 1ull); } while (0)
 #else
 #define KT_DECL
 #define KT_MARK(i) do {} while (0)
@@ -1301,21 +1576,46 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
     const uint32_t bytes = uint32_t(nr) * uint32_t(rcol) * 8u;
     bulk_fetch(bar, raw, s.ptr(v0), bytes & ~15u);
   };
-  if ((use_tma & 1) && tid == 0 && row_begin < row_end) issue(row_begin, row_begin);
+  // direct chunk loads (flag 256 off: JQ_TSQR_STAGED=1) for sources that have them
+  const bool direct = Src::DIRECT && !(use_tma & 256);
+  auto prefetch = [&](int64_t v0) {  // thread 0, direct mode: the chunk at v0 into L2
+    if (!(use_tma & 1) || v0 >= row_end) return;
+    const int64_t lim = v0 + C::K < row_end ? v0 + C::K : row_end;
+    int64_t nr = lim - v0;
+    const int64_t av = s.avail(v0);
+    nr = av < nr ? av : nr;
+    if (nr > 0) l2_prefetch(s.ptr(v0), uint32_t(nr * s.rc(v0) * 8) & ~15u);
+  };
+  if (tid == 0 && row_begin < row_end) {
+    if (direct) prefetch(row_begin);
+    else if (use_tma & 1) issue(row_begin, row_begin);
+  }
 
   double c[C::NLT][C::KWT][2];  // this warp's rows of every column tile (C^T accumulator layout)
   uint32_t phase = 0;
   KT_DECL
 
   for (int64_t row0 = row_begin; row0 < row_end; row0 += C::K) {
+    if (direct) {
+      if (tid == 0) prefetch(row0 + C::K);
+      const int64_t lim = row0 + C::K < row_end ? row0 + C::K : row_end;
+      int64_t nr = lim - row0;
+      const int64_t av = s.avail(row0);
+      nr = av < nr ? av : nr;
+      s.template load_direct<C, RowBar<C::WARPS, 0>>(c, row0, nr > 0 ? (int)nr : 0, S, raw, Zp, scratch, warp, lane,
+                                                    [&](int i) { KT_MARK(i); });
+      KT_MARK(6);
+    }
     const int rcol = s.rc(row0);
     const int rb = pass_rows<C>(rcol);
     const int npass = (C::K + rb - 1) / rb;
+    if (!direct) {
 #pragma unroll
-    for (int q = 0; q < C::NLT; ++q)
+      for (int q = 0; q < C::NLT; ++q)
 #pragma unroll
-      for (int it = 0; it < C::KWT; ++it) c[q][it][0] = c[q][it][1] = 0.0;  // rows past the range stay zero
-    for (int h = 0; h < npass && row0 + (int64_t)h * rb < row_end; ++h) {
+        for (int it = 0; it < C::KWT; ++it) c[q][it][0] = c[q][it][1] = 0.0;  // rows past the range stay zero
+    }
+    for (int h = 0; !direct && h < npass && row0 + (int64_t)h * rb < row_end; ++h) {
       const int64_t pv0 = row0 + (int64_t)h * rb;
       const int nr = pass_nrows(pv0, rb, row0);
       const int nel = nr * rcol;
@@ -1328,8 +1628,10 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
         for (int e = tid; e < nel; e += C::THREADS) raw[e] = __ldg(src_rows + e);
       }
       __syncthreads();
+      KT_MARK(0);
       s.template prep<C>(raw, S, scratch, pv0, nr);
       __syncthreads();
+      KT_MARK(5);
 #pragma unroll
       for (int q = 0; q < C::NLT; ++q) {
         const int l = q * 8 + g;
@@ -1347,8 +1649,8 @@ tsqr_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, const double* __r
         const int64_t nv0 = same ? pv0 + rb : row0 + C::K;
         if (nv0 < row_end) issue(nv0, same ? row0 : nv0);
       }
+      KT_MARK(6);
     }
-    KT_MARK(0);
 
 #pragma unroll 1
     for (int p = 0; p < C::NLT; ++p) {
@@ -1590,6 +1892,13 @@ static int launch_tsqr(jq_ctx* ctx, int grid, const Src& src, int64_t rows_per_c
     return e && e[0] == '1';
   }();
   if (explicit_panels) use_tma |= 2;
+  // JQ_TSQR_STAGED=1: chunks staged through shared memory (TMA + in-place transform) also
+  // where the direct register load applies (A/B timing and tests)
+  static const bool staged = [] {
+    const char* e = getenv("JQ_TSQR_STAGED");
+    return e && e[0] == '1';
+  }();
+  if (staged) use_tma |= 256;
   use_tma |= chain_flag();
   kern<<<grid, C::THREADS, C::SMEM, ctx->stream>>>(src, rows_per_cta, total_rows, r_init,
                                                    init_count, r_out, use_tma);
@@ -1701,8 +2010,8 @@ static int run_stream(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t ali
   return JQ_OK;
 }
 
-// Leaf kernel for NP <= 64: warp-specialised tsqr_ws2_kernel (default) or the CTA-wide
-// tsqr_kernel (JQ_TSQR_IMPL=cta, for A/B timing and tests); NP >= 128 always CTA-wide.
+// Leaf kernel for NP <= 128: warp-specialised tsqr_ws2_kernel (default) or the CTA-wide
+// tsqr_kernel (JQ_TSQR_IMPL=cta, for A/B timing and tests); NP = 256 always CTA-wide.
 static int leaf_impl() {
   static const int w = [] {
     const char* e = getenv("JQ_TSQR_IMPL");
@@ -1769,12 +2078,14 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t 
   return JQ_OK;
 }
 
-static bool ws128() {
-  static const bool on = [] {
+// NP = 128 warp-specialised leaf: 8 warps (6 data warps x 16 rows, 255 registers) by
+// default; JQ_TSQR_WS128=16x12: 16 warps (12 data warps x 8 rows, 128 registers)
+static int ws128_cfg() {
+  static const int c = [] {
     const char* e = getenv("JQ_TSQR_WS128");
-    return e && e[0] == '1';
+    return (e && strcmp(e, "16x12") == 0) ? 1 : 0;
   }();
-  return on;
+  return c;
 }
 
 template <class Src>
@@ -1792,10 +2103,19 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
     case 64:
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
       return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
-    case 128:  // CfgS<128, 16, 8, 1, 8> (opt-in, JQ_TSQR_WS128=1): 64-row chunks beside the 70 KB R
-      // -- slower also with the round-2 leaf (C5 14.9 vs 13.2 ms, C4 dense 1118 vs 864 ms): the
-      // chain costs per panel, and a 64-row chunk amortises it over too few rows)
-      if (ws128()) return run_stream_ws<CfgS<128, 16, 8, 1, 8>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
+    case 128:
+      // warp-specialised with direct loads: 12 data warps x 8 rows (96-row chunks) off the
+      // chain's SM sub-partition; the staged variant (loader warp + raw-row buffer beside the
+      // 70 KB R) only fitted 64-row chunks and was slower than the CTA-wide kernel
+      if constexpr (Src::DIRECT) {
+        if (leaf_impl() == 0) {
+          if (ws128_cfg() == 1)
+            return run_stream_ws<CfgS<128, 16, 12, 1, 8, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
+                                                                defer);
+          return run_stream_ws<CfgS<128, 8, 6, 1, 16, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
+                                                             defer);
+        }
+      }
       return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 256: return run_stream<Cfg<256>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
   }
@@ -1969,9 +2289,9 @@ extern "C" JQ_API int jq_debug_gram_fail(unsigned long long* out, int reset) {
 }
 extern "C" JQ_API int jq_debug_ktime(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, jq::g_ktime, sizeof(unsigned long long) * 8);
+  cudaMemcpyFromSymbol(out, jq::g_ktime, sizeof(unsigned long long) * 16);
   if (reset) {
-    unsigned long long z[8] = {};
+    unsigned long long z[16] = {};
     cudaMemcpyToSymbol(jq::g_ktime, z, sizeof(z));
   }
   return 0;

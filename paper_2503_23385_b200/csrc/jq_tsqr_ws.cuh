@@ -27,8 +27,12 @@
 // per chain), two spare SMSP-0 warps.  (Two CTAs of 8 warps, 6 data warps each, were
 // measured 5% slower: their chains share SMSP 0 and the lookahead DMMAs of one CTA
 // queue behind the other's bulk update.)
-template <int NP_, int WARPS_ = 16, int DW_ = 12, int MINB_ = 1, int KW_ = 16>
+// DIRECT_: the data warps load their rows straight from global memory (load_direct; no
+// loader warp, no raw-row buffer) -- the NP = 128 leaf, whose R leaves no room for a
+// staged chunk beside the partials.
+template <int NP_, int WARPS_ = 16, int DW_ = 12, int MINB_ = 1, int KW_ = 16, bool DIRECT_ = false>
 struct CfgS {
+  static constexpr bool DIRECT = DIRECT_;
   static constexpr int NP = NP_;
   static constexpr int NLT = NP / 8;
   static constexpr int WARPS = WARPS_;
@@ -42,7 +46,7 @@ struct CfgS {
   __host__ __device__ static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
   static constexpr int LDT = 10;
   static constexpr int LDYT = KW + 2;
-  static constexpr int RAW = K * NP;         // one whole chunk of raw rows
+  static constexpr int RAW = DIRECT ? 0 : K * NP;  // one whole chunk of raw rows
   static constexpr int OFF_R = 0;
   static constexpr int SZ_R = rp_off(NLT);
   static constexpr int OFF_RAW = OFF_R + SZ_R;
@@ -56,14 +60,15 @@ struct CfgS {
   static constexpr int OFF_TAU = OFF_U + 64;
   static constexpr int OFF_SC = OFF_TAU + 8;
   static constexpr int OFF_P = OFF_SC + 8;                // [2][DW][8]
-  static constexpr int OFF_LD = OFF_P + 2 * DW * 8;       // loader per-row scalars: c1, c2, mode [3][K], then
+  static constexpr int OFF_LD = OFF_U + (80 + 2 * DW * 8 > 16 * LDT + 48 ? 80 + 2 * DW * 8 : 16 * LDT + 48);
+  // ^ loader per-row scalars (past the partials [2][DW][8] and factor_panel_chol's scratch): c1, c2, mode [3][K], then
   // the multi-loader transform's packed {c1, c2, keep, w} per row [K][4]
   static constexpr int OFF_S = OFF_LD + (NP <= 32 ? 7 : 3) * K;  // loader running prefix (the packed
   // coefficients are only used by the multi-loader transform, NP <= 32)
   static constexpr int OFF_FLAG = OFF_S + NP;             // [2] chain accepted, by parity
   static constexpr int OFF_GP = OFF_FLAG + 2;             // [DW][64] C^T C partials of the next tile (ws2)
   static constexpr int OFF_GD = OFF_GP + DW * 64;         // [DW][64] direct Gram partials (ws2)
-  static constexpr int NLOAD = NP <= 32 ? 3 : 1;  // loader warps: narrow leaves are loader-bound; at
+  static constexpr int NLOAD = DIRECT ? 0 : NP <= 32 ? 3 : 1;  // loader warps: narrow leaves are loader-bound; at
   // NP = 64 two extra active warps on SMSP 0 slow the chain more than they help (4.62 vs 4.47 ms)
   static constexpr int NSPARE = WARPS - 1 - NLOAD - DW;  // spare warps: the side scan (FigaroSrc::side_scan)
   static constexpr int OFF_LSR = OFF_GD + DW * 64;        // [NLOAD][2][64] loader segment sums
@@ -75,7 +80,8 @@ struct CfgS {
   static_assert(NP <= 128, "loader transform assumes <= 128 columns per side");
   static_assert(OFF_LD - OFF_U >= 16 * LDT + 16 + 32, "factor_panel_chol scratch (U .. P)");
   static_assert((OFF_LD + 3 * K) % 2 == 0, "16-byte aligned packed loader coefficients");
-  static_assert(NP <= 32 || NLOAD == 1, "the packed loader coefficients need the 7 K scratch");
+  static_assert(NP <= 32 || NLOAD <= 1, "the packed loader coefficients need the 7 K scratch");
+  static_assert(NLT * DW * 32 + 2 * DW * NP <= DW * NLT * 64, "direct load: lo and wt inside the partials");
 };
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned count) {
@@ -472,21 +478,34 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       const int64_t r1 = chunk_end(r0);
       const int nr = chunk_rows(r0, r1);
       const int rcol = src.rc(r0);
-      if (d == 0) TR(1, 7);
-      mbar_wait(bar_ready, ph_ready);
-      ph_ready ^= 1;
-      if (d == 0) TR(1, 8);
+      if constexpr (C::DIRECT) {
+        // the partials' buffer holds the load's scan state: free since B of the last panel
+        if (d == 0 && lane == 0 && (flags & 1) && r1 < row_end) {
+          const int64_t r2 = chunk_end(r1);
+          const int nr2 = chunk_rows(r1, r2);
+          if (nr2 > 0) l2_prefetch(src.ptr(r1), uint32_t(nr2) * uint32_t(src.rc(r1)) * 8u & ~15u);
+        }
+        if (d == 0) TR(1, 7);
+        src.template load_direct<C, RowBar<C::DW, BAR_DATA>>(c, r0, nr, S, Zp, Zp + C::NLT * C::DW * 32, scratch,
+                                                             d, lane, [](int) {});
+        if (d == 0) TR(1, 8);
+      } else {
+        if (d == 0) TR(1, 7);
+        mbar_wait(bar_ready, ph_ready);
+        ph_ready ^= 1;
+        if (d == 0) TR(1, 8);
 #pragma unroll
-      for (int q = 0; q < C::NLT; ++q) {
-        const int l = q * 8 + g;
+        for (int q = 0; q < C::NLT; ++q) {
+          const int l = q * 8 + g;
 #pragma unroll
-        for (int it = 0; it < C::KWT; ++it)
+          for (int it = 0; it < C::KWT; ++it)
 #pragma unroll
-          for (int b = 0; b < 2; ++b)
-            c[q][it][b] = src.template value<C>(raw, scratch, r0, d * C::KW + 8 * it + 2 * t + b, l, nr, rcol);
+            for (int b = 0; b < 2; ++b)
+              c[q][it][b] = src.template value<C>(raw, scratch, r0, d * C::KW + 8 * it + 2 * t + b, l, nr, rcol);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_free);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_free);
       gram_partial(0, Gd);
       named_bar(BAR_ALL, NB);
 
@@ -495,8 +514,10 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       // chains the scheduler can interleave (C4 leaf 172.8 -> 138.7 ms; the runtime-p
       // loop left one predicated block per tile).  The chain warp's loop stays rolled
       // (unrolled it is slower: 190 ms, instruction-cache pressure on SMSP 0).
-#pragma unroll
-      for (int p = 0; p < C::NLT; ++p) {
+      // (static_for: at NP = 128 the compiler declines the 16-panel `#pragma unroll` and
+      // issues every tile's DMMAs predicated, so each panel cost as much as the first)
+      static_for<0, C::NLT>([&](auto pc) {
+        constexpr int p = decltype(pc)::value;
         const int j0 = 8 * p, par = p & 1;
         const double* Tp = smem_dyn + C::OFF_T + (par ^ 1) * 8 * C::LDT;
         const double* Mp = smem_dyn + C::OFF_M + (par ^ 1) * 8 * C::LDT;
@@ -652,8 +673,9 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
           named_bar(BAR_DATA, C::DW * 32);
           named_bar(BAR_ALL, NB);  // F_p
         }
-      }
+      });
     }
+    if (C::DIRECT && d == 0) src.finish(S, lane, 32);  // S final since the last load's barriers
     named_bar(BAR_ALL, NB);  // R final
   }
 
