@@ -322,7 +322,8 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       } else {
         named_bar(BAR_LOAD, C::NLOAD * 32);  // raw rows of the chunk in shared memory
         if (li == 0) TR(2, 4);
-        const int i0 = li * C::K / C::NLOAD, i1 = (li + 1) * C::K / C::NLOAD;
+        constexpr int NLD = C::NLOAD > 0 ? C::NLOAD : 1;
+        const int i0 = li * C::K / NLD, i1 = (li + 1) * C::K / NLD;
         src.template seg_coeffs<C>(scratch, r0, nr, lane, i0, i1);
         __syncwarp();
         if (li == 0) TR(2, 5);
@@ -487,7 +488,9 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
         }
         if (d == 0) TR(1, 7);
         src.template load_direct<C, RowBar<C::DW, BAR_DATA>>(c, r0, nr, S, Zp, Zp + C::NLT * C::DW * 32, scratch,
-                                                             d, lane, [](int) {});
+                                                             d, lane, [&](int i) {
+                                                               if (d == 0) TR(1, 10 + i);
+                                                             });
         if (d == 0) TR(1, 8);
       } else {
         if (d == 0) TR(1, 7);
