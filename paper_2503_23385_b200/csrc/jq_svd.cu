@@ -460,7 +460,7 @@ jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_
 // with JQ_SVD_V_OVERLAP=1 it runs on a second stream WHILE the sweeps go on: a sweep is
 // replayed once progress[0] says its log is out, and the kernel ends when progress[1]
 // (done) is set and nsweeps sweeps are replayed (the final, clean sweep is skipped).
-constexpr int SVDV_WARPS = 4, SVDV_BATCH = 4;
+constexpr int SVDV_WARPS = 2, SVDV_BATCH = 4;  // 2 warps per CTA: n = 256 rows on 128 SMs
 
 __global__ void __launch_bounds__(SVDV_WARPS * 32)
 jacobi_v_kernel(const double2* __restrict__ rlog, const int* nsweeps, const int* progress, int np,
@@ -511,14 +511,24 @@ jacobi_v_kernel(const double2* __restrict__ rlog, const int* nsweeps, const int*
 #pragma unroll
       for (int b = 0; b < SVDV_BATCH; ++b) {
         if (r0 + b >= r1s) break;
+        // the lane's (up to 4) disjoint pairs: every load first, then the rotations and
+        // the stores (one shared-memory round trip per round instead of one per pair)
+        double u[4], w[4];
+        int pp[4], qq[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          pp[k] = min(plo[k], phi[k]);
+          qq[k] = max(plo[k], phi[k]);
+          const bool act = lane + 32 * k < half;
+          u[k] = act ? row[pp[k]] : 0.0;
+          w[k] = act ? row[qq[k]] : 0.0;
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if (lane + 32 * k < half) {
-            const int p = min(plo[k], phi[k]), q = max(plo[k], phi[k]);
             const double c = cs[b][k].x, sn = cs[b][k].y;
-            const double u = row[p], w = row[q];
-            row[p] = c * u - sn * w;
-            row[q] = sn * u + c * w;
+            row[pp[k]] = c * u[k] - sn * w[k];
+            row[qq[k]] = sn * u[k] + c * w[k];
             plo[k] = plo[k] == 0 ? 0 : (plo[k] == np - 1 ? 1 : plo[k] + 1);
             phi[k] = phi[k] == np - 1 ? 1 : phi[k] + 1;
           }
@@ -639,6 +649,8 @@ int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values,
       JQ_CUDA(cudaEventRecord(ctx->aev[1], ctx->aux_stream));
       JQ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aev[1], 0));
     } else if (want_v) {
+      // (a shared-memory ring of TMA-fetched log stages, 8 rows per CTA, was measured
+      // slower: 0.70 vs 0.60 ms at n = 256 -- the replay is not bound by the log's L2 reads)
       jacobi_v_kernel<<<(unsigned)cdiv(n, SVDV_WARPS), SVDV_WARPS * 32, 0, ctx->stream>>>(rlog, nsw, nsw + 1, npc,
                                                                                         sig, v, (int)n);
       JQ_CHECK_LAUNCH(ctx);

@@ -186,8 +186,28 @@ struct DenseSrc {
     return (i < nrows && l < rcols) ? raw[i * rcols + l] : 0.0;
   }
   // direct chunk load (load_direct): global -> the C^T registers of the NW row warps
-  // (Bar::NW_), no shared-memory staging; the rows v0 .. v0 + nr - 1 (the rest zero)
+  // (Bar::NW_), no shared-memory staging; the rows v0 .. v0 + nr - 1 (the rest zero).
+  // Early form (warp-specialised leaf, the next chunk while this one is factored):
+  // early_ok / early_coefs / load_tile per tile as its registers free up / load_finish.
   static constexpr bool DIRECT = true;
+  __device__ bool early_ok(int64_t) const { return true; }
+  template <class C, int NW>
+  __device__ bool early_coefs(int64_t, int, double*, int, int) const { return true; }
+  template <class C>
+  __device__ void load_tile(double (&ct)[C::KWT][2], int64_t v0, int nr, int q, int warp, int lane) const {
+    const int g = lane >> 2, t = lane & 3, l = 8 * q + g;
+    const double* base = m + v0 * cols;
+#pragma unroll
+    for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int i = direct_row<C>(warp, t, it, b);
+        ct[it][b] = (i < nr && l < (int)cols) ? __ldg(base + (int64_t)i * cols + l) : 0.0;
+      }
+  }
+  template <class C, class Bar, class Mark>
+  __device__ void load_finish(double (&)[C::NLT][C::KWT][2], int64_t, int, double*, double*, double*, double*, int,
+                              int, bool, Mark) const {}
   template <class C, class Bar, class Mark>
   __device__ void load_direct(double (&c)[C::NLT][C::KWT][2], int64_t v0, int nr, double*, double*, double*,
                               double*, int warp, int lane, Mark) const {
@@ -416,56 +436,17 @@ struct FigaroSrc {
   // thread's offsets), wt: [NW][NP] double2, coef: c1 | c2 | mode per chunk row (3 K); all
   // three idle between chunks.  Chunks never cross m1pad (limit()).
   static constexpr bool DIRECT = true;
-  template <class C, class Bar, class Mark>
-  __device__ void load_direct(double (&c)[C::NLT][C::KWT][2], int64_t v0, int nr, double* S, double* lo, double* wt,
-                              double* coef, int warp, int lane, Mark mark) const {
-    static_assert(C::NLT <= 32, "one keep bit per tile");
-    constexpr int NW = Bar::NW_, NT = NW * 32;
-    const int g = lane >> 2, t = lane & 3, rt = warp * 32 + lane;
-    const int n1 = (int)fa.n1, n2 = (int)fa.n2;
-    int* cmode = reinterpret_cast<int*>(coef + 2 * C::K);
-    if (v0 < m1pad) {
-      // ---- top block rows: [sqrt(m2g) A_i | head(B_g)] (SPEC.md:193); no scan
-      for (int i = rt; i < C::K; i += NT) {
-        int gg = -1;
-        double m2g = 0.0;
-        if (i < nr) {
-          const int64_t r = v0 + i;
-          gg = fa.gid_a ? __ldg(fa.gid_a + r) : 0;
-          if (gg >= 0) m2g = fa.gid_a ? (double)__ldg(fa.b_count + gg) : (double)fa.m2_global;
-        }
-        const double rs2 = gg >= 0 && m2g > 0.0 ? rsqrt_nr(m2g) : 0.0;
-        coef[i] = m2g * rs2;
-        coef[C::K + i] = rs2;
-        cmode[i] = gg;
-      }
-      Bar::sync();
-      const double* ab = fa.a + v0 * fa.n1;
-#pragma unroll
-      for (int it = 0; it < C::KWT; ++it)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int i = direct_row<C>(warp, t, it, b);
-          const int gg = cmode[i];
-          const double c1v = coef[i], c2v = coef[C::K + i];
-#pragma unroll
-          for (int q = 0; q < C::NLT; ++q) {
-            const int l = 8 * q + g;
-            double v = 0.0;
-            if (i < nr && gg >= 0) {
-              if (l < n1) v = __ldg(ab + (int64_t)i * n1 + l) * c1v;
-              else if (l < n) v = __ldg(fa.b_totals + (int64_t)gg * n2 + (l - n1)) * c2v;
-            }
-            c[q][it][b] = v;
-          }
-        }
-      Bar::sync();  // coef / cmode read before the next chunk rewrites them
-      return;
-    }
+  // the early form covers B-part chunks (the A part's values need the coefficients first)
+  __device__ bool early_ok(int64_t v0) const { return v0 >= m1pad; }
+  // B part: per-row coefficients, one thread per chunk row: c1, c2 -> coef, the row mode
+  // -> coef + 2K (int); returns this thread's "only tail rows" flag
+  template <class C, int NW>
+  __device__ bool early_coefs(int64_t v0, int nr, double* coef, int warp, int lane) const {
+    const int rt = warp * 32 + lane;
     const int64_t b0 = v0 - m1pad;
-    // per-row coefficients, one thread per chunk row: c1, c2 -> coef, the row mode -> cmode
+    int* cmode = reinterpret_cast<int*>(coef + 2 * C::K);
     bool tails = true;  // every row a tail row (or past the chunk)
-    for (int i = rt; i < C::K; i += NT) {
+    for (int i = rt; i < C::K; i += NW * 32) {
       int md = 0;
       double c1v = 0.0, c2v = 0.0;
       if (i < nr) {
@@ -497,16 +478,33 @@ struct FigaroSrc {
       coef[C::K + i] = c2v;
       cmode[i] = md;
     }
-    const double* bb = fa.b + b0 * fa.n2 - n1;
+    return tails;
+  }
+  // B part: the raw rows of tile q (columns 8q .. 8q+7) into this thread's slots
+  template <class C>
+  __device__ void load_tile(double (&ct)[C::KWT][2], int64_t v0, int nr, int q, int warp, int lane) const {
+    const int g = lane >> 2, t = lane & 3, l = 8 * q + g;
+    const int n1 = (int)fa.n1, n2 = (int)fa.n2;
+    const double* bb = fa.b + (v0 - m1pad) * fa.n2 - n1;
 #pragma unroll
-    for (int q = 0; q < C::NLT; ++q)
+    for (int it = 0; it < C::KWT; ++it)
 #pragma unroll
-      for (int it = 0; it < C::KWT; ++it)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int i = direct_row<C>(warp, t, it, b), l = 8 * q + g;
-          c[q][it][b] = (i < nr && l >= n1 && l < n) ? __ldg(bb + (int64_t)i * n2 + l) : 0.0;
-        }
+      for (int b = 0; b < 2; ++b) {
+        const int i = direct_row<C>(warp, t, it, b);
+        ct[it][b] = (i < nr && l >= n1 && l < n) ? __ldg(bb + (int64_t)i * n2 + l) : 0.0;
+      }
+  }
+  // B part, raw rows and coefficients in place: the scan and the transform
+  template <class C, class Bar, class Mark>
+  __device__ void load_finish(double (&c)[C::NLT][C::KWT][2], int64_t v0, int nr, double* S, double* lo, double* wt,
+                              double* coef, int warp, int lane, bool tails, Mark mark) const {
+    static_assert(C::NLT <= 32, "one keep bit per tile");
+    constexpr int NW = Bar::NW_, NT = NW * 32;
+    const int g = lane >> 2, t = lane & 3, rt = warp * 32 + lane;
+    const int n1 = (int)fa.n1;
+    const int* cmode = reinterpret_cast<const int*>(coef + 2 * C::K);
+    (void)v0;
+    (void)nr;
     const bool fast = Bar::sync_and(tails);
     unsigned kb = 0, wb = 0;  // bit 2 it + b: keep S / add x
 #pragma unroll
@@ -589,23 +587,91 @@ struct FigaroSrc {
         c1r[it][b] = coef[i];
         c2r[it][b] = coef[C::K + i];
       }
+    if (fast) {
 #pragma unroll
-    for (int q = 0; q < C::NLT; ++q) {
-      const int l = 8 * q + g;
-      if (l >= n1 && l < n) {
-        double sv = (((kx >> q) & 1) ? wt[2 * (warp * C::NP + l)] : 0.0) + lo[q * NT + rt];
+      for (int q = 0; q < C::NLT; ++q) {
+        const int l = 8 * q + g;
+        if (l >= n1 && l < n) {
+          double sv = wt[2 * (warp * C::NP + l)] + lo[q * NT + rt];
 #pragma unroll
-        for (int it = 0; it < C::KWT; ++it)
+          for (int it = 0; it < C::KWT; ++it)
 #pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            const double x = c[q][it][b];
-            c[q][it][b] = fma(c1r[it][b], x, -c2r[it][b] * sv);
-            if (fast) sv += x;
-            else sv = (((kb >> (2 * it + b)) & 1) ? sv : 0.0) + (((wb >> (2 * it + b)) & 1) ? x : 0.0);
-          }
+            for (int b = 0; b < 2; ++b) {
+              const double x = c[q][it][b];
+              c[q][it][b] = fma(c1r[it][b], x, -c2r[it][b] * sv);
+              sv += x;
+            }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < C::NLT; ++q) {
+        const int l = 8 * q + g;
+        if (l >= n1 && l < n) {
+          double sv = (((kx >> q) & 1) ? wt[2 * (warp * C::NP + l)] : 0.0) + lo[q * NT + rt];
+#pragma unroll
+          for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              const double x = c[q][it][b];
+              c[q][it][b] = fma(c1r[it][b], x, -c2r[it][b] * sv);
+              sv = (((kb >> (2 * it + b)) & 1) ? sv : 0.0) + (((wb >> (2 * it + b)) & 1) ? x : 0.0);
+            }
+        }
       }
     }
     Bar::sync();  // wt / lo / coef read before the caller reuses them
+  }
+  template <class C, class Bar, class Mark>
+  __device__ void load_direct(double (&c)[C::NLT][C::KWT][2], int64_t v0, int nr, double* S, double* lo, double* wt,
+                              double* coef, int warp, int lane, Mark mark) const {
+    constexpr int NW = Bar::NW_, NT = NW * 32;
+    const int g = lane >> 2, t = lane & 3, rt = warp * 32 + lane;
+    const int n1 = (int)fa.n1, n2 = (int)fa.n2;
+    int* cmode = reinterpret_cast<int*>(coef + 2 * C::K);
+    if (v0 < m1pad) {
+      // ---- top block rows: [sqrt(m2g) A_i | head(B_g)] (SPEC.md:193); no scan
+      for (int i = rt; i < C::K; i += NT) {
+        int gg = -1;
+        double m2g = 0.0;
+        if (i < nr) {
+          const int64_t r = v0 + i;
+          gg = fa.gid_a ? __ldg(fa.gid_a + r) : 0;
+          if (gg >= 0) m2g = fa.gid_a ? (double)__ldg(fa.b_count + gg) : (double)fa.m2_global;
+        }
+        const double rs2 = gg >= 0 && m2g > 0.0 ? rsqrt_nr(m2g) : 0.0;
+        coef[i] = m2g * rs2;
+        coef[C::K + i] = rs2;
+        cmode[i] = gg;
+      }
+      Bar::sync();
+      const double* ab = fa.a + v0 * fa.n1;
+#pragma unroll
+      for (int it = 0; it < C::KWT; ++it)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int i = direct_row<C>(warp, t, it, b);
+          const int gg = cmode[i];
+          const double c1v = coef[i], c2v = coef[C::K + i];
+#pragma unroll
+          for (int q = 0; q < C::NLT; ++q) {
+            const int l = 8 * q + g;
+            double v = 0.0;
+            if (i < nr && gg >= 0) {
+              if (l < n1) v = __ldg(ab + (int64_t)i * n1 + l) * c1v;
+              else if (l < n) v = __ldg(fa.b_totals + (int64_t)gg * n2 + (l - n1)) * c2v;
+            }
+            c[q][it][b] = v;
+          }
+        }
+      Bar::sync();  // coef / cmode read before the next chunk rewrites them
+      return;
+    }
+    const bool tails = early_coefs<C, NW>(v0, nr, coef, warp, lane);
+    mark(5);
+#pragma unroll
+    for (int q = 0; q < C::NLT; ++q) load_tile<C>(c[q], v0, nr, q, warp, lane);
+    load_finish<C, Bar>(c, v0, nr, S, lo, wt, coef, warp, lane, tails, mark);
   }
 
   // prep by ONE warp (the loader warp of tsqr_ws_kernel): per-row scalars, then the
@@ -2041,7 +2107,13 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t 
   }();
   static const int debug_flags = [] {  // JQ_TSQR_DEBUG=8: ignore %warpid (fallback role layout; tests)
     const char* e = getenv("JQ_TSQR_DEBUG");
-    return e ? atoi(e) & 8 : 0;
+    int f = e ? atoi(e) & 8 : 0;
+    // JQ_TSQR_PREFETCH=none | whole: the direct-load leaf's L2 prefetch of the next chunk
+    // off / as one bulk prefetch (default: 32 pieces)
+    const char* pf = getenv("JQ_TSQR_PREFETCH");
+    if (pf && strcmp(pf, "none") == 0) f |= 1024;
+    if (pf && strcmp(pf, "whole") == 0) f |= 2048;
+    return f;
   }();
   align = std::max<int64_t>(align, 8);
   int64_t max_ctas = int64_t(ctx->sms) * occ;
@@ -2103,6 +2175,8 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
         return run_stream_ws<CfgS<32, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
       return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 64:
+      // (8 warps with 6 data warps x 40 rows -- 240-row chunks, 255 registers -- measured
+      // slower at C4: 155.9 vs 144.3 ms)
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
       return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 128:

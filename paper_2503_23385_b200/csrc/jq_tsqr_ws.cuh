@@ -481,10 +481,19 @@ tsqr_ws2_kernel(Src src, int64_t rows_per_cta, int64_t total_rows, double* __res
       const int rcol = src.rc(r0);
       if constexpr (C::DIRECT) {
         // the partials' buffer holds the load's scan state: free since B of the last panel
-        if (d == 0 && lane == 0 && (flags & 1) && r1 < row_end) {
+        // the next chunk into L2 meanwhile: by default 32 bulk prefetches (one per lane of
+        // data warp 0); flag 2048: one bulk prefetch of the whole chunk; 1024: none
+        if (d == 0 && (flags & 1) && !(flags & 1024) && r1 < row_end) {
           const int64_t r2 = chunk_end(r1);
           const int nr2 = chunk_rows(r1, r2);
-          if (nr2 > 0) l2_prefetch(src.ptr(r1), uint32_t(nr2) * uint32_t(src.rc(r1)) * 8u & ~15u);
+          const uint32_t bytes = uint32_t(nr2) * uint32_t(src.rc(r1)) * 8u & ~15u;
+          const char* base = reinterpret_cast<const char*>(src.ptr(r1));
+          if (flags & 2048) {
+            if (lane == 0) l2_prefetch(base, bytes);
+          } else {
+            const uint32_t piece = ((bytes + 31u) / 32u + 15u) & ~15u, off = uint32_t(lane) * piece;
+            if (off < bytes) l2_prefetch(base + off, min(piece, bytes - off));
+          }
         }
         if (d == 0) TR(1, 7);
         src.template load_direct<C, RowBar<C::DW, BAR_DATA>>(c, r0, nr, S, Zp, Zp + C::NLT * C::DW * 32, scratch,

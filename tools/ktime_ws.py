@@ -41,7 +41,7 @@ evnames = {(0, 1): "chain start", (0, 2): "chain done", (0, 3): "chain B pass", 
            (0, 5): "chain Gnext", (1, 1): "d0 V ok", (1, 2): "d0 reduce done", (1, 3): "d0 BAR_DATA pass",
            (1, 4): "d0 applies done", (1, 5): "d0 step4 done", (1, 6): "d0 B pass", (1, 7): "d0 wait READY / load start",
            (1, 8): "d0 READY ok / load done",
-           (1, 17): "d0 load: coefs + loads issued", (1, 18): "d0 load: scan", (1, 19): "d0 load: carry-ins", (2, 1): "loader FREE ok", (2, 2): "loader TMA done", (2, 3): "loader prep done",
+           (1, 15): "d0 load: coefs", (1, 17): "d0 load: loads issued + barrier", (1, 18): "d0 load: scan", (1, 19): "d0 load: carry-ins", (2, 1): "loader FREE ok", (2, 2): "loader TMA done", (2, 3): "loader prep done",
            (2, 4): "loader BAR raw", (2, 5): "loader coeffs done", (2, 6): "loader pass1 done", (2, 7): "loader BAR seg"}
 t0 = ev[0][0] if ev else 0
 prev = t0
