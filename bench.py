@@ -47,7 +47,11 @@ METRIC = "join rows/sec (m1*m2/t), time-to-R"
 NCU_TRAFFIC = {(4, "footnote"): {"bytes": 51.217598e9 + 16.129024e6,
                                  "note": "first tsqr_ws2_kernel launch (side A, carry-free leaves, round-2 final capture "
                                          "profiles/r02_ncu_ws2_c4.md / _final_raw.csv, 71.90 ms under ncu): its own "
-                                         "1e8 x 64 f64 rows = 51.2e9 algorithmic bytes, every byte read once"}}
+                                         "1e8 x 64 f64 rows = 51.2e9 algorithmic bytes, every byte read once"},
+               (5, "footnote"): {"bytes": 1.065093e9 + 6.2784e6,
+                                 "note": "first tsqr_ws2_kernel<CfgS<128,8,6,1,24,direct>> launch (side A, carry-free "
+                                         "leaves; profiles/r02_ncu_ws128_c5.md, 2.525 ms under ncu): its own 1e6 x 128 "
+                                         "f64 rows = 1.024e9 algorithmic bytes (+4 %)"}}
 
 
 def peaks():
@@ -394,10 +398,17 @@ def main():
         # DRAM traffic of one leaf launch from the ncu --set full capture of this config
         # (profiles/r01_ncu_ws2_c4.md): footnote C4, one side = 1e8 x 64 f64 rows
         traffic = NCU_TRAFFIC.get((args.config, args.variant))
-        roof = {"kernel": ("tsqr_ws2_kernel (warp-specialised TSQR leaf: loader warp builds the Claim-1 / tail rows, "
-                           "chain warp runs the Cholesky panel factorisation, 12 data warps do the DMMA updates)"
-                           if args.variant == "footnote" and n <= 64 else
-                           "tsqr_kernel (CTA-wide TSQR leaf, Gram-panel chain + explicit fallback, DMMA updates)"),
+        leaf_n = n if args.variant == "footnote" else 2 * n  # columns of one leaf
+        if leaf_n <= 64:
+            kname = ("tsqr_ws2_kernel (warp-specialised TSQR leaf: loader warp builds the Claim-1 / tail rows, "
+                     "chain warp runs the Cholesky panel factorisation, 12 data warps do the DMMA updates)")
+        elif leaf_n <= 128:
+            kname = ("tsqr_ws2_kernel<CfgS<128,8,6,1,24,direct>> (warp-specialised TSQR leaf: 6 data warps load "
+                     "their 24 rows straight into the DMMA layout and run the tail transform there, chain warp "
+                     "alone on SM sub-partition 0)")
+        else:
+            kname = "tsqr_kernel (CTA-wide TSQR leaf, Cholesky / Gram panel chain + explicit fallback, DMMA updates)"
+        roof = {"kernel": kname,
                 "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS,
                 "traffic": traffic["bytes"] if traffic else None,
@@ -417,7 +428,8 @@ def main():
             # Cartesian footnote default: carry-free leaves, no prefix-scan pass in the step
             roof_hbm = {"kernel": None, "bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s",
                         "note": "no HBM-bound pass in this step: the carry-free TSQR leaves transform their own "
-                                "row blocks in the loader warp (every input byte read once, by TMA); the head/tail "
+                                "row blocks inside the leaf (N <= 64: the loader warp, from a TMA copy; N = 128: the data "
+                                "warps, from their direct loads; every input byte read once); the head/tail "
                                 "kernels' own roofline (reduced-matrix API, keyed configs) is in "
                                 "profiles/r01_ncu_headtail.md and the C3 line"}
         if gbs and gbs_kernel:
