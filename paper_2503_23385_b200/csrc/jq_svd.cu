@@ -548,6 +548,64 @@ jacobi_v_kernel(const double2* __restrict__ rlog, const int* nsweeps, const int*
   }
 }
 
+// The default (after-sweeps) V replay: FOUR warps per row of V, lane l of warp k doing
+// pair 32 k + l of every round, a 128-thread named barrier between rounds.  A round is
+// then one load / rotate / store per lane (the one-warp replay above does four pairs per
+// lane and is bound by that serial chain: ~400 cycles per round).  The log is read
+// SVDV4_D rounds ahead into registers.  Same element arithmetic, in the same order, as
+// jacobi_v_kernel (every pair's rotation is independent of the others in its round).
+constexpr int SVDV4_ROWS = 2, SVDV4_D = 8;
+
+__global__ void __launch_bounds__(SVDV4_ROWS * 128)
+jacobi_v4_kernel(const double2* __restrict__ rlog, const int* nsweeps, int np, const double* sig,
+                 double* __restrict__ vout, int n_out) {
+  __shared__ double rows[SVDV4_ROWS][256];
+  const int grp = threadIdx.x >> 7, k = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31, gt = threadIdx.x & 127;
+  const int i = blockIdx.x * SVDV4_ROWS + grp, half = np >> 1, pi = lane + 32 * k;
+  const bool act = pi < half;
+  const int total = __ldcg(nsweeps) * (np - 1);  // the final, clean sweep is not replayed
+  double* row = rows[grp];
+  for (int j = gt; j < np; j += 128) row[j] = i == j ? 1.0 : 0.0;
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+  int plo = pi, phi = np - 1 - pi;
+  double2 nx[SVDV4_D];
+  auto load = [&](int r0) {
+#pragma unroll
+    for (int b = 0; b < SVDV4_D; ++b)
+      nx[b] = (act && r0 + b < total) ? __ldcg(rlog + (size_t)(r0 + b) * half + pi) : make_double2(1.0, 0.0);
+  };
+  load(0);
+  for (int r0 = 0; r0 < total; r0 += SVDV4_D) {
+    double2 cs[SVDV4_D];
+#pragma unroll
+    for (int b = 0; b < SVDV4_D; ++b) cs[b] = nx[b];
+    if (r0 + SVDV4_D < total) load(r0 + SVDV4_D);
+#pragma unroll
+    for (int b = 0; b < SVDV4_D; ++b) {
+      if (r0 + b >= total) break;
+      if (act) {
+        const int p = min(plo, phi), q = max(plo, phi);
+        const double u = row[p], w = row[q];
+        row[p] = cs[b].x * u - cs[b].y * w;
+        row[q] = cs[b].y * u + cs[b].x * w;
+        plo = plo == 0 ? 0 : (plo == np - 1 ? 1 : plo + 1);
+        phi = phi == np - 1 ? 1 : phi + 1;
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+    }
+  }
+  if (i >= n_out) return;
+  for (int j = gt; j < np; j += 128) {
+    const double sj = __ldcg(sig + j);
+    int rk = 0;
+    for (int kk = 0; kk < np; ++kk) {
+      const double sk = __ldcg(sig + kk);
+      rk += (sk > sj) || (sk == sj && kk < j);
+    }
+    if (rk < n_out) vout[(size_t)i * n_out + rk] = row[j];
+  }
+}
+
 // A_cm[j*np + i] = R[i*n + j] (zero padded to np), V = I
 __global__ void svd_init_kernel(const double* __restrict__ r, int n, int np, double* __restrict__ A,
                                 double* __restrict__ V) {
@@ -649,10 +707,19 @@ int svd_dev(jq_ctx* ctx, const double* r, int64_t n, int want_v, double* values,
       JQ_CUDA(cudaEventRecord(ctx->aev[1], ctx->aux_stream));
       JQ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aev[1], 0));
     } else if (want_v) {
-      // (a shared-memory ring of TMA-fetched log stages, 8 rows per CTA, was measured
-      // slower: 0.70 vs 0.60 ms at n = 256 -- the replay is not bound by the log's L2 reads)
-      jacobi_v_kernel<<<(unsigned)cdiv(n, SVDV_WARPS), SVDV_WARPS * 32, 0, ctx->stream>>>(rlog, nsw, nsw + 1, npc,
-                                                                                        sig, v, (int)n);
+      // four warps per row (a shared-memory ring of TMA-fetched log stages for the one-warp
+      // replay was measured slower: 0.70 vs 0.60 ms at n = 256 -- the replay is bound by
+      // its per-round chain, not by the log's L2 reads).  JQ_SVD_V1=1: the one-warp replay.
+      static const bool v1 = [] {
+        const char* e = getenv("JQ_SVD_V1");
+        return e && e[0] == '1';
+      }();
+      if (v1)
+        jacobi_v_kernel<<<(unsigned)cdiv(n, SVDV_WARPS), SVDV_WARPS * 32, 0, ctx->stream>>>(rlog, nsw, nsw + 1, npc,
+                                                                                          sig, v, (int)n);
+      else
+        jacobi_v4_kernel<<<(unsigned)cdiv(n, SVDV4_ROWS), SVDV4_ROWS * 128, 0, ctx->stream>>>(rlog, nsw, npc, sig, v,
+                                                                                             (int)n);
       JQ_CHECK_LAUNCH(ctx);
     }
     return JQ_OK;

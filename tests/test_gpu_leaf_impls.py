@@ -48,3 +48,13 @@ def test_svd_coop_impl_parity():
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "svd"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_svd_v_one_warp_replay_parity():
+    # JQ_SVD_V1=1: the one-warp-per-row V replay instead of the four-warp default
+    e = dict(os.environ, JQ_SVD_V1="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "svd"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
