@@ -82,7 +82,10 @@ struct Cfg {
   static constexpr int KW = K / WARPS;      // rows per warp
   static constexpr int KWT = KW / 8;        // row tiles per warp
   static constexpr bool R_SMEM = NP <= 128;
-  static constexpr int MIN_CTAS = NP <= 64 ? 2 : 1;  // two independent chains per SM when they fit
+  // one CTA per SM (255 registers): this kernel is the tree combine of every leaf width
+  // (and the JQ_TSQR_IMPL=cta leaf); at 2 CTAs per SM its N <= 64 instantiations spilled
+  // in the panel loop (192-224 bytes of stack)
+  static constexpr int MIN_CTAS = 1;
   // R packed by 8-row panels: panel p holds rows 8p..8p+7, columns 8p..NP-1,
   // row stride NP - 8p + 2 (== 2 or 10 mod 16: conflict-free DMMA fragment access)
   __host__ __device__ static constexpr int rp_off(int p) { return 8 * (p * (NP + 2) - 4 * p * (p - 1)); }
