@@ -45,6 +45,17 @@ __global__ void __launch_bounds__(256, 4) segscan_tile_narrow_kernel(
   segscan_tile_narrow<SL == 1 ? 16 : 8, SL>(x, rows, cols, gid, t, agg, flag, totals, lane);  // 4 KB per warp in flight
 }
 
+// keyed, <= 16 columns: several rows per warp load (32 rows in flight per warp)
+template <int CP>
+__global__ void __launch_bounds__(256, 2) segscan_tile_tiny_kernel(
+    const double* __restrict__ x, int64_t rows, int cols, const int32_t* __restrict__ gid,
+    int64_t ntiles, double* __restrict__ agg, int* __restrict__ flag, double* __restrict__ totals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= ntiles) return;
+  segscan_tile_tiny<CP>(x, rows, cols, gid, t, agg, flag, totals, lane);
+}
+
 static bool narrow_tiles() {
   static const bool on = [] {
     const char* e = getenv("JQ_SEGSCAN_GENERIC");
@@ -185,7 +196,17 @@ int segscan_tiles(jq_ctx* ctx, const SideScan& side) {
   const int k = ctx->tile_launches < 4 && ctx->tev[0] ? ctx->tile_launches : -1;
   if (k >= 0) cudaEventRecord(ctx->tev[2 * k], ctx->stream);
   const unsigned grid = (unsigned)cdiv(side.ntiles, wpb);
-  if (narrow_tiles() && side.cols <= 32)
+  static const bool tiny = [] {  // JQ_SEGSCAN_TINY=0: keyed <= 16 columns on the narrow pass (A/B)
+    const char* e = getenv("JQ_SEGSCAN_TINY");
+    return !(e && e[0] == '0');
+  }();
+  if (narrow_tiles() && tiny && side.gid && side.cols <= 8)
+    segscan_tile_tiny_kernel<8><<<grid, 32 * wpb, 0, ctx->stream>>>(
+        side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
+  else if (narrow_tiles() && tiny && side.gid && side.cols <= 16)
+    segscan_tile_tiny_kernel<16><<<grid, 32 * wpb, 0, ctx->stream>>>(
+        side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
+  else if (narrow_tiles() && side.cols <= 32)
     segscan_tile_narrow_kernel<1><<<grid, 32 * wpb, 0, ctx->stream>>>(
         side.x, side.rows, side.cols, side.gid, side.ntiles, side.agg, side.flag, side.totals);
   else if (narrow_tiles() && side.cols <= 64)

@@ -262,4 +262,63 @@ __device__ __forceinline__ void segscan_tile_narrow(const double* __restrict__ x
   if (lane == 0) flag[t] = any_start;
 }
 
+// Keyed tile pass for <= CP columns (CP = 8 or 16): a warp load covers R = 32 / CP rows
+// (lane = (row slot, column)), 32 rows per iteration in flight -- twice the bytes of the
+// narrow pass, whose lanes 16-31 sit idle on a 16-column row -- and lanes 0 .. cols-1 run
+// the same row-by-row segment logic on the values shuffled to them: the same additions in
+// the same order as segscan_tile_narrow, so the same bits.
+template <int CP>
+__device__ __forceinline__ void segscan_tile_tiny(const double* __restrict__ x, int64_t rows, int cols,
+                                                  const int32_t* __restrict__ gid, int64_t t,
+                                                  double* __restrict__ agg, int* __restrict__ flag,
+                                                  double* __restrict__ totals, int lane) {
+  constexpr int R = 32 / CP, RB = 32, NI = RB / R;
+  const int64_t r0 = t * TILE_ROWS, r1 = min(rows, r0 + TILE_ROWS);
+  const int slot = lane / CP, col = lane % CP;
+  const bool h = lane < cols;  // a processing lane: slot 0 and a real column
+  int seg = gid[r0];
+  int any_start = (r0 == 0) || (gid[r0 - 1] != seg);
+  double s = 0.0;
+  auto row_step = [&](int64_t rr, int sr, double v) {
+    const bool start = (rr == 0) || (rr > r0 && sr != seg);
+    if (start && rr > r0) {
+      if (seg >= 0 && h) totals[(int64_t)seg * cols + lane] = s;
+      any_start = 1;
+    }
+    seg = sr;
+    s = start ? v : s + v;
+  };
+  int64_t r = r0;
+  for (; r + RB <= r1; r += RB) {
+    int g[RB];
+    double v[NI];  // load u: row r + u R + slot, column col
+#pragma unroll
+    for (int u = 0; u < RB; ++u) g[u] = gid[r + u];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) v[u] = col < cols ? __ldg(x + (r + (int64_t)u * R + slot) * cols + col) : 0.0;
+    bool uniform = r != 0;
+#pragma unroll
+    for (int u = 0; u < RB; ++u) uniform = uniform && g[u] == seg;
+    if (uniform) {
+#pragma unroll
+      for (int u = 0; u < NI; ++u)
+#pragma unroll
+        for (int j = 0; j < R; ++j) s = s + __shfl_sync(0xffffffffu, v[u], j * CP + col);
+    } else {
+#pragma unroll
+      for (int u = 0; u < NI; ++u)
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          row_step(r + u * R + j, g[u * R + j], __shfl_sync(0xffffffffu, v[u], j * CP + col));
+    }
+  }
+  for (; r < r1; ++r) row_step(r, gid[r], h ? __ldg(x + r * cols + lane) : 0.0);
+  const bool ends_here = (r1 == rows) || (gid[r1] != seg);
+  if (h) {
+    if (ends_here && seg >= 0) totals[(int64_t)seg * cols + lane] = s;
+    agg[t * cols + lane] = s;
+  }
+  if (lane == 0) flag[t] = any_start;
+}
+
 }  // namespace jq

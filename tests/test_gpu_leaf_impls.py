@@ -58,3 +58,13 @@ def test_svd_v_one_warp_replay_parity():
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "svd"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_segscan_narrow_pass_parity():
+    # JQ_SEGSCAN_TINY=0: keyed <= 16-column tile passes on the one-row-per-load narrow kernel
+    e = dict(os.environ, JQ_SEGSCAN_TINY="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "figaro or head_tail or reduce"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -182,8 +182,14 @@ def variant(request, P):
     # sides with different leaf counts: separate trees), an odd leaf count (147 leaves,
     # three dense elements, both trees in shared launches), a partial last block
     (200000, 8, 150000, 12, None), (150001, 64, 150001, 64, None),
-    # sides of different leaf widths (NP 64 ws2 leaves / NP 128 CTA-wide leaves)
-    (200000, 40, 150000, 100, None)])
+    # sides of different leaf widths (NP 64 ws2 leaves / NP 128 ws2 direct-load leaves)
+    (200000, 40, 150000, 100, None),
+    # keyed tile passes of <= 16 columns (several rows per warp load), groups spanning
+    # 1024-row tiles, 1 / 3 / 8 / 9 / 16 columns
+    (5000, 1, 4000, 3, 700), (6000, 8, 5000, 9, 40), (9000, 16, 7000, 1, 5),
+    # N = 128 direct-load leaves on keyed joins: group starts inside chunks, rows
+    # without a partner group
+    (9000, 70, 8000, 58, 900), (20000, 128, 3000, 128, 17)])
 def test_figaro_r_matches_oracle(P, variant, m1, n1, m2, n2, groups):
     rng = np.random.default_rng(m1 + 3 * m2 + n1 + (groups or 0))
     a, b = rand_tables(rng, m1, n1, m2, n2, groups)
