@@ -290,7 +290,7 @@ __device__ __forceinline__ void pos_home(int k, int np, int& cta, int& slot) {
   slot = (k < half ? 0 : WPC) + pi % WPC;
 }
 
-template <int WPC>
+template <int WPC, int NKC = 0>  // NKC > 0: np = 32 NKC at compile time (the row bounds fold away)
 __global__ void __launch_bounds__(WPC * 32, 1)
 jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_sweeps, int* flags,
                       double* __restrict__ sig, double2* __restrict__ rlog, int* __restrict__ nsweeps,
@@ -335,7 +335,7 @@ jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_
   double* const whi0 = dhi_c == rank ? cols + dhi_s * np : cluster.map_shared_rank(cols + dhi_s * np, dhi_c);
   const size_t bufsz = size_t(COLS) * np;
   constexpr int RPL = 256 / 32;  // rows per lane (np <= 256, a multiple of 32: warp-uniform bounds)
-  const int nk = np >> 5;
+  const int nk = NKC > 0 ? NKC : np >> 5;
   cluster.sync();
 
   int sweep = 0, cur = 0;
@@ -624,10 +624,19 @@ size_t svd_ws_bytes(int64_t n) {
 
 // one cluster over the np/2 pairs: 8 warps per CTA (a 16-CTA cluster at np = 256, opt-in
 // non-portable size), else 16 warps per CTA when the device refuses clusters above 8
+static bool svd_generic() {  // JQ_SVD_GENERIC=1: the runtime-np cluster kernel only (A/B)
+  static const bool g = [] {
+    const char* e = getenv("JQ_SVD_GENERIC");
+    return e && e[0] == '1';
+  }();
+  return g;
+}
+
 template <int WPC>
 static int launch_cluster_wpc(jq_ctx* ctx, const double* A, int np, double* sig, double2* rlog, int* nsw,
                               double* values, int n_out) {
-  auto kern = jacobi_cluster_kernel<WPC>;
+  // np = 256 (n in 225..256, C5's 128 + 128) gets the compile-time row count
+  auto kern = np == 256 && !svd_generic() ? jacobi_cluster_kernel<WPC, 8> : jacobi_cluster_kernel<WPC>;
   const int nct = (np / 2 + WPC - 1) / WPC;
   const size_t smem = size_t(2) * 2 * WPC * np * sizeof(double) + size_t(np - 1) * WPC * sizeof(double2);
   JQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

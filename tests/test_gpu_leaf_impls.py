@@ -68,3 +68,13 @@ def test_segscan_narrow_pass_parity():
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "figaro or head_tail or reduce"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_svd_generic_cluster_kernel_parity():
+    # JQ_SVD_GENERIC=1: the runtime-np cluster kernel also at np = 256
+    e = dict(os.environ, JQ_SVD_GENERIC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "svd"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
