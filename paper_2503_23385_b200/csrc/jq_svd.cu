@@ -290,6 +290,11 @@ __device__ __forceinline__ void pos_home(int k, int np, int& cta, int& slot) {
   slot = (k < half ? 0 : WPC) + pi % WPC;
 }
 
+#ifndef JQ_SVD_ZETA_ROT
+constexpr bool kFastRot = true;  // the two-MUFU rotation scalars (-DJQ_SVD_ZETA_ROT: the zeta form, A/B)
+#else
+constexpr bool kFastRot = false;
+#endif
 template <int WPC, int NKC = 0>  // NKC > 0: np = 32 NKC at compile time (the row bounds fold away)
 __global__ void __launch_bounds__(WPC * 32, 1)
 jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_sweeps, int* flags,
@@ -367,16 +372,28 @@ jacobi_cluster_kernel(const double* __restrict__ A, int np, double tol, int max_
       const bool rot = !(al <= tiny || be <= tiny || ga == 0.0 || ga * ga < tol2 * (al * be));
       double c = 1.0, sn = 0.0;
       if (rot) {
-        const double zeta = (be - al) * rcp_nr(2.0 * ga);
-        const double az = fabs(zeta);
+        // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = d / e (d = be - al, e = 2 ga),
+        // as sign(d) e / (|d| + sqrt(d^2 + e^2)): one reciprocal square root and one
+        // reciprocal on the chain instead of two of each (the warp-uniform branch keeps
+        // the zeta form where d^2 + e^2 could leave the double range)
+        const double d = be - al, e = 2.0 * ga;
+        const double ad = fabs(d), ae = fabs(e);
         double t;
-        if (az < 1e100) {
-          const double q = fma(az, az, 1.0);
-          t = rcp_nr(fma(q, rsqrt_nr(q), az));  // 1 / (|zeta| + sqrt(1 + zeta^2))
+        if (!(kFastRot && ad < 1e150 && ae < 1e150 && ae > 1e-150)) {
+          const double zeta = d * rcp_nr(e);
+          const double az = fabs(zeta);
+          if (az < 1e100) {
+            const double q = fma(az, az, 1.0);
+            t = rcp_nr(fma(q, rsqrt_nr(q), az));  // 1 / (|zeta| + sqrt(1 + zeta^2))
+          } else {
+            t = 0.5 * rcp_nr(az);
+          }
+          t = zeta >= 0.0 ? t : -t;
         } else {
-          t = 0.5 * rcp_nr(az);
+          const double h = fma(d, d, e * e);
+          t = e * rcp_nr(fma(h, rsqrt_nr(h), ad));  // e / (|d| + sqrt(d^2 + e^2))
+          t = (d >= 0.0) == (e >= 0.0) ? fabs(t) : -fabs(t);  // the sign of zeta = d / e
         }
-        t = zeta >= 0.0 ? t : -t;
         c = rsqrt_nr(fma(t, t, 1.0));
         sn = c * t;
 #pragma unroll
