@@ -338,6 +338,23 @@ static int figaro_r_footnote_blocks(jq_ctx* ctx, const double* a, int64_t m1, in
   return rc;
 }
 
+// JQ_FOOTNOTE_SERIAL_TREES=1: the keyed footnote's side trees on the main stream, after
+// the leaves and before the head rows (A/B)
+static bool serial_trees() {
+  static const bool on = [] {
+    const char* e = getenv("JQ_FOOTNOTE_SERIAL_TREES");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+static int ensure_aux(jq_ctx* ctx) {
+  if (!ctx->aux_stream) {
+    JQ_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->aev) JQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return JQ_OK;
+}
+
 static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64_t n1, const int64_t* ka,
                                  const double* b, int64_t m2, int64_t n2, const int64_t* kb, double* r_out) {
   const bool keyed = ka != nullptr;
@@ -380,6 +397,11 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   // tails of A scaled by sqrt(m2g): the "B-part" of a source with an empty A-part
   FigaroArgs fa{};
   LeafSet leaves_a{};
+  bool trees_on_aux = false;  // the side trees run on the aux stream (joined before the stack)
+  auto join_trees = [&]() {
+    if (trees_on_aux) cudaStreamWaitEvent(ctx->stream, ctx->aev[1], 0);
+    trees_on_aux = false;
+  };
   if (n1 > 0) {
     fa.b = a; fa.m2 = m1; fa.n2 = n1;
     fa.gid_b = keyed ? gr.gid_a : nullptr;
@@ -408,7 +430,23 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
     if (n1 > 0) {
       LeafSet leaves_b{};
       rc = figaro_tsqr_leaves(ctx, fb, &leaves_b);
-      if (!rc) rc = tsqr_finish_pair(ctx, leaves_a, leaves_b, ra, rb);
+      if (!rc && ng > FOOTNOTE_GIVENS_MAX_HEADS && !serial_trees()) {
+        // the two sides' trees (latency-bound, a few CTAs per level) on the aux stream,
+        // beside the head rows' TSQR on this one; joined before the stack below
+        rc = ensure_aux(ctx);
+        if (!rc) {
+          cudaEventRecord(ctx->aev[0], ctx->stream);
+          cudaStreamWaitEvent(ctx->aux_stream, ctx->aev[0], 0);
+          cudaStream_t main_stream = ctx->stream;
+          ctx->stream = ctx->aux_stream;
+          rc = tsqr_finish_pair(ctx, leaves_a, leaves_b, ra, rb);
+          ctx->stream = main_stream;
+          cudaEventRecord(ctx->aev[1], ctx->aux_stream);
+          trees_on_aux = true;
+        }
+      } else if (!rc) {
+        rc = tsqr_finish_pair(ctx, leaves_a, leaves_b, ra, rb);
+      }
     } else {
       rc = figaro_tsqr_dev(ctx, fb, rb, false);
     }
@@ -434,10 +472,12 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
         ng, m1, m2, heads);
     JQ_CHECK_LAUNCH(ctx);
     int rc = tsqr_dense_dev(ctx, heads, ng, n, rh, false);
+    join_trees();
     if (rc) { ctx->record_tsqr_events = true; return rc; }
   } else {
     JQ_CUDA(cudaMemsetAsync(rh, 0, n * n * 8, ctx->stream));
   }
+  join_trees();
   if (getenv("JQ_DEBUG_FOOTNOTE")) {
     cudaStreamSynchronize(ctx->stream);
     auto nan_count = [&](const double* d, int64_t cnt) {
