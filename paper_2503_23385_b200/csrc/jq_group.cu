@@ -65,18 +65,37 @@ __global__ void scan_reduce_kernel(const int64_t* __restrict__ in, int64_t n, co
   if (threadIdx.x == 0) partial[blockIdx.x] = tot;
 }
 
+// In-place exclusive scan of c[0 .. nt) by ONE block of SCAN_THREADS threads; returns the
+// total.  Rounds of SCAN_TILE values, SCAN_ITEMS consecutive values per thread loaded
+// together (one global round trip per 2048 values instead of per 256).  Integer: the
+// result does not depend on the association.
+__device__ __forceinline__ int64_t block_scan_inplace(int64_t* c, int64_t nt, int64_t* ws, int64_t* tot) {
+  int64_t carry = 0;
+  for (int64_t b0 = 0; b0 < nt; b0 += SCAN_TILE) {
+    const int64_t i0 = b0 + (int64_t)threadIdx.x * SCAN_ITEMS;
+    int64_t v[SCAN_ITEMS], sum = 0;
+#pragma unroll
+    for (int u = 0; u < SCAN_ITEMS; ++u) {
+      v[u] = i0 + u < nt ? c[i0 + u] : 0;
+      sum += v[u];
+    }
+    int64_t run = carry + block_exclusive_scan(sum, ws, tot);
+#pragma unroll
+    for (int u = 0; u < SCAN_ITEMS; ++u)
+      if (i0 + u < nt) {
+        c[i0 + u] = run;
+        run += v[u];
+      }
+    carry += *tot;
+    __syncthreads();
+  }
+  return carry;
+}
+
 __global__ void scan_partials_kernel(int64_t* partial, int64_t nb) {
   __shared__ int64_t ws[SCAN_THREADS / 32];
   __shared__ int64_t tot;
-  int64_t carry = 0;
-  for (int64_t b0 = 0; b0 < nb; b0 += SCAN_THREADS) {
-    int64_t i = b0 + threadIdx.x;
-    int64_t v = i < nb ? partial[i] : 0;
-    int64_t ex = block_exclusive_scan(v, ws, &tot);
-    if (i < nb) partial[i] = carry + ex;
-    carry += tot;
-    __syncthreads();
-  }
+  const int64_t carry = block_scan_inplace(partial, nb, ws, &tot);
   if (threadIdx.x == 0) partial[nb] = carry;
 }
 
@@ -240,15 +259,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) run_offsets_kernel(int64_t* cnt,
   for (int side = 0; side < 2; ++side) {
     int64_t* c = cnt + (side ? tiles0 : 0);
     const int64_t nt = side ? tiles1 : tiles0;
-    int64_t carry = 0;
-    for (int64_t b0 = 0; b0 < nt; b0 += SCAN_THREADS) {
-      const int64_t i = b0 + threadIdx.x;
-      const int64_t v = i < nt ? c[i] : 0;
-      const int64_t ex = block_exclusive_scan(v, ws, &tot);
-      if (i < nt) c[i] = carry + ex;
-      carry += tot;
-      __syncthreads();
-    }
+    const int64_t carry = block_scan_inplace(c, nt, ws, &tot);
     if (threadIdx.x == 0) nr[side] = carry;
   }
 }
