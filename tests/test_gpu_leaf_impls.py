@@ -78,3 +78,13 @@ def test_svd_generic_cluster_kernel_parity():
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "svd"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_footnote_serial_trees_parity():
+    # JQ_FOOTNOTE_SERIAL_TREES=1: the keyed footnote's side trees on the main stream
+    e = dict(os.environ, JQ_FOOTNOTE_SERIAL_TREES="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", "figaro"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
