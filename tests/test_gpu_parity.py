@@ -189,7 +189,9 @@ def variant(request, P):
     (5000, 1, 4000, 3, 700), (6000, 8, 5000, 9, 40), (9000, 16, 7000, 1, 5),
     # N = 128 direct-load leaves on keyed joins: group starts inside chunks, rows
     # without a partner group
-    (9000, 70, 8000, 58, 900), (20000, 128, 3000, 128, 17)])
+    (9000, 70, 8000, 58, 900), (20000, 128, 3000, 128, 17),
+    # N = 128 leaves with fewer rows than one chunk / a leaf, and single rows
+    (3, 100, 2, 120, None), (130, 64, 7, 64, None), (1, 128, 200, 128, None), (145, 65, 1, 63, 2)])
 def test_figaro_r_matches_oracle(P, variant, m1, n1, m2, n2, groups):
     rng = np.random.default_rng(m1 + 3 * m2 + n1 + (groups or 0))
     a, b = rand_tables(rng, m1, n1, m2, n2, groups)
