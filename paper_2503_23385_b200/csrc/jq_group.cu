@@ -21,7 +21,7 @@ namespace jq {
 
 // ------------------------------------------------------------------ scan (int64)
 constexpr int SCAN_THREADS = 256;
-constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_ITEMS = 8;  // (load_keys8 and the run-id stores assume 8)
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
 __device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* warp_sums, int64_t* total) {
@@ -223,6 +223,26 @@ __device__ __forceinline__ void run_tile(const RunSides& rs, int64_t& t, int& si
   i0 = t * SCAN_TILE;
   i1 = min(rs.m[side], i0 + SCAN_TILE);
 }
+// the thread's SCAN_ITEMS consecutive keys k[b .. b+7] (0 past i1) and the key before
+// them: 16-byte loads when the key array is 16-byte aligned and the 8 keys are whole
+// (4 LDG.128 + 1 LDG.64 instead of 16 LDG.64)
+__device__ __forceinline__ void load_keys8(const int64_t* __restrict__ k, int64_t b, int64_t i1, int64_t (&key)[SCAN_ITEMS],
+                                           int64_t& prev) {
+  prev = b > 0 && b - 1 < i1 ? __ldg(k + b - 1) : 0;
+  if (((reinterpret_cast<uintptr_t>(k) & 15) == 0) && b + SCAN_ITEMS <= i1) {
+    const longlong2* k2 = reinterpret_cast<const longlong2*>(k + b);
+#pragma unroll
+    for (int u = 0; u < SCAN_ITEMS / 2; ++u) {
+      const longlong2 v = __ldg(k2 + u);
+      key[2 * u] = v.x;
+      key[2 * u + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < SCAN_ITEMS; ++u) key[u] = b + u < i1 ? __ldg(k + b + u) : 0;
+  }
+}
+
 // heads per tile + the sortedness check (unsorted keys raise)
 __global__ void __launch_bounds__(SCAN_THREADS) run_count_kernel(RunSides rs) {
   __shared__ int64_t ws[SCAN_THREADS / 32];
@@ -234,14 +254,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) run_count_kernel(RunSides rs) {
   int64_t h = 0;
   int bad = 0;
   const int64_t b = i0 + threadIdx.x * SCAN_ITEMS;
+  int64_t key[SCAN_ITEMS], prev;
+  load_keys8(k, b, i1, key, prev);
 #pragma unroll
   for (int u = 0; u < SCAN_ITEMS; ++u) {
     const int64_t i = b + u;
     if (i < i1) {
-      const int64_t ki = __ldg(k + i);
+      const int64_t ki = key[u];
       if (i == 0) h += 1;
       else {
-        const int64_t kp = __ldg(k + i - 1);
+        const int64_t kp = u == 0 ? prev : key[u - 1];
         h += ki != kp;
         bad |= kp > ki;
       }
@@ -272,24 +294,25 @@ __global__ void __launch_bounds__(SCAN_THREADS) run_tables_fused_kernel(RunSides
   run_tile(rs, t, side, i0, i1);
   const int64_t* k = rs.k[side];
   const int64_t b = i0 + threadIdx.x * SCAN_ITEMS;
-  int64_t key[SCAN_ITEMS];
+  int64_t key[SCAN_ITEMS], prev;
   int hd[SCAN_ITEMS];
   int64_t h = 0;
+  load_keys8(k, b, i1, key, prev);
 #pragma unroll
   for (int u = 0; u < SCAN_ITEMS; ++u) {
     const int64_t i = b + u;
     hd[u] = 0;
-    key[u] = 0;
     if (i < i1) {
-      key[u] = __ldg(k + i);
-      hd[u] = (i == 0 || __ldg(k + i - 1) != key[u]) ? 1 : 0;
+      hd[u] = (i == 0 || (u == 0 ? prev : key[u - 1]) != key[u]) ? 1 : 0;
       h += hd[u];
     }
   }
   int64_t run = rs.cnt[blockIdx.x] + block_exclusive_scan(h, ws, &tot);  // heads before this thread
+  int32_t rid[SCAN_ITEMS];
 #pragma unroll
   for (int u = 0; u < SCAN_ITEMS; ++u) {
     const int64_t i = b + u;
+    rid[u] = 0;
     if (i < i1) {
       if (hd[u]) {
         rs.rs[side][run] = i;
@@ -297,8 +320,17 @@ __global__ void __launch_bounds__(SCAN_THREADS) run_tables_fused_kernel(RunSides
         if (side) rs.r_to_g_b[run] = -1;
         ++run;
       }
-      rs.runid[side][i] = (int32_t)(run - 1);
+      rid[u] = (int32_t)(run - 1);
     }
+  }
+  int32_t* out = rs.runid[side] + b;
+  if (((reinterpret_cast<uintptr_t>(out) & 15) == 0) && b + SCAN_ITEMS <= i1) {  // two 16-byte stores
+    reinterpret_cast<int4*>(out)[0] = make_int4(rid[0], rid[1], rid[2], rid[3]);
+    reinterpret_cast<int4*>(out)[1] = make_int4(rid[4], rid[5], rid[6], rid[7]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < SCAN_ITEMS; ++u)
+      if (b + u < i1) out[u] = rid[u];
   }
 }
 
