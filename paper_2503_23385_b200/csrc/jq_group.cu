@@ -334,12 +334,27 @@ __global__ void __launch_bounds__(SCAN_THREADS) run_tables_fused_kernel(RunSides
   }
 }
 
+// gid[i] = run_to_group[runid[i]] for both sides, four rows per thread (16-byte loads and
+// stores; the run ids and gid arrays are workspace allocations, 256-byte aligned)
+__device__ __forceinline__ void row_gid_side(const int32_t* __restrict__ runid, int64_t m,
+                                             const int32_t* __restrict__ r_to_g, int32_t* __restrict__ gid,
+                                             int64_t q) {
+  const int64_t i = 4 * q;
+  if (i + 4 <= m) {
+    const int4 r = __ldg(reinterpret_cast<const int4*>(runid + i));
+    reinterpret_cast<int4*>(gid + i)[0] = make_int4(__ldg(r_to_g + r.x), __ldg(r_to_g + r.y), __ldg(r_to_g + r.z),
+                                                    __ldg(r_to_g + r.w));
+  } else {
+    for (int64_t j = i; j < m; ++j) gid[j] = r_to_g[runid[j]];
+  }
+}
 __global__ void row_gid2_kernel(const int32_t* __restrict__ runid_a, int64_t m1, const int32_t* __restrict__ ra_to_g,
                                 int32_t* __restrict__ gid_a, const int32_t* __restrict__ runid_b, int64_t m2,
                                 const int32_t* __restrict__ rb_to_g, int32_t* __restrict__ gid_b) {
-  GRID_STRIDE(i, m1 + m2) {
-    if (i < m1) gid_a[i] = ra_to_g[runid_a[i]];
-    else gid_b[i - m1] = rb_to_g[runid_b[i - m1]];
+  const int64_t qa = (m1 + 3) / 4, qb = (m2 + 3) / 4;
+  GRID_STRIDE(q, qa + qb) {
+    if (q < qa) row_gid_side(runid_a, m1, ra_to_g, gid_a, q);
+    else row_gid_side(runid_b, m2, rb_to_g, gid_b, q - qa);
   }
 }
 
@@ -440,8 +455,8 @@ int group_keys_dev(jq_ctx* ctx, const int64_t* ka, int64_t m1, const int64_t* kb
   JQ_TRY(scan_i64_dev(ctx, rowcnt, cap, ng_dev, g->red_off));
   finish_counts_kernel<<<1, 32, 0, ctx->stream>>>(gidx, nra, g->red_off, g->d_n);
   JQ_CHECK_LAUNCH(ctx);
-  row_gid2_kernel<<<gridn(m1 + m2), 256, 0, ctx->stream>>>(runid_a, m1, ra_to_g, g->gid_a, runid_b, m2, rb_to_g,
-                                                          g->gid_b);
+  row_gid2_kernel<<<gridn((m1 + 3) / 4 + (m2 + 3) / 4), 256, 0, ctx->stream>>>(runid_a, m1, ra_to_g, g->gid_a,
+                                                                               runid_b, m2, rb_to_g, g->gid_b);
   JQ_CHECK_LAUNCH(ctx);
   return JQ_OK;
 }
