@@ -123,15 +123,16 @@ static size_t figaro_ws(int64_t m1, int64_t n1, int64_t m2, int64_t n2, bool key
 __global__ void head_rows_kernel(const double* __restrict__ totA, int n1, const double* __restrict__ totB, int n2,
                                  const int64_t* __restrict__ a_count, const int64_t* __restrict__ b_count,
                                  int64_t ng, int64_t m1_all, int64_t m2_all, double* __restrict__ out) {
-  const int n = n1 + n2;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < ng * n;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = idx / n;
-    const int c = (int)(idx - g * n);
+  // one warp per head row (grid-stride), lanes over the columns: the row's two scales once
+  // per row, coalesced stores
+  const int n = n1 + n2, lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < ng; g += nw) {
     const double m1g = a_count ? (double)a_count[g] : (double)m1_all;
     const double m2g = b_count ? (double)b_count[g] : (double)m2_all;
-    out[idx] = c < n1 ? sqrt(m2g) * (totA[g * n1 + c] / sqrt(m1g))
-                      : sqrt(m1g) * (totB[g * n2 + (c - n1)] / sqrt(m2g));
+    const double sa = sqrt(m2g) / sqrt(m1g), sb = sqrt(m1g) / sqrt(m2g);
+    double* row = out + g * n;
+    for (int c = lane; c < n; c += 32) row[c] = c < n1 ? totA[g * n1 + c] * sa : totB[g * n2 + (c - n1)] * sb;
   }
 }
 
@@ -455,7 +456,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   stage_event(ctx, 4);
   if (ng <= FOOTNOTE_GIVENS_MAX_HEADS) {
     if (ng > 0) {
-      head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng * n, 256), 4096), 256, 0, ctx->stream>>>(
+      head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng, 8), 4096), 256, 0, ctx->stream>>>(
           sa.totals, (int)n1, sb.totals, (int)n2, keyed ? gr.a_count : nullptr, keyed ? gr.b_count : nullptr,
           ng, m1, m2, heads);
       JQ_CHECK_LAUNCH(ctx);
@@ -467,7 +468,7 @@ static int figaro_r_footnote_dev(jq_ctx* ctx, const double* a, int64_t m1, int64
   }
   // head rows (G x n) -> R_H, then [blockdiag(R_A, R_B); R_H] -> canonical R
   if (ng > 0) {
-    head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng * n, 256), 4096), 256, 0, ctx->stream>>>(
+    head_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng, 8), 4096), 256, 0, ctx->stream>>>(
         sa.totals, (int)n1, sb.totals, (int)n2, keyed ? gr.a_count : nullptr, keyed ? gr.b_count : nullptr,
         ng, m1, m2, heads);
     JQ_CHECK_LAUNCH(ctx);
