@@ -330,10 +330,14 @@ def main():
             return P.figaro_r(P.Table(A, ka), P.Table(B, kb))
         from paper_2503_23385_b200 import sharded
         if keyed_sharded:   # one all-gather (interior R, split-part R's and sums) over NCCL
-            return sharded.figaro_r_sharded_join(A, ka, B, kb, plan)
-        if N.get_variant() == "footnote":
-            return sharded.figaro_r_sharded_local(A, B, m, m, a0, a0)  # one all-gather (R + sums) over NCCL
-        return sharded.figaro_r_sharded(A, B, m, m, a0, a0)   # carry + R all-gathers over NCCL
+            r = sharded.figaro_r_sharded_join(A, ka, B, kb, plan)
+        elif N.get_variant() == "footnote":
+            r = sharded.figaro_r_sharded_local(A, B, m, m, a0, a0)  # one all-gather (R + sums) over NCCL
+        else:
+            r = sharded.figaro_r_sharded(A, B, m, m, a0, a0)   # carry + R all-gathers over NCCL
+        if cfg.get("want_v"):   # sigma and V of the (replicated) R on every rank, inside the step
+            return P.svd_of_r(r, want_vectors=True).values
+        return r
 
     def timed(variant, steps):
         N.set_variant(variant)
@@ -621,8 +625,9 @@ def run_e2e_sharded(args, A, B, m, a0, jrows, world, device):
     max over ranks."""
     import torch
     import torch.distributed as dist
-    from paper_2503_23385_b200 import sharded
+    from paper_2503_23385_b200 import sharded, svd
     from paper_2503_23385_b200 import _native as N
+    want_v = bool(CONFIGS[args.config].get("want_v"))
     N.use_torch_stream(A)
     if N.get_variant() == "footnote":
         r_ref = sharded.figaro_r_sharded_local(A, B, m, m, a0, a0).cpu().numpy()
@@ -642,6 +647,9 @@ def run_e2e_sharded(args, A, B, m, a0, jrows, world, device):
                 r = sharded.figaro_r_sharded_local(A, B, m, m, a0, a0)
             else:
                 r = sharded.figaro_r_sharded(A, B, m, m, a0, a0)
+            if want_v:   # sigma and V of the replicated R, inside the step (read back with R)
+                sv = svd.svd_of_r(r, want_vectors=True)
+                sv.values.cpu(), sv.right_vectors.cpu()
             return r.cpu()
 
         step()                                   # warm-up
@@ -663,7 +671,7 @@ def run_e2e_sharded(args, A, B, m, a0, jrows, world, device):
         ms = float(t.item())
         return {"value": jrows / (ms / 1e3), "unit": "join rows/s", "ms_per_step": ms, "steps": nsteps,
                 "h2d_bytes_per_step": int(host["A"][0].nbytes + host["B"][0].nbytes),
-                "d2h_bytes_per_step": int(r.numpy().nbytes),
+                "d2h_bytes_per_step": int(r.numpy().nbytes) + (8 * (r.shape[0] + r.shape[0] ** 2) if want_v else 0),
                 "per_rank": True, "pinned": bool(host["A"][1] and host["B"][1]),
                 "parity": {"max_rel_err_vs_device_path": err, "bar": 1e-12, "ok": err <= 1e-12,
                            "rank": int(os.environ.get("RANK", "0"))},
