@@ -887,7 +887,7 @@ struct FigaroSrc {
       // packed per-row coefficients of the branch-free passes: out = c1 x - c2 S and
       // S <- keep S + w x (group start: keep 0, w 1; tail row: 1, 1; no row: 1, 0) --
       // exactly the selects of the row mode (multiplications by 0 / 1 are exact)
-      *reinterpret_cast<double4*>(scratch + 3 * C::K + 4 * i) =
+      *reinterpret_cast<double4*>(scratch + 4 * i) =
           make_double4(a1, a2, md == 1 ? 0.0 : 1.0, md == 0 ? 0.0 : 1.0);
       (void)imode;
     }
@@ -903,7 +903,7 @@ struct FigaroSrc {
     const int n2 = (int)fa.n2;
     const int e = min(i1, nrows);
     const int L = (i1 - i0 + SEG_SUB - 1) / SEG_SUB;
-    const double4* cf = reinterpret_cast<const double4*>(scratch + 3 * C::K);
+    const double4* cf = reinterpret_cast<const double4*>(scratch);
     int cnt[SEG_SUB];
 #pragma unroll
     for (int u = 0; u < SEG_SUB; ++u) cnt[u] = max(0, min(L, e - (i0 + u * L)));
@@ -975,7 +975,7 @@ struct FigaroSrc {
     const int n2 = (int)fa.n2;
     const int e = min(i1, nrows);
     const int L = (i1 - i0 + SEG_SUB - 1) / SEG_SUB;
-    const double4* cf = reinterpret_cast<const double4*>(scratch + 3 * C::K);
+    const double4* cf = reinterpret_cast<const double4*>(scratch);
     int cnt[SEG_SUB];
 #pragma unroll
     for (int u = 0; u < SEG_SUB; ++u) cnt[u] = max(0, min(L, e - (i0 + u * L)));
@@ -2165,17 +2165,32 @@ static int ws128_cfg() {
   return c;
 }
 
+// N = 32 warp-specialised leaf: 12 data warps x 40 rows (480-row chunks; C3 TSQR 5.46 vs
+// 5.82 ms for 384-row chunks, the chain's per-panel cost over more rows) by default;
+// JQ_TSQR_WS32=kw32: x 32 rows (A/B).
+static int ws32_cfg() {
+  static const int c = [] {
+    const char* e = getenv("JQ_TSQR_WS32");
+    return (e && strcmp(e, "kw32") == 0) ? 1 : 0;
+  }();
+  return c;
+}
+
 template <class Src>
 static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
                            bool canonical, double* r_out, int use_tma, LeafSet* defer = nullptr) {
   switch (np_for(n)) {
     case 16:
+      // (12 x 64-row data warps measured the same at C2: 0.638 ms either way)
       if (leaf_impl() == 0)
         return run_stream_ws<CfgS<16, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
       return run_stream<Cfg<16>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 32:
-      if (leaf_impl() == 0)
-        return run_stream_ws<CfgS<32, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
+      if (leaf_impl() == 0) {
+        if (ws32_cfg() == 1)
+          return run_stream_ws<CfgS<32, 16, 12, 1, 32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
+        return run_stream_ws<CfgS<32, 16, 12, 1, 40>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
+      }
       return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 64:
       // (8 warps with 6 data warps x 40 rows -- 240-row chunks, 255 registers -- measured

@@ -62,8 +62,9 @@ struct CfgS {
   static constexpr int OFF_P = OFF_SC + 8;                // [2][DW][8]
   static constexpr int OFF_LD = OFF_U + (80 + 2 * DW * 8 > 16 * LDT + 48 ? 80 + 2 * DW * 8 : 16 * LDT + 48);
   // ^ loader per-row scalars (past the partials [2][DW][8] and factor_panel_chol's scratch): c1, c2, mode [3][K], then
-  // the multi-loader transform's packed {c1, c2, keep, w} per row [K][4]
-  static constexpr int OFF_S = OFF_LD + (NP <= 32 ? 7 : 3) * K;  // loader running prefix (the packed
+  // the multi-loader transform's packed {c1, c2, keep, w} per row [K][4] (B-part chunks; it
+  // aliases the scalars, which only A-part chunks use)
+  static constexpr int OFF_S = OFF_LD + (NP <= 32 ? 4 : 3) * K;  // loader running prefix (the packed
   // coefficients are only used by the multi-loader transform, NP <= 32)
   static constexpr int OFF_FLAG = OFF_S + NP;             // [2] chain accepted, by parity
   static constexpr int OFF_GP = OFF_FLAG + 2;             // [DW][64] C^T C partials of the next tile (ws2)
@@ -79,8 +80,8 @@ struct CfgS {
   static_assert(SMEM <= (MIN_CTAS == 1 ? 227 : 113) * 1024, "shared memory per CTA");
   static_assert(NP <= 128, "loader transform assumes <= 128 columns per side");
   static_assert(OFF_LD - OFF_U >= 16 * LDT + 16 + 32, "factor_panel_chol scratch (U .. P)");
-  static_assert((OFF_LD + 3 * K) % 2 == 0, "16-byte aligned packed loader coefficients");
-  static_assert(NP <= 32 || NLOAD <= 1, "the packed loader coefficients need the 7 K scratch");
+  static_assert(OFF_LD % 2 == 0, "16-byte aligned packed loader coefficients");
+  static_assert(NP <= 32 || NLOAD <= 1, "the packed loader coefficients need the 4 K scratch");
   static_assert(NLT * DW * 32 + 2 * DW * NP <= DW * NLT * 64, "direct load: lo and wt inside the partials");
 };
 
