@@ -2079,7 +2079,8 @@ static int run_stream(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t ali
   return JQ_OK;
 }
 
-// Leaf kernel for NP <= 128: warp-specialised tsqr_ws2_kernel (default) or the CTA-wide
+// Leaf kernel for NP <= 128: warp-specialised tsqr_ws2_kernel (default; direct loads for
+// NP = 64 / 128, a staged loader warp for NP <= 32) or the CTA-wide
 // tsqr_kernel (JQ_TSQR_IMPL=cta, for A/B timing and tests); NP = 256 always CTA-wide.
 static int leaf_impl() {
   static const int w = [] {
@@ -2176,6 +2177,15 @@ static int ws32_cfg() {
   return c;
 }
 
+// N = 64: JQ_TSQR_WS64=staged -- the 16-warp leaf with a loader warp (A/B, tests)
+static bool ws64_staged() {
+  static const bool on = [] {
+    const char* e = getenv("JQ_TSQR_WS64");
+    return e && strcmp(e, "staged") == 0;
+  }();
+  return on;
+}
+
 template <class Src>
 static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t align, int n,
                            bool canonical, double* r_out, int use_tma, LeafSet* defer = nullptr) {
@@ -2193,8 +2203,16 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
       }
       return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 64:
-      // (8 warps with 6 data warps x 40 rows -- 240-row chunks, 255 registers -- measured
-      // slower at C4: 155.9 vs 144.3 ms)
+      // default: warp-specialised with direct loads, 8 warps (255 registers), 6 data warps x
+      // 48 rows (288-row chunks; C4 132.3 vs 144.3 ms for the staged 16-warp leaf: the chain
+      // alone on SMSP 0 and 1.5x the rows per panel chain).  JQ_TSQR_WS64=staged: the 16-warp
+      // leaf with the loader warp (12 data warps x 16 rows).  (A staged 8-warp leaf with 6 x 40
+      // rows was slower: 155.9 ms.)
+      if constexpr (Src::DIRECT) {
+        if (leaf_impl() == 0 && !ws64_staged())
+          return run_stream_ws<CfgS<64, 8, 6, 1, 48, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
+                                                            defer);
+      }
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
       return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 128:
