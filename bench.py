@@ -408,8 +408,8 @@ def main():
             kname = ("tsqr_ws2_kernel (warp-specialised TSQR leaf: loader warps build the Claim-1 / tail rows, "
                      "chain warp runs the Cholesky panel factorisation, 12 data warps do the DMMA updates)")
         elif leaf_n <= 64:
-            kname = ("tsqr_ws2_kernel<CfgS<64,8,6,1,48,direct>> (warp-specialised TSQR leaf: 6 data warps load "
-                     "their 48 rows straight into the DMMA layout and run the tail transform there, chain warp "
+            kname = ("tsqr_ws2_kernel<CfgS<64,16,12,1,24,direct>> (warp-specialised TSQR leaf: 12 data warps load "
+                     "their 24 rows straight into the DMMA layout and run the tail transform there, chain warp "
                      "alone on SM sub-partition 0 runs the Cholesky panel factorisation)")
         elif leaf_n <= 128:
             kname = ("tsqr_ws2_kernel<CfgS<128,8,6,1,24,direct>> (warp-specialised TSQR leaf: 6 data warps load "

@@ -2177,6 +2177,14 @@ static int ws32_cfg() {
   return c;
 }
 
+// N = 64: JQ_TSQR_WS64=w8 -- direct loads with 8 warps, 6 data warps x 48 rows (A/B)
+static bool ws64_w8() {
+  static const bool on = [] {
+    const char* e = getenv("JQ_TSQR_WS64");
+    return e && strcmp(e, "w8") == 0;
+  }();
+  return on;
+}
 // N = 64: JQ_TSQR_WS64=staged -- the 16-warp leaf with a loader warp (A/B, tests)
 static bool ws64_staged() {
   static const bool on = [] {
@@ -2203,15 +2211,19 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
       }
       return run_stream<Cfg<32>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
     case 64:
-      // default: warp-specialised with direct loads, 8 warps (255 registers), 6 data warps x
-      // 48 rows (288-row chunks; C4 132.3 vs 144.3 ms for the staged 16-warp leaf: the chain
-      // alone on SMSP 0 and 1.5x the rows per panel chain).  JQ_TSQR_WS64=staged: the 16-warp
-      // leaf with the loader warp (12 data warps x 16 rows).  (A staged 8-warp leaf with 6 x 40
-      // rows was slower: 155.9 ms.)
+      // default: warp-specialised with direct loads, 16 warps (128 registers), 12 data warps x
+      // 24 rows (288-row chunks; C4 127.4 ms vs 144.3 for the staged 16-warp leaf -- the chain
+      // alone on SMSP 0 and 1.5x the rows per panel chain -- and 131.9 for 8 warps with 6 x 48
+      // rows, JQ_TSQR_WS64=w8: four data warps per SMSP hide the DMMA latency better).
+      // JQ_TSQR_WS64=staged: the staged leaf with the loader warp (12 data warps x 16 rows).
+      // (A staged 8-warp leaf with 6 x 40 rows was slower: 155.9 ms.)
       if constexpr (Src::DIRECT) {
-        if (leaf_impl() == 0 && !ws64_staged())
+        if (leaf_impl() == 0 && ws64_w8())
           return run_stream_ws<CfgS<64, 8, 6, 1, 48, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
                                                             defer);
+        if (leaf_impl() == 0 && !ws64_staged())
+          return run_stream_ws<CfgS<64, 16, 12, 1, 24, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
+                                                              defer);
       }
       if (leaf_impl() == 0) return run_stream_ws<CfgS<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
       return run_stream<Cfg<64>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);
