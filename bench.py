@@ -44,11 +44,11 @@ CONFIGS = {
 }
 METRIC = "join rows/sec (m1*m2/t), time-to-R"
 # dram__bytes_read.sum + dram__bytes_write.sum per leaf-kernel launch (ncu --set full)
-NCU_TRAFFIC = {(4, "footnote"): {"bytes": 53.038299e9 + 89.34016e6,
-                                 "note": "first tsqr_ws2_kernel<CfgS<64,8,6,1,48,direct>> launch (side A, carry-free "
-                                         "leaves; profiles/r02_ncu_ws64d_c4.md / _raw.csv, 65.66 ms under ncu): its own "
-                                         "1e8 x 64 f64 rows = 51.2e9 algorithmic bytes (+3.6 %: the direct loads "
-                                         "re-fetch a little of what the L2 prefetch brought in)"},
+NCU_TRAFFIC = {(4, "footnote"): {"bytes": 53.184211e9 + 381.695744e6,
+                                 "note": "first tsqr_ws2_kernel<CfgS<64,16,12,1,24,direct>> launch (side A, carry-free "
+                                         "leaves; profiles/r02_ncu_ws64d_c4.md / _raw.csv, 63.63 ms under ncu): its own "
+                                         "1e8 x 64 f64 rows = 51.2e9 algorithmic bytes (+3.9 %: the direct loads "
+                                         "re-fetch a little of what the L2 prefetch brought in; writes: R and spills)"},
                (5, "footnote"): {"bytes": 1.065093e9 + 6.2784e6,
                                  "note": "first tsqr_ws2_kernel<CfgS<128,8,6,1,24,direct>> launch (side A, carry-free "
                                          "leaves; profiles/r02_ncu_ws128_c5.md, 2.525 ms under ncu): its own 1e6 x 128 "
