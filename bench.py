@@ -412,8 +412,8 @@ def main():
                      "their 24 rows straight into the DMMA layout and run the tail transform there, chain warp "
                      "alone on SM sub-partition 0 runs the Cholesky panel factorisation)")
         elif leaf_n <= 128:
-            kname = ("tsqr_ws2_kernel<CfgS<128,8,6,1,24,direct>> (warp-specialised TSQR leaf: 6 data warps load "
-                     "their 24 rows straight into the DMMA layout and run the tail transform there, chain warp "
+            kname = ("tsqr_ws2_kernel<CfgS<128,12,9,1,16,direct>> (warp-specialised TSQR leaf: 9 data warps load "
+                     "their 16 rows straight into the DMMA layout and run the tail transform there, chain warp "
                      "alone on SM sub-partition 0)")
         else:
             kname = "tsqr_kernel (CTA-wide TSQR leaf, Cholesky / Gram panel chain + explicit fallback, DMMA updates)"

@@ -2154,14 +2154,15 @@ static int run_stream_ws(jq_ctx* ctx, const Src& src_in, int64_t vrows, int64_t 
   return JQ_OK;
 }
 
-// NP = 128 warp-specialised leaf: 8 warps (255 registers), 6 data warps x 24 rows
-// (144-row chunks) by default; JQ_TSQR_WS128=kw16: x 16 rows (C5 TSQR 6.93 vs 6.00 ms,
-// dense C4 828 vs 686 ms: the chain's per-panel cost over fewer rows).  (16 warps with
-// 12 data warps x 8 rows at 128 registers: 7.02 ms.)
+// NP = 128 warp-specialised leaf: 12 warps (168 registers), 9 data warps x 16 rows (144-row
+// chunks, three data warps per SM sub-partition: C5 TSQR 5.86 ms, dense C4 642 ms) by default;
+// JQ_TSQR_WS128=kw24: 8 warps, 6 data warps x 24 rows (5.93 / 691 ms); =kw16: 8 warps, 6 x 16
+// rows (6.93 / 828 ms: the chain's per-panel cost over fewer rows).  (16 warps with 12 data
+// warps x 8 rows at 128 registers: 7.02 ms.)
 static int ws128_cfg() {
   static const int c = [] {
     const char* e = getenv("JQ_TSQR_WS128");
-    return (e && strcmp(e, "kw16") == 0) ? 1 : 0;
+    return (e && strcmp(e, "kw16") == 0) ? 1 : (e && strcmp(e, "kw24") == 0) ? 2 : 0;
   }();
   return c;
 }
@@ -2236,8 +2237,11 @@ static int dispatch_stream(jq_ctx* ctx, const Src& src, int64_t vrows, int64_t a
           if (ws128_cfg() == 1)
             return run_stream_ws<CfgS<128, 8, 6, 1, 16, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
                                                                defer);
-          return run_stream_ws<CfgS<128, 8, 6, 1, 24, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
-                                                             defer);
+          if (ws128_cfg() == 2)
+            return run_stream_ws<CfgS<128, 8, 6, 1, 24, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
+                                                               defer);
+          return run_stream_ws<CfgS<128, 12, 9, 1, 16, true>>(ctx, src, vrows, align, n, canonical, r_out, use_tma,
+                                                              defer);
         }
       }
       return run_stream<Cfg<128>>(ctx, src, vrows, align, n, canonical, r_out, use_tma, defer);

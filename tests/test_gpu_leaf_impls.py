@@ -17,12 +17,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                  {"JQ_TSQR_IMPL": "cta", "JQ_TSQR_EXPLICIT": "1"},
                                  {"JQ_TSQR_DEBUG": "8"}, {"JQ_TSQR_CHAIN": "householder"},
                                  {"JQ_TSQR_CHAIN": "householder", "JQ_TSQR_IMPL": "cta"},
-                                 {"JQ_TSQR_REDUCERS": "1"}, {"JQ_TSQR_WS128": "kw16"},
+                                 {"JQ_TSQR_REDUCERS": "1"}, {"JQ_TSQR_WS128": "kw16"}, {"JQ_TSQR_WS128": "kw24"},
                                  {"JQ_TSQR_WS32": "kw32"}, {"JQ_TSQR_WS64": "staged"}, {"JQ_TSQR_WS64": "w8"},
                                  {"JQ_TSQR_WS64": "staged", "JQ_TSQR_CHAIN": "householder"},
                                  {"JQ_TSQR_STAGED": "1"}, {"JQ_TSQR_STAGED": "1", "JQ_TSQR_IMPL": "cta"}],
                          ids=["cta", "ws-explicit", "cta-explicit", "ws-fixed-roles", "ws-reflector-chain",
-                              "cta-reflector-chain", "ws-reducer-warps", "ws-np128-kw16", "ws-np32-kw32", "ws-np64-staged", "ws-np64-w8", "ws-np64-staged-reflector",
+                              "cta-reflector-chain", "ws-reducer-warps", "ws-np128-kw16", "ws-np128-kw24", "ws-np32-kw32", "ws-np64-staged", "ws-np64-w8", "ws-np64-staged-reflector",
                               "staged-tree", "cta-staged"])
 def test_leaf_impl_parity(env):
     e = dict(os.environ, **env)
