@@ -49,10 +49,10 @@ NCU_TRAFFIC = {(4, "footnote"): {"bytes": 53.184211e9 + 381.695744e6,
                                          "leaves; profiles/r02_ncu_ws64d_c4.md / _raw.csv, 63.63 ms under ncu): its own "
                                          "1e8 x 64 f64 rows = 51.2e9 algorithmic bytes (+3.9 %: the direct loads "
                                          "re-fetch a little of what the L2 prefetch brought in; writes: R and spills)"},
-               (5, "footnote"): {"bytes": 1.065093e9 + 6.2784e6,
-                                 "note": "first tsqr_ws2_kernel<CfgS<128,8,6,1,24,direct>> launch (side A, carry-free "
-                                         "leaves; profiles/r02_ncu_ws128_c5.md, 2.525 ms under ncu): its own 1e6 x 128 "
-                                         "f64 rows = 1.024e9 algorithmic bytes (+4 %)"}}
+               (5, "footnote"): {"bytes": 1.061011e9 + 10.555904e6,
+                                 "note": "first tsqr_ws2_kernel<CfgS<128,12,9,1,16,direct>> launch (side A, carry-free "
+                                         "leaves; profiles/r02_ncu_ws128_c5.md, r02_ncu_ws128w12_c5_raw.csv, 2.474 ms "
+                                         "under ncu): its own 1e6 x 128 f64 rows = 1.024e9 algorithmic bytes (+3.6 %)"}}
 
 
 def peaks():
